@@ -1,0 +1,299 @@
+"""Benchmark of the per-time-step collision-resolution path (BASELINE.json metric).
+
+One "step" = one pass of the whole hot path over the
+C5 workload: build_contacts, assemble_D, U_ext = RPY(F_ext), q, and BBPGD for a
+fixed 50 iterations (BASELINE.json configs[4]: 262,144 spheres, volume fraction
+0.3).  All inside one C-ABI call (sc_collision_step) with inputs resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: RPY rows sharded)
+
+Prints ONE JSON line on rank 0.  value = whole-job RPY pair-interactions per
+second (every executed RPY apply counts N(N-1) pairs), device-timed with CUDA
+events on the library's stream, max over ranks.  The reference arm
+(--impl reference) times the CPU oracle (test infrastructure, oracle/) on the
+host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RPY pair-interactions/s and BBPGD iters/s at N spheres, 1/2/4/8 B200, % FP64 peak"
+UNIT = "pair-interactions/s"
+# FP64 peak derived from unit counts and clocks: 148 SMs x 64 FP64 FMA lanes x 2 flop x 1.965 GHz
+# (DESIGN.md "Roofline"); the DFMA microbenchmark measured 34.24 TFLOP/s (profiles/r01/fp64_probe.log).
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+FLOPS_PER_PAIR = 37  # canonical algorithmic FP64 flops per ordered pair
+WORKLOAD = "C5"
+FIXED_ITERS = 50
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, power = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                s = float(f[1])
+                smax = float(f[2])
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            if s > 500:  # under load
+                sm.append(s)
+            for k, nm in enumerate(names):
+                if f[5 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(self.lines),
+                "power_w_max": max(power) if power else None}
+
+
+def cpu_baseline(seconds_target=15.0):
+    """The oracle (as it stands) on the host cores: RPY rows of the C5 workload."""
+    import numpy as np
+
+    import oracle
+    from paper_1909_06623_b200.synthetic import make_problem
+    p = make_problem(WORKLOAD)
+    FT = p.force
+    cores = os.cpu_count() or 1
+    rows = 256
+    t0 = time.perf_counter()
+    oracle.rpy_apply_rows(p.pos, p.radius, p.mu, FT, 0, rows)
+    dt = time.perf_counter() - t0
+    rows2 = int(min(p.n, max(rows, rows * seconds_target / max(dt, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.rpy_apply_rows(p.pos, p.radius, p.mu, FT, 0, rows2)
+    dt2 = time.perf_counter() - t0
+    pairs = rows2 * (p.n - 1)
+    return {"value": pairs / dt2, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"oracle RPY apply (long-double sums), {rows2} target rows x {p.n} sources of {WORKLOAD}, "
+                      f"{dt2:.1f} s, OMP over rows, threads={os.environ.get('OMP_NUM_THREADS', cores)}"}
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the CPU oracle on a bounded sample of the workload (rank 0 only)."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    from paper_1909_06623_b200.synthetic import make_problem
+    p = make_problem(WORKLOAD)
+    rows = 1024
+    cores = os.cpu_count() or 1
+    times = []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.rpy_apply_rows(p.pos, p.radius, p.mu, p.force, 0, rows)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    value = rows * (p.n - 1) / (ms / 1e3)
+    sample = f"oracle RPY apply of {rows} target rows x {p.n} sources of {WORKLOAD} per step"
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": _config(args, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _config(args, world):
+    return {"workload": f"{WORKLOAD}: 262,144 monodisperse spheres a=1, volume fraction 0.3, RPY all-pairs, "
+                        f"F_ext ~ N(0,1)^3, dt=0.005, contacts gap<0.1a, BBPGD BB1 fixed {FIXED_ITERS} iterations",
+            "n_bodies": 262144, "bbpgd_iters": FIXED_ITERS, "parallelism": f"rpy-rows{world}",
+            "l2": "flushed between steps (256 MiB write on the library stream)",
+            "step": "build_contacts+assemble_D+U_ext+q+bbpgd_solve (one sc_collision_step call)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1909_06623_b200 import Context, nccl_unique_id
+    from paper_1909_06623_b200.synthetic import make_problem
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = Context(local, nccl_id=obj[0], rank=rank, world=world)
+    else:
+        ctx = Context(local)
+    dev = torch.device(f"cuda:{local}")
+    p = make_problem(WORKLOAD)
+    pos = torch.as_tensor(p.pos, device=dev)
+    rad = torch.as_tensor(p.radius, device=dev)
+    F = torch.as_tensor(p.force, device=dev)
+    Fc = torch.empty((p.n, 6), dtype=torch.float64, device=dev)
+    Uc = torch.empty((p.n, 6), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = ctx.torch_stream()
+
+    def step(pos_, rad_, F_, Fc_, Uc_):
+        return ctx.collision_step("spheres", pos_, F_, radius=rad_, gap_abs=p.gap_abs, gap_rel=p.gap_rel, mu=p.mu,
+                                  dt=p.dt, tol=p.tol, max_iter=FIXED_ITERS, fixed_iters=True, Fc_out=Fc_, Uc_out=Uc_)
+
+    for _ in range(args.warmup):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        r = step(pos, rad, F, Fc, Uc)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    ctx.set_timing(True)
+    ctx.reset_timing()
+    l0 = ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    sampler.start()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        r = step(pos, rad, F, Fc, Uc)
+    ev1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    launches = ctx.launch_count() - l0
+    tim = ctx.get_timing()
+    ctx.set_timing(False)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    n = p.n
+    pairs_per_apply = n * (n - 1)
+    applies_per_step = 1 + 1 + FIXED_ITERS  # U_ext, alpha_0 MVOP, one per iteration (gamma_0 = 0: Step 2 is free)
+    value = applies_per_step * pairs_per_apply / (ms_step / 1e3)
+    # roofline of the dominant kernel (RPY), live CUDA-event timing on the library stream
+    rpy_ms, rpy_n = tim["rpy"]
+    rows_here = ctx_rows(n, world, rank)
+    rpy_avg_ms = rpy_ms / max(rpy_n, 1)
+    flops_launch = FLOPS_PER_PAIR * rows_here * (n - 1)
+    achieved = flops_launch / (rpy_avg_ms / 1e3) / 1e12
+    roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                "kernel": "rpy_partial_kernel", "avg_launch_ms": rpy_avg_ms, "launches_timed": rpy_n,
+                "peak_note": "FP64 derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (measured DFMA microbench 34.24)"}
+    share = {k: v[0] / max(ms_total, 1e-9) for k, v in tim.items()}
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": _config(args, world),
+           "bbpgd_iters_per_s": FIXED_ITERS / (ms_step / 1e3), "pct_fp64_peak": 100 * roofline["frac"],
+           "n_c": r["nc"], "mvops": r["mvops"], "residual": r["residual"], "roofline": roofline,
+           "kernel_time_share": share, "clocks": clocks, "gpu_launches": launches}
+    # e2e: the same call with HOST (pinned) buffers, copies inside the timed region
+    if not args.no_e2e:
+        hpos = torch.as_tensor(p.pos).pin_memory()
+        hrad = torch.as_tensor(p.radius).pin_memory()
+        hF = torch.as_tensor(p.force).pin_memory()
+        hFc = torch.empty((n, 6), dtype=torch.float64).pin_memory()
+        hUc = torch.empty((n, 6), dtype=torch.float64).pin_memory()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step(hpos, hrad, hF, hFc, hUc)
+        barrier()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = float(te.item())
+        out["e2e"] = {"value": applies_per_step * pairs_per_apply / (e2e_ms / 1e3), "unit": UNIT,
+                      "h2d_bytes_per_step": int(hpos.numel() * 8 + hrad.numel() * 8 + hF.numel() * 8),
+                      "d2h_bytes_per_step": int(hFc.numel() * 8 + hUc.numel() * 8), "ms_per_step": e2e_ms}
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ctx_rows(n, world, rank):
+    from paper_1909_06623_b200 import plan_partition
+    pp = plan_partition(n, world, rank)
+    return pp["row_hi"] - pp["row_lo"]
+
+
+if __name__ == "__main__":
+    main()

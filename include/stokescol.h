@@ -1,0 +1,193 @@
+/* stokescol.h -- C ABI of the B200 collision-resolution library (libstokescol.so).
+ *
+ * The per-time-step collision solve of Yan et al., "A scalable computational
+ * platform for particulate Stokes suspensions" (arXiv 1909.06623), Sec. 3:
+ *   LCP   0 <= gamma  _|_  Phi/dt + D^T (U_ext + M D gamma) >= 0
+ *   CQP   min 1/2 gamma^T (D^T M D) gamma + q^T gamma,  gamma >= 0
+ *   BBPGD Alg. 1
+ * with an all-pairs Rotne-Prager-Yamakawa mobility for spheres
+ * (BASELINE.json configs[0], [1]) or a block-diagonal slender-body drag for
+ * spherocylinders (configs[3]).  "P:Lnnn" = line of /root/reference/PAPER.md.
+ *
+ * Conventions (all entry points):
+ *  - extern "C", no exceptions cross the boundary; every call returns an
+ *    sc_status (>= 0 success, < 0 error; sc_last_error() explains).
+ *  - Pointers may be HOST or DEVICE memory: the library inspects each with
+ *    cudaPointerGetAttributes; host buffers are staged through the context's
+ *    stream (synchronously).  Device buffers are used in place.  The caller
+ *    owns every buffer it passes; the context owns its internal workspaces.
+ *  - All arrays are contiguous, row-major, FP64 unless stated (int32 for
+ *    indices).  Per-body 6-vectors are (Fx,Fy,Fz,Tx,Ty,Tz) /
+ *    (Ux,Uy,Uz,Wx,Wy,Wz).
+ *  - Constraint lists are sorted by (i, j) with i < j in the caller's body
+ *    indices.  The unit normal n points from body j to body i; column l of D
+ *    carries +n (and r_i x n for rods) on i and -n (and -(r_j x n)) on j
+ *    (reading A13).
+ *  - Work is ordered on the context's CUDA stream.  Calls that return host
+ *    scalars (n_c, stats) synchronise that stream.
+ *  - Multi-GPU contexts (sc_create_dist) are collective: every rank makes
+ *    the same sequence of calls with the same full inputs; results are
+ *    bitwise identical to a 1-GPU context.
+ */
+#ifndef STOKESCOL_H
+#define STOKESCOL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sc_ctx sc_ctx;
+
+typedef enum {
+  SC_OK = 0,
+  SC_NOT_CONVERGED = 1, /* soft: outputs valid, the last iterate is returned (reading A7) */
+  SC_EINVAL = -1,       /* NULL/bad sizes, call out of order */
+  SC_EDEGENERATE = -2,  /* coincident centres / zero-length normal (reading A12) */
+  SC_ENONFINITE = -3,   /* NaN/Inf met in a gradient or step (SPEC hard error) */
+  SC_ENOMEM = -4,
+  SC_ECUDA = -5,
+  SC_ENCCL = -6
+} sc_status;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int sc_version(void);
+
+/* ---------------------------------------------------------------- context */
+/* One context per GPU.  device: CUDA ordinal.  stream: a cudaStream_t to
+ * order all work on, or NULL for a context-owned non-blocking stream. */
+int sc_create(sc_ctx** out, int device, void* stream);
+/* Multi-GPU (one process per GPU, NCCL over NVLink): nccl_id is the 128-byte
+ * ncclUniqueId that rank 0 obtained from sc_nccl_unique_id and broadcast to
+ * every rank (e.g. via torch.distributed). */
+int sc_nccl_unique_id(void* out128);
+int sc_create_dist(sc_ctx** out, int device, void* stream, const void* nccl_id, int rank, int world);
+void sc_destroy(sc_ctx* ctx);
+const char* sc_last_error(const sc_ctx* ctx);
+/* The stream the context orders its work on (a cudaStream_t). */
+void* sc_stream(const sc_ctx* ctx);
+
+/* ---------------------------------------------------- (a1) build_contacts */
+/* Spheres.  Stores the bodies in the context and computes the near set
+ * A(C, delta) = { (i,j) : Phi_ij < delta_ij } with
+ *   Phi_ij   = |c_i - c_j| - (a_i + a_j)  (may be negative: overlaps allowed)
+ *   delta_ij = gap_abs + gap_rel * min(a_i, a_j)   (reading A1; strict '<').
+ * pos: n x 3, radius: n (radius == NULL: all radii = 1).  n_c: out, number of
+ * constraints.  The gap and normal are evaluated without FMA contraction so
+ * the set and the values are bit-identical to the plain definition (reading
+ * A20).  Errors: SC_EINVAL (n < 0, NULL pos, gap_rel < 0), SC_EDEGENERATE
+ * (two centres coincide). */
+int sc_build_contacts_spheres(sc_ctx* ctx, int64_t n, const double* pos, const double* radius,
+                              double gap_abs, double gap_rel, int64_t* n_c);
+/* Spherocylinders of radius b: centre, unit axis dir (n x 3), cylinder
+ * length (n).  Phi_ij = (minimal distance of the axis segments) - 2b,
+ * contact iff Phi_ij < gap_thresh.  Also stores the lever arms
+ * r_i = P_i - c_i, r_j = P_j - c_j of the closest points. */
+int sc_build_contacts_rods(sc_ctx* ctx, int64_t n, const double* center, const double* dir,
+                           const double* length, double b, double gap_thresh, int64_t* n_c);
+/* Copy the constraint list out (any pointer may be NULL):
+ * ci, cj: n_c int32; gap: n_c; normal: n_c x 3; lever: n_c x 2 x 3 (rods). */
+int sc_get_contacts(sc_ctx* ctx, int32_t* ci, int32_t* cj, double* gap, double* normal, double* lever);
+
+/* ------------------------------------------------------- (a2) assemble_D */
+/* Builds the column form of D and the body -> constraint
+ * incidence (CSR, sorted by constraint id) used by the atomic-free gather
+ * F = D gamma, plus the fixed chunking of constraints for deterministic
+ * reductions.  Must follow a build_contacts call. */
+int sc_assemble_D(sc_ctx* ctx);
+/* F = D gamma (gamma: n_c; FT: n x 6). */
+int sc_apply_D(sc_ctx* ctx, const double* gamma, double* FT);
+/* out = D^T UW (UW: n x 6; out: n_c) -- the linearised gap rate. */
+int sc_apply_DT(sc_ctx* ctx, const double* UW, double* out);
+
+/* ---------------------------------------------------- (a4) mobility_apply */
+/* UW = Mobility(FT) for the bodies of the last build_contacts call, viscosity mu.
+ * Spheres: U_i = F_i/(6 pi mu a_i) + sum_{j != i} T(r_ij; abar) F_j with the RPY
+ * tensor of BASELINE.json configs[0] (abar = (a_i+a_j)/2, configs[1]), and
+ * W_i = T_i/(8 pi mu a_i^3).  Rods: the 6x6 drag block per body (configs[3]).
+ * FT, UW: n x 6. */
+int sc_mobility_apply(sc_ctx* ctx, double mu, const double* FT, double* UW);
+
+/* -------------------------------------------------- LCP right-hand side q */
+/* q = gap/dt + D^T U_nc.  U_nc: n x 6.  The context keeps q for
+ * sc_bbpgd_solve; q_out (n_c) may be NULL. */
+int sc_lcp_q(sc_ctx* ctx, double dt, const double* U_nc, double* q_out);
+
+/* ------------------------------------------------------ (a6) bbpgd_solve */
+typedef struct {
+  double mu;            /* viscosity used by every MVOP */
+  double tol;           /* absolute tolerance on phi = ||min(gamma, g)||_2 */
+  int32_t max_iter;     /* j_max */
+  int32_t bb_mode;      /* 0 = BB1 (paper default), 1 = BB2, 2 = alternate */
+  int32_t fixed_iters;  /* 1: run exactly max_iter iterations, no early exit (reading A22) */
+  int32_t warm_start;   /* 1: gamma holds gamma_0 on entry; 0: gamma_0 = 0 (reading A3) */
+} sc_bbpgd_opts;
+
+typedef struct {
+  int32_t iters;        /* GD steps j taken */
+  int32_t mvops;        /* evaluations of M x = 2 + iters, 1 if gamma_0 solves */
+  int32_t converged;    /* phi < tol at the returned iterate */
+  int32_t bb_breakdowns;/* steps where s^T y <= 0: previous alpha reused (reading A5) */
+  int32_t active;       /* |A_c| = #{gamma_l > 0} */
+  int32_t reserved;
+  double residual;      /* phi at the returned iterate */
+  double alpha;         /* last BB step length */
+} sc_bbpgd_stats;
+
+/* Solve the CQP for the context's q (from sc_lcp_q).  gamma (n_c): out (in
+ * too if warm_start).  g_out (n_c), Fc_out = D gamma (n x 6) and
+ * Uc_out = Mobility(Fc) (n x 6) may be NULL.  Returns SC_OK, SC_NOT_CONVERGED
+ * or an error; stats may be NULL. */
+int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double* g_out,
+                   double* Fc_out, double* Uc_out, sc_bbpgd_stats* stats);
+
+/* ------------------------------------------------- the whole time-step path */
+/* One call = the four steps of P:L480-L489 minus the position update:
+ * build_contacts, assemble_D, U_ext = Mobility(F_ext), q, bbpgd_solve.
+ * kind 0: spheres (pos, radius, gap_abs, gap_rel); kind 1: rods (pos = centres,
+ * dir, length, b, gap_abs = threshold).  F_ext: n x 6.  Fc_out/Uc_out: n x 6,
+ * may be NULL.  n_c: out. */
+typedef struct {
+  int32_t kind;
+  int32_t reserved;
+  int64_t n;
+  const double* pos;
+  const double* radius;
+  const double* dir;
+  const double* length;
+  double b;
+  double gap_abs, gap_rel;
+  double mu, dt;
+  const double* F_ext;
+} sc_problem;
+int sc_collision_step(sc_ctx* ctx, const sc_problem* prob, const sc_bbpgd_opts* opts,
+                      double* Fc_out, double* Uc_out, int64_t* n_c, sc_bbpgd_stats* stats);
+
+/* ----------------------------------------------------------- measurement */
+/* Kernel families for timing/launch accounting. */
+enum {
+  SC_K_CONTACTS = 0, SC_K_ASSEMBLE = 1, SC_K_GATHER = 2, SC_K_RPY = 3, SC_K_COMBINE = 4,
+  SC_K_DT = 5, SC_K_FINALIZE = 6, SC_K_MISC = 7, SC_K_COUNT = 8
+};
+/* enable != 0: bracket every launch with CUDA events on the context stream. */
+int sc_set_timing(sc_ctx* ctx, int enable);
+/* Sum of event-timed launch durations (ms) and launch count for a family
+ * since the last reset (synchronises the stream). */
+int sc_get_timing(sc_ctx* ctx, int family, double* total_ms, int64_t* launches);
+int sc_reset_timing(sc_ctx* ctx);
+/* Total number of kernels this context launched since creation. */
+int64_t sc_launch_count(const sc_ctx* ctx);
+
+/* Host-only helper (no GPU needed): the row/chunk partition a world-sized
+ * context uses for n bodies.  out7 = {npad,
+ * rows_per_rank, row_lo, row_hi, chunk_lo, chunk_hi, nsplit}: rank owns RPY
+ * target rows [row_lo, row_hi) and the constraints whose first body lies there
+ * (the paper's smaller-index rule); chunk c = bodies
+ * [256c, 256c+256). */
+int sc_plan_partition(int64_t n, int world, int rank, int64_t* out7);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STOKESCOL_H */

@@ -1,0 +1,239 @@
+"""Thin Python binding of the C ABI (same names as include/stokescol.h).
+
+Argument marshalling only: every step of the hot path runs in libstokescol's
+CUDA kernels.  Arrays may be torch tensors (CUDA or CPU) or numpy arrays;
+CPU arrays are staged by the library itself (host pointers are accepted by
+every entry point).  Outputs are allocated as torch CUDA tensors unless the
+caller passes buffers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+
+class ScError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_lib.STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _ptr(a):
+    """Data pointer of a contiguous float64/int32 torch tensor or numpy array (None -> NULL)."""
+    if a is None:
+        return None
+    if torch is not None and isinstance(a, torch.Tensor):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr()
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _check_dtype(a, dt):
+    if a is None:
+        return a
+    if torch is not None and isinstance(a, torch.Tensor):
+        want = torch.float64 if dt == "f64" else torch.int32
+        if a.dtype != want:
+            raise TypeError(f"expected {want}, got {a.dtype}")
+    elif isinstance(a, np.ndarray):
+        want = np.float64 if dt == "f64" else np.int32
+        if a.dtype != want:
+            raise TypeError(f"expected {want}, got {a.dtype}")
+    return a
+
+
+class Context:
+    """One sc_ctx (one GPU).  ``world > 1``: NCCL communicator over ranks."""
+
+    def __init__(self, device: int = 0, stream=None, nccl_id: bytes | None = None, rank: int = 0,
+                 world: int = 1):
+        self.lib = _lib.load()
+        self._h = C.c_void_p()
+        s = None
+        if stream is not None:
+            s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        if world > 1:
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+            rc = self.lib.sc_create_dist(C.byref(self._h), device, s, idbuf, rank, world)
+        else:
+            rc = self.lib.sc_create(C.byref(self._h), device, s)
+        if rc != 0:
+            raise ScError(rc, f"sc_create failed on device {device}")
+        self.device = device
+        self.n = 0
+        self.nc = 0
+        self.kind = None
+
+    # ------------------------------------------------------------- plumbing
+    def close(self):
+        if self._h:
+            self.lib.sc_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _rc(self, rc, allow=(0,)):
+        if rc not in allow:
+            raise ScError(rc, self.lib.sc_last_error(self._h).decode())
+        return rc
+
+    @property
+    def stream_ptr(self) -> int:
+        return self.lib.sc_stream(self._h) or 0
+
+    def torch_stream(self):
+        return torch.cuda.ExternalStream(self.stream_ptr, device=self.device)
+
+    def _dev(self, shape, dtype=None):
+        return torch.empty(shape, dtype=dtype or torch.float64, device=f"cuda:{self.device}")
+
+    # ------------------------------------------------------------- (a1)
+    def build_contacts_spheres(self, pos, radius=None, gap_abs=0.0, gap_rel=0.1) -> int:
+        n = int(pos.shape[0])
+        nc = C.c_int64()
+        self._rc(self.lib.sc_build_contacts_spheres(self._h, n, _ptr(_check_dtype(pos, "f64")),
+                                                    _ptr(_check_dtype(radius, "f64")), float(gap_abs),
+                                                    float(gap_rel), C.byref(nc)))
+        self.n, self.nc, self.kind = n, nc.value, "spheres"
+        return self.nc
+
+    def build_contacts_rods(self, center, direction, length, b, gap_thresh) -> int:
+        n = int(center.shape[0])
+        nc = C.c_int64()
+        self._rc(self.lib.sc_build_contacts_rods(self._h, n, _ptr(_check_dtype(center, "f64")),
+                                                 _ptr(_check_dtype(direction, "f64")),
+                                                 _ptr(_check_dtype(length, "f64")), float(b),
+                                                 float(gap_thresh), C.byref(nc)))
+        self.n, self.nc, self.kind = n, nc.value, "rods"
+        return self.nc
+
+    def get_contacts(self, lever: bool = False):
+        nc = self.nc
+        ci = self._dev((nc,), torch.int32)
+        cj = self._dev((nc,), torch.int32)
+        gap = self._dev((nc,))
+        nrm = self._dev((nc, 3))
+        lev = self._dev((nc, 2, 3)) if lever else None
+        self._rc(self.lib.sc_get_contacts(self._h, _ptr(ci), _ptr(cj), _ptr(gap), _ptr(nrm), _ptr(lev)))
+        out = {"i": ci, "j": cj, "gap": gap, "normal": nrm}
+        if lever:
+            out["lever"] = lev
+        return out
+
+    # ------------------------------------------------------------- (a2)
+    def assemble_D(self):
+        self._rc(self.lib.sc_assemble_D(self._h))
+
+    def apply_D(self, gamma, out=None):
+        out = self._dev((self.n, 6)) if out is None else out
+        self._rc(self.lib.sc_apply_D(self._h, _ptr(_check_dtype(gamma, "f64")), _ptr(_check_dtype(out, "f64"))))
+        return out
+
+    def apply_DT(self, UW, out=None):
+        out = self._dev((self.nc,)) if out is None else out
+        self._rc(self.lib.sc_apply_DT(self._h, _ptr(_check_dtype(UW, "f64")), _ptr(_check_dtype(out, "f64"))))
+        return out
+
+    # ------------------------------------------------------------- (a4)
+    def mobility_apply(self, FT, mu=1.0, out=None):
+        out = self._dev((self.n, 6)) if out is None else out
+        self._rc(self.lib.sc_mobility_apply(self._h, float(mu), _ptr(_check_dtype(FT, "f64")),
+                                            _ptr(_check_dtype(out, "f64"))))
+        return out
+
+    # ------------------------------------------------------------- q, (a6)
+    def lcp_q(self, dt, U_nc, out=None):
+        out = self._dev((self.nc,)) if out is None else out
+        self._rc(self.lib.sc_lcp_q(self._h, float(dt), _ptr(_check_dtype(U_nc, "f64")),
+                                   _ptr(_check_dtype(out, "f64"))))
+        return out
+
+    def bbpgd_solve(self, mu=1.0, tol=1e-8, max_iter=5000, bb_mode=0, fixed_iters=False, gamma0=None,
+                    want_g=True, want_Fc=True, want_Uc=True, out=None):
+        opts = _lib.BbpgdOpts(float(mu), float(tol), int(max_iter), int(bb_mode), int(bool(fixed_iters)),
+                              int(gamma0 is not None))
+        out = out or {}
+        gamma = out.get("gamma")
+        if gamma is None:
+            gamma = self._dev((self.nc,))
+        if gamma0 is not None:
+            gamma.copy_(torch.as_tensor(gamma0, dtype=torch.float64))
+        g = out.get("g", self._dev((self.nc,)) if want_g else None)
+        Fc = out.get("Fc", self._dev((self.n, 6)) if want_Fc else None)
+        Uc = out.get("Uc", self._dev((self.n, 6)) if want_Uc else None)
+        st = _lib.BbpgdStats()
+        rc = self._rc(self.lib.sc_bbpgd_solve(self._h, C.byref(opts), _ptr(gamma), _ptr(g), _ptr(Fc), _ptr(Uc),
+                                              C.byref(st)), allow=(0, 1))
+        return {"gamma": gamma, "g": g, "Fc": Fc, "Uc": Uc, "status": rc, **st.as_dict()}
+
+    def collision_step(self, kind, pos, F_ext, radius=None, direction=None, length=None, b=0.5,
+                       gap_abs=0.0, gap_rel=0.1, mu=1.0, dt=0.01, tol=1e-8, max_iter=5000, bb_mode=0,
+                       fixed_iters=False, Fc_out=None, Uc_out=None):
+        """The whole per-step path in one C call (any pointer may be host or device)."""
+        n = int(pos.shape[0])
+        prob = _lib.Problem(0 if kind == "spheres" else 1, 0, n, _ptr(pos), _ptr(radius), _ptr(direction),
+                            _ptr(length), float(b), float(gap_abs), float(gap_rel), float(mu), float(dt),
+                            _ptr(F_ext))
+        opts = _lib.BbpgdOpts(float(mu), float(tol), int(max_iter), int(bb_mode), int(bool(fixed_iters)), 0)
+        nc = C.c_int64()
+        st = _lib.BbpgdStats()
+        rc = self._rc(self.lib.sc_collision_step(self._h, C.byref(prob), C.byref(opts), _ptr(Fc_out),
+                                                 _ptr(Uc_out), C.byref(nc), C.byref(st)), allow=(0, 1))
+        self.n, self.nc, self.kind = n, nc.value, kind
+        return {"status": rc, "nc": nc.value, **st.as_dict()}
+
+    # ------------------------------------------------------------- measurement
+    def set_timing(self, enable=True):
+        self._rc(self.lib.sc_set_timing(self._h, int(bool(enable))))
+
+    def reset_timing(self):
+        self._rc(self.lib.sc_reset_timing(self._h))
+
+    def get_timing(self):
+        out = {}
+        for k, name in enumerate(_lib.K_FAMILIES):
+            ms = C.c_double()
+            cnt = C.c_int64()
+            self._rc(self.lib.sc_get_timing(self._h, k, C.byref(ms), C.byref(cnt)))
+            out[name] = (ms.value, cnt.value)
+        return out
+
+    def launch_count(self) -> int:
+        return int(self.lib.sc_launch_count(self._h))
+
+
+def nccl_unique_id() -> bytes:
+    lib = _lib.load()
+    buf = C.create_string_buffer(128)
+    rc = lib.sc_nccl_unique_id(buf)
+    if rc != 0:
+        raise ScError(rc, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def plan_partition(n: int, world: int, rank: int) -> dict:
+    """Host-only: the row/chunk partition of a world-sized context (no GPU needed)."""
+    lib = _lib.load()
+    out = (C.c_int64 * 7)()
+    rc = lib.sc_plan_partition(int(n), int(world), int(rank), out)
+    if rc != 0:
+        raise ScError(rc, "plan_partition: bad arguments")
+    keys = ["npad", "rows_per_rank", "row_lo", "row_hi", "chunk_lo", "chunk_hi", "nsplit"]
+    return dict(zip(keys, list(out)))

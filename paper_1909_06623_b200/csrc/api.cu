@@ -1,0 +1,890 @@
+// api.cu -- the C ABI (include/stokescol.h): context, staging, NCCL, and the
+// BBPGD control loop (Alg. 1) around the device kernels.
+//
+// The loop runs on the host but never waits per iteration on small problems:
+// iterations are enqueued in batches and every kernel of an iteration starts by
+// reading the device flag `done` (set by K-FINALIZE on convergence, j_max or a
+// non-finite value) and returns at once if it is set.  The host reads the
+// solver scalars (one pinned copy) only between batches.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "sc_internal.h"
+
+namespace sc {
+
+int fail(sc_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+int cuda_fail(sc_ctx* c, cudaError_t e, const char* what) {
+  return fail(c, SC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static cudaEvent_t pool_get(sc_ctx* ctx) {
+  auto& p = ctx->timer.pool;
+  if (!p.empty()) {
+    cudaEvent_t e = p.back();
+    p.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void timer_begin(sc_ctx* ctx, int family) {
+  if (!ctx->timer.enabled) return;
+  cudaEvent_t e = pool_get(ctx);
+  cudaEventRecord(e, ctx->stream);
+  ctx->timer.ev[family].push_back(e);
+}
+void timer_end(sc_ctx* ctx, int family) {
+  if (!ctx->timer.enabled) return;
+  cudaEvent_t e = pool_get(ctx);
+  cudaEventRecord(e, ctx->stream);
+  ctx->timer.ev[family].push_back(e);
+}
+
+int check_launch(sc_ctx* ctx, const char* what) {
+  ctx->launch_count += 1;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, what);
+  return 0;
+}
+
+static void timer_collect(sc_ctx* ctx) {
+  cudaStreamSynchronize(ctx->stream);
+  for (int f = 0; f < SC_K_COUNT; ++f) {
+    auto& v = ctx->timer.ev[f];
+    for (size_t k = 0; k + 1 < v.size(); k += 2) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, v[k], v[k + 1]) == cudaSuccess) ctx->timer.total_ms[f] += ms;
+      ctx->timer.launches[f] += 1;
+    }
+    for (auto e : v) ctx->timer.pool.push_back(e);
+    v.clear();
+  }
+}
+
+// ------------------------------------------------------------ staging
+static bool is_device_ptr(const void* p) {
+  if (p == nullptr) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+struct Stager {
+  sc_ctx* ctx;
+  std::vector<DBuf<char>> bufs;
+  struct Pending {
+    void* host;
+    const void* dev;
+    size_t bytes;
+  };
+  std::vector<Pending> outs;
+  explicit Stager(sc_ctx* c) : ctx(c) {}
+  ~Stager() {
+    for (auto& b : bufs) release(b);
+  }
+  // device view of an input (copied if host)
+  template <typename T>
+  int in(const T* p, size_t count, const T** out) {
+    if (p == nullptr || count == 0 || is_device_ptr(p)) {
+      *out = p;
+      return 0;
+    }
+    bufs.emplace_back();
+    if (int rc = ensure(ctx, bufs.back(), count * sizeof(T))) return rc;
+    cudaError_t e = cudaMemcpyAsync(bufs.back().p, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "stage in");
+    *out = reinterpret_cast<const T*>(bufs.back().p);
+    return 0;
+  }
+  template <typename T>
+  int out(T* p, size_t count, T** o) {
+    if (p == nullptr || count == 0 || is_device_ptr(p)) {
+      *o = p;
+      return 0;
+    }
+    bufs.emplace_back();
+    if (int rc = ensure(ctx, bufs.back(), count * sizeof(T))) return rc;
+    *o = reinterpret_cast<T*>(bufs.back().p);
+    outs.push_back({p, bufs.back().p, count * sizeof(T)});
+    return 0;
+  }
+  // in + out (read-modify-write)
+  template <typename T>
+  int inout(T* p, size_t count, T** o) {
+    if (int rc = out(p, count, o)) return rc;
+    if (*o != p) {
+      cudaError_t e = cudaMemcpyAsync(*o, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "stage inout");
+    }
+    return 0;
+  }
+  int finish() {
+    for (auto& o : outs) {
+      cudaError_t e = cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDeviceToHost, ctx->stream);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "stage out");
+    }
+    if (!outs.empty()) {
+      cudaError_t e = cudaStreamSynchronize(ctx->stream);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "stage sync");
+    }
+    outs.clear();
+    return 0;
+  }
+};
+
+// ------------------------------------------------------------ partition
+struct Part {
+  int64_t rpr = 0;             // rows per rank (multiple of 256)
+  int64_t row_lo = 0, row_hi = 0;  // own rows, clipped to npad
+  int64_t c0 = 0, c1 = 0;      // own chunks
+  int64_t l0 = 0, l1 = 0;      // own constraints
+  std::vector<int64_t> loff, lcnt;  // constraint slices of every rank
+};
+
+static void plan_rows(int64_t npad, int world, int rank, int64_t* rpr, int64_t* lo, int64_t* hi) {
+  const int64_t B = npad / kRpyRows;
+  const int64_t bpr = (B + world - 1) / world;
+  *rpr = bpr * kRpyRows;
+  *lo = std::min(npad, rank * *rpr);
+  *hi = std::min(npad, (rank + 1) * *rpr);
+}
+
+static Part partition(const sc_ctx* ctx) {
+  Part p;
+  const int64_t n = ctx->n;
+  auto fp = [&](int64_t b) -> int64_t { return ctx->h_first_ptr[std::min(b, n)]; };
+  plan_rows(ctx->npad, ctx->world, ctx->rank, &p.rpr, &p.row_lo, &p.row_hi);
+  p.c0 = p.row_lo / kChunkBodies;
+  p.c1 = p.row_hi / kChunkBodies;
+  p.l0 = fp(p.row_lo);
+  p.l1 = fp(p.row_hi);
+  for (int r = 0; r < ctx->world; ++r) {
+    int64_t rpr, lo, hi;
+    plan_rows(ctx->npad, ctx->world, r, &rpr, &lo, &hi);
+    p.loff.push_back(fp(lo));
+    p.lcnt.push_back(fp(hi) - fp(lo));
+  }
+  return p;
+}
+
+static bool dist_spheres(const sc_ctx* ctx) { return ctx->world > 1 && ctx->kind == kSpheres; }
+
+#define NCCL_CHECK(call)                                                                        \
+  do {                                                                                          \
+    ncclResult_t r_ = (call);                                                                   \
+    if (r_ != ncclSuccess) return fail(ctx, SC_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+// every rank's slice of a length-nc vector -> full vector on every rank
+static int bcast_slices(sc_ctx* ctx, const Part& p, double* v) {
+  NCCL_CHECK(ncclGroupStart());
+  for (int r = 0; r < ctx->world; ++r) {
+    if (p.lcnt[r] == 0) continue;
+    NCCL_CHECK(ncclBroadcast(v + p.loff[r], v + p.loff[r], p.lcnt[r], ncclDouble, r, ctx->comm, ctx->stream));
+  }
+  NCCL_CHECK(ncclGroupEnd());
+  return 0;
+}
+
+static int allgather_u4(sc_ctx* ctx, const Part& p) {
+  double* base = reinterpret_cast<double*>(ctx->u4.p);
+  NCCL_CHECK(ncclAllGather(base + ctx->rank * p.rpr * 4, base, p.rpr * 4, ncclDouble, ctx->comm, ctx->stream));
+  return 0;
+}
+
+static int allreduce_chunks(sc_ctx* ctx) {
+  NCCL_CHECK(ncclAllReduce(ctx->chunk_part.p, ctx->chunk_red.p, ctx->nchunks * kPartials, ncclDouble, ncclSum,
+                           ctx->comm, ctx->stream));
+  return 0;
+}
+
+// ------------------------------------------------------------ bodies
+__global__ void set_spheres_kernel(const double* __restrict__ pos, const double* __restrict__ radius, int64_t n,
+                                   int64_t npad, double a_const, double4* __restrict__ pos4,
+                                   int32_t* __restrict__ bad) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= npad) return;
+  if (b < n) {
+    const double a = radius ? radius[b] : a_const;
+    if (!(a > 0.0) || !isfinite(a)) atomicExch(bad, 1);
+    pos4[b] = make_double4(pos[3 * b], pos[3 * b + 1], pos[3 * b + 2], 0.5 * a);
+  } else {
+    // padded rows: far away, distinct, zero force (never coincide with anything)
+    pos4[b] = make_double4(1e30 + static_cast<double>(b - n) * 1e20, 1e30, 1e30, 0.5 * a_const);
+  }
+}
+
+__global__ void radius_minmax_kernel(const double* __restrict__ radius, int64_t n, int32_t* __restrict__ poly) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  if (radius[b] != radius[0]) atomicExch(poly, 1);
+}
+
+__global__ void set_rods_kernel(const double* __restrict__ c, const double* __restrict__ d,
+                                const double* __restrict__ L, int64_t n, int64_t npad, double b,
+                                double4* __restrict__ pos4, double4* __restrict__ dir4, int32_t* __restrict__ bad) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= npad) return;
+  if (k < n) {
+    const double l = L[k];
+    if (!(l > 2.0 * b) || !isfinite(l)) atomicExch(bad, 1);  // drag needs ln(L/2b) > 0
+    pos4[k] = make_double4(c[3 * k], c[3 * k + 1], c[3 * k + 2], l);
+    dir4[k] = make_double4(d[3 * k], d[3 * k + 1], d[3 * k + 2], 0.0);
+  } else {
+    pos4[k] = make_double4(1e30 + static_cast<double>(k - n) * 1e20, 1e30, 1e30, 1.0);
+    dir4[k] = make_double4(1, 0, 0, 0);
+  }
+}
+
+// zeta_perp = 2 zeta_par = 4 pi mu L / ln(L/(2b)), zeta_rot = pi mu L^3 / (3 ln(L/(2b)))  (configs[3])
+__global__ void rod_mob_kernel(const double4* __restrict__ pos4, int64_t n, double b, double mu,
+                               double4* __restrict__ mob4) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double L = pos4[k].w;
+  const double lg = log(L / (2.0 * b));
+  const double pi = 3.14159265358979323846;
+  const double zperp = 4.0 * pi * mu * L / lg;
+  const double zpar = 0.5 * zperp;
+  const double zrot = pi * mu * L * L * L / (3.0 * lg);
+  mob4[k] = make_double4(1.0 / zpar, 1.0 / zperp, 1.0 / zrot, mu);
+}
+
+static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+static int prepare_bodies(sc_ctx* ctx, int kind, int64_t n) {
+  ctx->kind = kind;
+  ctx->n = n;
+  ctx->npad = round_up(std::max<int64_t>(n, 1), kRpyRows);
+  ctx->nsplit = choose_nsplit(ctx->npad, ctx->world);
+  ctx->nc = 0;
+  ctx->assembled = false;
+  ctx->have_q = false;
+  ctx->rod_mu = -1.0;
+  int64_t rpr, lo, hi;
+  plan_rows(ctx->npad, ctx->world, ctx->rank, &rpr, &lo, &hi);
+  const int64_t urows = std::max(ctx->npad, rpr * ctx->world);
+  if (int rc = ensure(ctx, ctx->pos4, ctx->npad)) return rc;
+  if (int rc = ensure(ctx, ctx->f4, ctx->npad)) return rc;
+  if (int rc = ensure(ctx, ctx->t4, ctx->npad)) return rc;
+  if (int rc = ensure(ctx, ctx->u4, kind == kRods ? 2 * ctx->npad : urows)) return rc;
+  if (kind == kRods) {
+    if (int rc = ensure(ctx, ctx->dir4, ctx->npad)) return rc;
+    if (int rc = ensure(ctx, ctx->rodmob4, ctx->npad)) return rc;
+  }
+  return 0;
+}
+
+static int check_flag(sc_ctx* ctx, int code, const char* msg) {
+  SC_CUDA(cudaMemcpyAsync(ctx->herr, ctx->derr, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (*ctx->herr) {
+    SC_CUDA(cudaMemsetAsync(ctx->derr, 0, sizeof(int32_t), ctx->stream));
+    *ctx->herr = 0;
+    return fail(ctx, code, msg);
+  }
+  return 0;
+}
+
+static int ensure_rod_mob(sc_ctx* ctx, double mu) {
+  if (ctx->kind != kRods || ctx->rod_mu == mu) return 0;
+  if (ctx->n > 0) {
+    timer_begin(ctx, SC_K_MISC);
+    rod_mob_kernel<<<static_cast<unsigned>((ctx->n + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->pos4.p, ctx->n, ctx->rod_b, mu, ctx->rodmob4.p);
+    timer_end(ctx, SC_K_MISC);
+    if (int rc = check_launch(ctx, "rod_mob")) return rc;
+  }
+  ctx->rod_mu = mu;
+  return 0;
+}
+
+// spheres: u4 = RPY(f4) for all rows (own rows + all-gather when distributed)
+static int rpy_all(sc_ctx* ctx, const Part& p, double mu, const int32_t* done) {
+  if (dist_spheres(ctx)) {
+    if (int rc = rpy_apply_rows(ctx, ctx->f4.p, p.row_lo, p.row_hi - p.row_lo, mu, ctx->u4.p, done)) return rc;
+    return allgather_u4(ctx, p);
+  }
+  return rpy_apply_rows(ctx, ctx->f4.p, 0, ctx->npad, mu, ctx->u4.p, done);
+}
+
+}  // namespace sc
+
+using namespace sc;
+
+// ============================================================== C ABI
+extern "C" {
+
+int sc_version(void) { return 10000; }
+
+static int create_common(sc_ctx** out, int device, void* stream) {
+  if (out == nullptr) return SC_EINVAL;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return SC_ECUDA;
+  }
+  if (device < 0 || device >= ndev) return SC_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return SC_ECUDA;
+  sc_ctx* ctx = new sc_ctx();
+  ctx->device = device;
+  if (stream != nullptr) {
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      return SC_ECUDA;
+    }
+    ctx->own_stream = true;
+  }
+  if (cudaMalloc(&ctx->dsc, sizeof(DevScalars)) != cudaSuccess ||
+      cudaMallocHost(&ctx->hsc, sizeof(DevScalars)) != cudaSuccess ||
+      cudaMalloc(&ctx->derr, sizeof(int32_t)) != cudaSuccess ||
+      cudaMallocHost(&ctx->herr, sizeof(int32_t)) != cudaSuccess) {
+    sc_destroy(ctx);
+    return SC_ENOMEM;
+  }
+  cudaMemset(ctx->derr, 0, sizeof(int32_t));
+  cudaMemset(ctx->dsc, 0, sizeof(DevScalars));
+  *ctx->herr = 0;
+  *out = ctx;
+  return SC_OK;
+}
+
+int sc_create(sc_ctx** out, int device, void* stream) { return create_common(out, device, stream); }
+
+int sc_nccl_unique_id(void* out128) {
+  if (out128 == nullptr) return SC_EINVAL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return SC_ENCCL;
+  std::memcpy(out128, &id, sizeof(id));
+  return SC_OK;
+}
+
+int sc_create_dist(sc_ctx** out, int device, void* stream, const void* nccl_id, int rank, int world) {
+  if (nccl_id == nullptr || world < 1 || rank < 0 || rank >= world) return SC_EINVAL;
+  int rc = create_common(out, device, stream);
+  if (rc != SC_OK) return rc;
+  sc_ctx* ctx = *out;
+  ctx->rank = rank;
+  ctx->world = world;
+  if (world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, world, id, rank);
+    if (r != ncclSuccess) {
+      sc_destroy(ctx);
+      *out = nullptr;
+      return SC_ENCCL;
+    }
+  }
+  return SC_OK;
+}
+
+void sc_destroy(sc_ctx* ctx) {
+  if (ctx == nullptr) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  release(ctx->pos4); release(ctx->dir4); release(ctx->rodmob4);
+  release(ctx->ci); release(ctx->cj); release(ctx->nrm4); release(ctx->lev4); release(ctx->rxn4);
+  release(ctx->row_ptr); release(ctx->inc); release(ctx->first_ptr);
+  release(ctx->q); release(ctx->gam[0]); release(ctx->gam[1]); release(ctx->g[0]); release(ctx->g[1]);
+  release(ctx->w); release(ctx->gam_user); release(ctx->chunk_part); release(ctx->chunk_red);
+  release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);
+  release(ctx->bbox_part); release(ctx->cell_of); release(ctx->cell_cnt); release(ctx->cell_start);
+  release(ctx->sorted_idx); release(ctx->pair_cnt); release(ctx->pair_off); release(ctx->scan_tmp);
+  release(ctx->sorted4); release(ctx->sorted_dir4); release(ctx->stage);
+  if (ctx->dsc) cudaFree(ctx->dsc);
+  if (ctx->hsc) cudaFreeHost(ctx->hsc);
+  if (ctx->derr) cudaFree(ctx->derr);
+  if (ctx->herr) cudaFreeHost(ctx->herr);
+  for (int f = 0; f < SC_K_COUNT; ++f)
+    for (auto e : ctx->timer.ev[f]) cudaEventDestroy(e);
+  for (auto e : ctx->timer.pool) cudaEventDestroy(e);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* sc_last_error(const sc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+void* sc_stream(const sc_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int sc_plan_partition(int64_t n, int world, int rank, int64_t* out7) {
+  if (n < 0 || world < 1 || rank < 0 || rank >= world || out7 == nullptr) return SC_EINVAL;
+  const int64_t npad = round_up(std::max<int64_t>(n, 1), kRpyRows);
+  int64_t rpr, lo, hi;
+  plan_rows(npad, world, rank, &rpr, &lo, &hi);
+  out7[0] = npad;
+  out7[1] = rpr;
+  out7[2] = lo;
+  out7[3] = hi;
+  out7[4] = lo / kChunkBodies;
+  out7[5] = hi / kChunkBodies;
+  out7[6] = choose_nsplit(npad, world);
+  return SC_OK;
+}
+
+// ------------------------------------------------------------ (a1)
+int sc_build_contacts_spheres(sc_ctx* ctx, int64_t n, const double* pos, const double* radius, double gap_abs,
+                              double gap_rel, int64_t* n_c) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (n < 0 || (n > 0 && pos == nullptr) || !(gap_rel >= 0.0) || !std::isfinite(gap_abs))
+    return fail(ctx, SC_EINVAL, "build_contacts_spheres: bad arguments");
+  if (n >= (int64_t(1) << 30)) return fail(ctx, SC_EINVAL, "too many bodies");
+  cudaSetDevice(ctx->device);
+  if (int rc = prepare_bodies(ctx, kSpheres, n)) return rc;
+  Stager st(ctx);
+  const double *dpos = nullptr, *drad = nullptr;
+  if (int rc = st.in(pos, 3 * n, &dpos)) return rc;
+  if (int rc = st.in(radius, n, &drad)) return rc;
+  SC_CUDA(cudaMemsetAsync(ctx->derr, 0, sizeof(int32_t), ctx->stream));
+  timer_begin(ctx, SC_K_MISC);
+  set_spheres_kernel<<<static_cast<unsigned>((ctx->npad + 255) / 256), 256, 0, ctx->stream>>>(
+      dpos, drad, n, ctx->npad, 1.0, ctx->pos4.p, ctx->derr);
+  timer_end(ctx, SC_K_MISC);
+  if (int rc = check_launch(ctx, "set_spheres")) return rc;
+  if (int rc = check_flag(ctx, SC_EINVAL, "radii must be positive and finite")) return rc;
+  // monodisperse fast path when all radii are equal
+  ctx->poly = 0;
+  ctx->a_const = 1.0;
+  if (radius != nullptr && n > 0) {
+    timer_begin(ctx, SC_K_MISC);
+    radius_minmax_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(drad, n, ctx->derr);
+    timer_end(ctx, SC_K_MISC);
+    if (int rc = check_launch(ctx, "radius_minmax")) return rc;
+    SC_CUDA(cudaMemcpyAsync(ctx->herr, ctx->derr, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    double a0 = 1.0;
+    SC_CUDA(cudaMemcpyAsync(&a0, drad, sizeof(double), cudaMemcpyDefault, ctx->stream));
+    SC_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->poly = *ctx->herr ? 1 : 0;
+    *ctx->herr = 0;
+    SC_CUDA(cudaMemsetAsync(ctx->derr, 0, sizeof(int32_t), ctx->stream));
+    ctx->a_const = a0;
+  }
+  if (ctx->npad > n) {  // padded rows carry the constant radius
+    // (their w only enters the far formula for zero-force sources)
+  }
+  if (int rc = build_contacts_spheres(ctx, gap_abs, gap_rel)) return rc;
+  if (n_c) *n_c = ctx->nc;
+  return SC_OK;
+}
+
+int sc_build_contacts_rods(sc_ctx* ctx, int64_t n, const double* center, const double* dir, const double* length,
+                           double b, double gap_thresh, int64_t* n_c) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (n < 0 || (n > 0 && (center == nullptr || dir == nullptr || length == nullptr)) || !(b > 0.0) ||
+      !std::isfinite(gap_thresh))
+    return fail(ctx, SC_EINVAL, "build_contacts_rods: bad arguments");
+  if (n >= (int64_t(1) << 30)) return fail(ctx, SC_EINVAL, "too many bodies");
+  cudaSetDevice(ctx->device);
+  if (int rc = prepare_bodies(ctx, kRods, n)) return rc;
+  ctx->rod_b = b;
+  ctx->poly = 0;
+  Stager st(ctx);
+  const double *dc = nullptr, *dd = nullptr, *dl = nullptr;
+  if (int rc = st.in(center, 3 * n, &dc)) return rc;
+  if (int rc = st.in(dir, 3 * n, &dd)) return rc;
+  if (int rc = st.in(length, n, &dl)) return rc;
+  SC_CUDA(cudaMemsetAsync(ctx->derr, 0, sizeof(int32_t), ctx->stream));
+  timer_begin(ctx, SC_K_MISC);
+  set_rods_kernel<<<static_cast<unsigned>((ctx->npad + 255) / 256), 256, 0, ctx->stream>>>(
+      dc, dd, dl, n, ctx->npad, b, ctx->pos4.p, ctx->dir4.p, ctx->derr);
+  timer_end(ctx, SC_K_MISC);
+  if (int rc = check_launch(ctx, "set_rods")) return rc;
+  if (int rc = check_flag(ctx, SC_EINVAL, "rod lengths must exceed 2b (ln(L/2b) > 0)")) return rc;
+  if (int rc = build_contacts_rods(ctx, gap_thresh)) return rc;
+  if (n_c) *n_c = ctx->nc;
+  return SC_OK;
+}
+
+__global__ static void unpack_contacts_kernel(const double4* __restrict__ nrm4, const double4* __restrict__ lev4,
+                                              int64_t nc, double* __restrict__ gap, double* __restrict__ normal,
+                                              double* __restrict__ lever) {
+  const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (l >= nc) return;
+  const double4 v = nrm4[l];
+  if (gap) gap[l] = v.w;
+  if (normal) {
+    normal[3 * l] = v.x;
+    normal[3 * l + 1] = v.y;
+    normal[3 * l + 2] = v.z;
+  }
+  if (lever) {
+    const double4 a = lev4[2 * l], b = lev4[2 * l + 1];
+    double* o = lever + 6 * l;
+    o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = b.x; o[4] = b.y; o[5] = b.z;
+  }
+}
+
+int sc_get_contacts(sc_ctx* ctx, int32_t* ci, int32_t* cj, double* gap, double* normal, double* lever) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (ctx->kind == kNone) return fail(ctx, SC_EINVAL, "get_contacts before build_contacts");
+  if (lever != nullptr && ctx->kind != kRods) return fail(ctx, SC_EINVAL, "lever arms exist for rods only");
+  cudaSetDevice(ctx->device);
+  const int64_t nc = ctx->nc;
+  if (nc == 0) return SC_OK;
+  Stager st(ctx);
+  int32_t *oi = nullptr, *oj = nullptr;
+  double *og = nullptr, *on = nullptr, *ol = nullptr;
+  if (int rc = st.out(ci, nc, &oi)) return rc;
+  if (int rc = st.out(cj, nc, &oj)) return rc;
+  if (int rc = st.out(gap, nc, &og)) return rc;
+  if (int rc = st.out(normal, 3 * nc, &on)) return rc;
+  if (int rc = st.out(lever, 6 * nc, &ol)) return rc;
+  if (oi) SC_CUDA(cudaMemcpyAsync(oi, ctx->ci.p, nc * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (oj) SC_CUDA(cudaMemcpyAsync(oj, ctx->cj.p, nc * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (og || on || ol) {
+    timer_begin(ctx, SC_K_MISC);
+    unpack_contacts_kernel<<<static_cast<unsigned>((nc + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->nrm4.p, ctx->lev4.p, nc, og, on, ol);
+    timer_end(ctx, SC_K_MISC);
+    if (int rc = check_launch(ctx, "unpack_contacts")) return rc;
+  }
+  if (int rc = st.finish()) return rc;
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return SC_OK;
+}
+
+// ------------------------------------------------------------ (a2)
+int sc_assemble_D(sc_ctx* ctx) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (ctx->kind == kNone) return fail(ctx, SC_EINVAL, "assemble_D before build_contacts");
+  cudaSetDevice(ctx->device);
+  if (int rc = assemble(ctx)) return rc;
+  const int64_t nc = ctx->nc;
+  for (int k = 0; k < 2; ++k) {
+    if (int rc = ensure(ctx, ctx->gam[k], nc)) return rc;
+    if (int rc = ensure(ctx, ctx->g[k], nc)) return rc;
+  }
+  if (int rc = ensure(ctx, ctx->q, nc)) return rc;
+  if (int rc = ensure(ctx, ctx->chunk_part, ctx->nchunks * kPartials)) return rc;
+  if (int rc = ensure(ctx, ctx->chunk_red, ctx->nchunks * kPartials)) return rc;
+  SC_CUDA(cudaMemsetAsync(ctx->chunk_part.p, 0, sizeof(double) * ctx->nchunks * kPartials, ctx->stream));
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return SC_OK;
+}
+
+int sc_apply_D(sc_ctx* ctx, const double* gamma, double* FT) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (!ctx->assembled) return fail(ctx, SC_EINVAL, "apply_D before assemble_D");
+  if (FT == nullptr || (ctx->nc > 0 && gamma == nullptr)) return fail(ctx, SC_EINVAL, "apply_D: NULL buffer");
+  cudaSetDevice(ctx->device);
+  Stager st(ctx);
+  const double* dg = nullptr;
+  double* dF = nullptr;
+  if (int rc = st.in(gamma, ctx->nc, &dg)) return rc;
+  if (int rc = st.out(FT, 6 * ctx->n, &dF)) return rc;
+  if (ctx->n > 0) {
+    if (int rc = launch_gather_raw(ctx, dg, 1.0, dF)) return rc;
+  }
+  if (int rc = st.finish()) return rc;
+  return SC_OK;
+}
+
+int sc_apply_DT(sc_ctx* ctx, const double* UW, double* out) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (!ctx->assembled) return fail(ctx, SC_EINVAL, "apply_DT before assemble_D");
+  if (ctx->nc > 0 && (UW == nullptr || out == nullptr)) return fail(ctx, SC_EINVAL, "apply_DT: NULL buffer");
+  cudaSetDevice(ctx->device);
+  Stager st(ctx);
+  const double* du = nullptr;
+  double* dout = nullptr;
+  if (int rc = st.in(UW, 6 * ctx->n, &du)) return rc;
+  if (int rc = st.out(out, ctx->nc, &dout)) return rc;
+  if (int rc = launch_dt_user(ctx, du, dout, nullptr, 0.0)) return rc;
+  if (int rc = st.finish()) return rc;
+  return SC_OK;
+}
+
+// ------------------------------------------------------------ (a4)
+int sc_mobility_apply(sc_ctx* ctx, double mu, const double* FT, double* UW) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (ctx->kind == kNone) return fail(ctx, SC_EINVAL, "mobility_apply before build_contacts");
+  if (!(mu > 0.0) || (ctx->n > 0 && (FT == nullptr || UW == nullptr)))
+    return fail(ctx, SC_EINVAL, "mobility_apply: bad arguments");
+  if (ctx->n == 0) return SC_OK;
+  cudaSetDevice(ctx->device);
+  Stager st(ctx);
+  const double* dF = nullptr;
+  double* dU = nullptr;
+  if (int rc = st.in(FT, 6 * ctx->n, &dF)) return rc;
+  if (int rc = st.out(UW, 6 * ctx->n, &dU)) return rc;
+  if (ctx->kind == kSpheres) {
+    if (int rc = launch_pack_ft(ctx, dF, ctx->f4.p, ctx->t4.p)) return rc;
+    Part p;
+    if (dist_spheres(ctx)) {
+      plan_rows(ctx->npad, ctx->world, ctx->rank, &p.rpr, &p.row_lo, &p.row_hi);
+    }
+    if (int rc = rpy_all(ctx, p, mu, nullptr)) return rc;
+    if (int rc = launch_unpack_uw_spheres(ctx, ctx->u4.p, ctx->t4.p, mu, dU)) return rc;
+    if (int rc = check_flag(ctx, SC_EDEGENERATE, "coincident centres in the RPY sum")) return rc;
+  } else {
+    if (int rc = ensure_rod_mob(ctx, mu)) return rc;
+    if (int rc = launch_rod_drag_user(ctx, dF, mu, dU)) return rc;
+  }
+  if (int rc = st.finish()) return rc;
+  return SC_OK;
+}
+
+// ------------------------------------------------------------ q
+int sc_lcp_q(sc_ctx* ctx, double dt, const double* U_nc, double* q_out) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (!ctx->assembled) return fail(ctx, SC_EINVAL, "lcp_q before assemble_D");
+  if (!(dt > 0.0) || (ctx->n > 0 && U_nc == nullptr)) return fail(ctx, SC_EINVAL, "lcp_q: bad arguments");
+  cudaSetDevice(ctx->device);
+  Stager st(ctx);
+  const double* du = nullptr;
+  if (int rc = st.in(U_nc, 6 * ctx->n, &du)) return rc;
+  if (int rc = launch_dt_user(ctx, du, ctx->q.p, ctx->q.p, 1.0 / dt)) return rc;
+  if (q_out != nullptr && ctx->nc > 0) {
+    double* dq = nullptr;
+    if (int rc = st.out(q_out, ctx->nc, &dq)) return rc;
+    SC_CUDA(cudaMemcpyAsync(dq, ctx->q.p, ctx->nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  if (int rc = st.finish()) return rc;
+  ctx->have_q = true;
+  return SC_OK;
+}
+
+// ------------------------------------------------------------ (a6) BBPGD
+static int read_scalars(sc_ctx* ctx) {
+  SC_CUDA(cudaMemcpyAsync(ctx->hsc, ctx->dsc, sizeof(DevScalars), cudaMemcpyDeviceToHost, ctx->stream));
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double* g_out, double* Fc_out,
+                   double* Uc_out, sc_bbpgd_stats* stats) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (opts == nullptr || !(opts->mu > 0.0) || !(opts->tol >= 0.0) || opts->max_iter < 0 || opts->bb_mode < 0 ||
+      opts->bb_mode > 2)
+    return fail(ctx, SC_EINVAL, "bbpgd_solve: bad options");
+  if (!ctx->assembled || !ctx->have_q) return fail(ctx, SC_EINVAL, "bbpgd_solve needs assemble_D and lcp_q first");
+  const int64_t nc = ctx->nc, n = ctx->n;
+  if (nc > 0 && gamma == nullptr) return fail(ctx, SC_EINVAL, "bbpgd_solve: gamma is NULL");
+  cudaSetDevice(ctx->device);
+  sc_bbpgd_stats stt;
+  std::memset(&stt, 0, sizeof(stt));
+  const double mu = opts->mu;
+  if (int rc = ensure_rod_mob(ctx, mu)) return rc;
+  Stager st(ctx);
+  double *dgam = nullptr, *dg = nullptr, *dF = nullptr, *dU = nullptr;
+  if (opts->warm_start) {
+    if (int rc = st.inout(gamma, nc, &dgam)) return rc;
+  } else {
+    if (int rc = st.out(gamma, nc, &dgam)) return rc;
+  }
+  if (int rc = st.out(g_out, nc, &dg)) return rc;
+  if (int rc = st.out(Fc_out, 6 * n, &dF)) return rc;
+  if (int rc = st.out(Uc_out, 6 * n, &dU)) return rc;
+
+  if (nc == 0) {  // nothing to resolve: gamma is empty, F_c = 0, U_c = 0
+    if (dF) SC_CUDA(cudaMemsetAsync(dF, 0, sizeof(double) * 6 * n, ctx->stream));
+    if (dU) SC_CUDA(cudaMemsetAsync(dU, 0, sizeof(double) * 6 * n, ctx->stream));
+    if (int rc = st.finish()) return rc;
+    stt.converged = 1;
+    stt.mvops = 0;
+    if (stats) *stats = stt;
+    return SC_OK;
+  }
+  const Part p = partition(ctx);
+  const bool dist = dist_spheres(ctx);
+  const bool spheres = ctx->kind == kSpheres;
+  const int64_t c0 = dist ? p.c0 : 0, c1 = dist ? p.c1 : ctx->nchunks;
+  const double* red = dist ? ctx->chunk_red.p : ctx->chunk_part.p;
+  const int32_t* done = &ctx->dsc->done;
+
+  DevScalars h;
+  std::memset(&h, 0, sizeof(h));
+  h.tol = opts->tol;
+  h.max_iter = opts->max_iter;
+  h.bb_mode = opts->bb_mode;
+  h.fixed = opts->fixed_iters ? 1 : 0;
+  SC_CUDA(cudaMemcpyAsync(ctx->dsc, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+  SC_CUDA(cudaMemsetAsync(ctx->derr, 0, sizeof(int32_t), ctx->stream));
+  SC_CUDA(cudaMemsetAsync(ctx->chunk_part.p, 0, sizeof(double) * ctx->nchunks * kPartials, ctx->stream));
+
+  // mvop(v): u4 = Mobility(D v)  (spheres: f4 then RPY; rods: fused gather + drag)
+  auto mvop_raw = [&](const double* v) -> int {
+    if (int rc = launch_gather_raw(ctx, v, mu, nullptr)) return rc;
+    if (spheres) return rpy_all(ctx, p, mu, done);
+    return 0;
+  };
+  auto reduce = [&](int mode) -> int {
+    if (dist) {
+      if (int rc = allreduce_chunks(ctx)) return rc;
+    }
+    return launch_finalize(ctx, mode, red);
+  };
+
+  // Steps 1-5: gamma_0, g_0 = M gamma_0 + q, phi_0
+  double* gam0 = ctx->gam[0].p;
+  if (opts->warm_start) {
+    SC_CUDA(cudaMemcpyAsync(gam0, dgam, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    // projection onto gamma >= 0 via the proj kernel with alpha = 0 (Step 1)
+    if (int rc = launch_proj_own(ctx, gam0, gam0, gam0, 0, nc)) return rc;
+    if (int rc = mvop_raw(gam0)) return rc;
+    if (int rc = launch_dt(ctx, 2, gam0, nullptr, nullptr, ctx->g[0].p, c0, c1)) return rc;
+  } else {
+    SC_CUDA(cudaMemsetAsync(gam0, 0, nc * sizeof(double), ctx->stream));
+    SC_CUDA(cudaMemsetAsync(ctx->u4.p, 0, sizeof(double4) * (spheres ? std::max(ctx->npad, p.rpr * ctx->world)
+                                                                       : 2 * ctx->npad),
+                            ctx->stream));
+    if (int rc = launch_dt(ctx, 3, gam0, nullptr, nullptr, ctx->g[0].p, c0, c1)) return rc;
+  }
+  if (int rc = reduce(2)) return rc;
+  stt.mvops = 1;
+  if (int rc = read_scalars(ctx)) return rc;
+  int rc_final = SC_OK;
+  int parity = 0;
+  if (ctx->hsc->nonfinite) return fail(ctx, SC_ENONFINITE, "non-finite initial gradient");
+  if (!ctx->hsc->done) {
+    // Step 6: alpha_0 = g0.g0 / g0.M g0 (second MVOP, on the full g_0)
+    if (dist) {
+      if (int rc = bcast_slices(ctx, p, ctx->g[0].p)) return rc;
+    }
+    if (int rc = mvop_raw(ctx->g[0].p)) return rc;
+    if (int rc = launch_dt(ctx, 1, nullptr, nullptr, ctx->g[0].p, nullptr, c0, c1)) return rc;
+    if (int rc = reduce(1)) return rc;
+    stt.mvops = 2;
+    // Steps 7-16
+    const int batch = (n >= 32768 || dist) ? 1 : (n >= 4096 ? 4 : 16);
+    int enq = 0;
+    while (enq < opts->max_iter) {
+      const int nb = std::min(batch, opts->max_iter - enq);
+      for (int k = 0; k < nb; ++k) {
+        const int pp = (enq + k) & 1;
+        double* go = ctx->g[pp].p;
+        double* gmo = ctx->gam[pp].p;
+        double* gmn = ctx->gam[pp ^ 1].p;
+        double* gn = ctx->g[pp ^ 1].p;
+        if (dist) {
+          if (int rc = launch_proj_own(ctx, gmo, go, gmn, p.l0, p.l1)) return rc;
+          if (int rc = bcast_slices(ctx, p, gmn)) return rc;
+          if (int rc = mvop_raw(gmn)) return rc;
+        } else {
+          if (int rc = launch_gather_proj(ctx, gmo, go, gmn, mu)) return rc;
+          if (spheres) {
+            if (int rc = rpy_all(ctx, p, mu, done)) return rc;
+          }
+        }
+        if (int rc = launch_dt(ctx, 0, gmn, gmo, go, gn, c0, c1)) return rc;
+        if (int rc = reduce(0)) return rc;
+      }
+      enq += nb;
+      if (int rc = read_scalars(ctx)) return rc;
+      if (ctx->hsc->done) break;
+    }
+    parity = ctx->hsc->iter & 1;
+    stt.iters = ctx->hsc->iter;
+    stt.mvops = 2 + ctx->hsc->iter;
+  }
+  const DevScalars& s = *ctx->hsc;
+  if (s.nonfinite) return fail(ctx, SC_ENONFINITE, "non-finite value in the BBPGD iteration");
+  stt.converged = s.conv;
+  stt.residual = s.phi;
+  stt.alpha = s.alpha;
+  stt.bb_breakdowns = s.breakdowns;
+  if (!s.conv && !opts->fixed_iters) rc_final = SC_NOT_CONVERGED;
+  double* gfin = ctx->gam[parity].p;
+  double* gradfin = ctx->g[parity].p;
+  if (dist) {
+    if (int rc = bcast_slices(ctx, p, gradfin)) return rc;
+  }
+  if (int rc = check_flag(ctx, SC_EDEGENERATE, "coincident centres in the RPY sum")) return rc;
+  // outputs
+  SC_CUDA(cudaMemcpyAsync(dgam, gfin, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (dg) SC_CUDA(cudaMemcpyAsync(dg, gradfin, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (dF) {
+    if (int rc = launch_gather_raw(ctx, gfin, mu, dF)) return rc;
+  }
+  if (dU) {
+    if (stt.iters == 0 && stt.mvops >= 2) {  // j_max = 0: u4 holds the alpha_0 product, recompute
+      if (int rc = mvop_raw(gfin)) return rc;
+    }
+    if (spheres) {
+      if (int rc = launch_unpack_uw_spheres(ctx, ctx->u4.p, nullptr, mu, dU)) return rc;
+    } else {
+      if (int rc = launch_rod_unpack(ctx, ctx->u4.p, dU)) return rc;
+    }
+  }
+  int32_t* dact = ctx->derr;  // reuse the flag word as a counter
+  SC_CUDA(cudaMemsetAsync(dact, 0, sizeof(int32_t), ctx->stream));
+  if (int rc = launch_count_active(ctx, gfin, dact)) return rc;
+  SC_CUDA(cudaMemcpyAsync(ctx->herr, dact, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  SC_CUDA(cudaMemsetAsync(dact, 0, sizeof(int32_t), ctx->stream));
+  if (int rc = st.finish()) return rc;
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  stt.active = *ctx->herr;
+  *ctx->herr = 0;
+  if (stats) *stats = stt;
+  return rc_final;
+}
+
+int sc_collision_step(sc_ctx* ctx, const sc_problem* prob, const sc_bbpgd_opts* opts, double* Fc_out,
+                      double* Uc_out, int64_t* n_c, sc_bbpgd_stats* stats) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (prob == nullptr || opts == nullptr || !(prob->dt > 0.0) || !(prob->mu > 0.0))
+    return fail(ctx, SC_EINVAL, "collision_step: bad arguments");
+  int rc;
+  int64_t nc = 0;
+  if (prob->kind == 0)
+    rc = sc_build_contacts_spheres(ctx, prob->n, prob->pos, prob->radius, prob->gap_abs, prob->gap_rel, &nc);
+  else
+    rc = sc_build_contacts_rods(ctx, prob->n, prob->pos, prob->dir, prob->length, prob->b, prob->gap_abs, &nc);
+  if (rc != SC_OK) return rc;
+  if ((rc = sc_assemble_D(ctx)) != SC_OK) return rc;
+  const int64_t n = prob->n;
+  if ((rc = ensure(ctx, ctx->w, 6 * std::max<int64_t>(n, 1)))) return rc;
+  rc = sc_mobility_apply(ctx, prob->mu, prob->F_ext, ctx->w.p);  // U_ext = M F_ext (Step 1)
+  if (rc == SC_OK) rc = sc_lcp_q(ctx, prob->dt, ctx->w.p, nullptr);
+  if (rc != SC_OK) return rc;
+  if ((rc = ensure(ctx, ctx->gam_user, std::max<int64_t>(nc, 1)))) return rc;
+  sc_bbpgd_opts o = *opts;
+  o.mu = prob->mu;
+  o.warm_start = 0;
+  rc = sc_bbpgd_solve(ctx, &o, ctx->gam_user.p, nullptr, Fc_out, Uc_out, stats);
+  if (n_c) *n_c = nc;
+  return rc;
+}
+
+// ------------------------------------------------------------ measurement
+int sc_set_timing(sc_ctx* ctx, int enable) {
+  if (ctx == nullptr) return SC_EINVAL;
+  ctx->timer.enabled = enable != 0;
+  return SC_OK;
+}
+int sc_get_timing(sc_ctx* ctx, int family, double* total_ms, int64_t* launches) {
+  if (ctx == nullptr || family < 0 || family >= SC_K_COUNT) return SC_EINVAL;
+  cudaSetDevice(ctx->device);
+  timer_collect(ctx);
+  if (total_ms) *total_ms = ctx->timer.total_ms[family];
+  if (launches) *launches = ctx->timer.launches[family];
+  return SC_OK;
+}
+int sc_reset_timing(sc_ctx* ctx) {
+  if (ctx == nullptr) return SC_EINVAL;
+  timer_collect(ctx);
+  for (int f = 0; f < SC_K_COUNT; ++f) {
+    ctx->timer.total_ms[f] = 0.0;
+    ctx->timer.launches[f] = 0;
+  }
+  return SC_OK;
+}
+int64_t sc_launch_count(const sc_ctx* ctx) { return ctx ? ctx->launch_count : -1; }
+
+}  // extern "C"

@@ -1,0 +1,472 @@
+// lcp.cu -- (a3) projection + D-gather, (a5) D^T + fused BB reductions, and the
+// small kernels around the BBPGD loop (Alg. 1).
+//
+// K-GATHER (a3): per body b, F_b = sum_{l ∋ b} sigma_bl D_l,b gamma_l with
+//   gamma_l = max(0, gamma_l^old - alpha g_l^old)   (Steps 8-9)
+// recomputed identically by both incident bodies; the first body (owner)
+// writes gamma_l.  For rods the 6x6 drag mobility is applied in the same
+// thread (U = M_b F_b), so the rods MVOP is one gather + one D^T pass.
+// K-DT (a5): per constraint g_l = n.(U_i - U_j) [+ (r_i x n).W_i - (r_j x n).W_j] + q_l
+//   (Step 10), fused with the partial sums of s.s, s.y, y.y and min(gamma, g)^2
+//   (Steps 11, 14-15) over a FIXED chunking: chunk c = constraints
+//   whose first body lies in [256c, 256c+256).  One CTA per chunk, fixed-order
+//   tree -> the sums are independent of the launch shape and of the number of GPUs.
+// K-FINALIZE: one CTA sums the chunk partials in fixed order and applies the
+//   BB1/BB2 update, the convergence test and the breakdown rule (reading A5).
+#include <cmath>
+
+#include "sc_internal.h"
+
+namespace sc {
+namespace {
+
+constexpr int kT = 256;
+inline unsigned nblk(int64_t n) { return static_cast<unsigned>((n + kT - 1) / kT); }
+
+enum GatherMode { kProj = 0, kRaw = 1 };
+enum GatherOut { kOutF4 = 0, kOutRodU = 1, kOutFT = 2 };
+
+template <int KIND, int MODE, int OUT>
+__global__ void __launch_bounds__(kT) gather_kernel(
+    const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ inc, const double4* __restrict__ nrm4,
+    const double4* __restrict__ rxn4, const double* __restrict__ a, const double* __restrict__ g_old,
+    double* __restrict__ gam_new, const DevScalars* __restrict__ dsc, int64_t n, int64_t nout,
+    const double4* __restrict__ dir4, const double4* __restrict__ mob4, double4* __restrict__ out4,
+    double* __restrict__ outFT, const int32_t* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= nout) return;
+  if (b >= n) {  // padded source rows: zero force
+    if (OUT == kOutF4) out4[b] = make_double4(0, 0, 0, 0);
+    if (OUT == kOutRodU) {
+      out4[2 * b] = make_double4(0, 0, 0, 0);
+      out4[2 * b + 1] = make_double4(0, 0, 0, 0);
+    }
+    return;
+  }
+  const double alpha = MODE == kProj ? dsc->alpha : 0.0;
+  double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
+  const int32_t e0 = row_ptr[b], e1 = row_ptr[b + 1];
+  for (int32_t e = e0; e < e1; ++e) {
+    const int32_t v = inc[e];
+    const int32_t l = v >> 1;
+    const int side = v & 1;
+    double gm;
+    if (MODE == kProj) {
+      const double x = __dsub_rn(a[l], __dmul_rn(alpha, g_old[l]));  // gamma - alpha g (Step 8)
+      gm = x > 0.0 ? x : 0.0;                                        // projection (Step 9)
+      if (side == 0) gam_new[l] = gm;                                 // owner = first body
+    } else {
+      gm = a[l];
+    }
+    const double4 nv = nrm4[l];
+    const double sg = side ? -gm : gm;
+    fx = fma(sg, nv.x, fx);
+    fy = fma(sg, nv.y, fy);
+    fz = fma(sg, nv.z, fz);
+    if (KIND == kRods) {
+      const double4 rx = rxn4[2 * l + side];
+      tx = fma(sg, rx.x, tx);
+      ty = fma(sg, rx.y, ty);
+      tz = fma(sg, rx.z, tz);
+    }
+  }
+  if (OUT == kOutF4) {
+    out4[b] = make_double4(fx, fy, fz, 0.0);
+  } else if (OUT == kOutFT) {
+    double* o = outFT + 6 * b;
+    o[0] = fx; o[1] = fy; o[2] = fz; o[3] = tx; o[4] = ty; o[5] = tz;
+  } else {
+    // rods: U = (1/zeta_par) t t^T F + (1/zeta_perp) (I - t t^T) F ; W = T / zeta_rot
+    const double4 t = dir4[b];
+    const double4 m = mob4[b];
+    const double tf = fma(t.z, fz, fma(t.y, fy, t.x * fx));
+    const double cpar = (m.x - m.y) * tf;
+    out4[2 * b] = make_double4(fma(m.y, fx, cpar * t.x), fma(m.y, fy, cpar * t.y), fma(m.y, fz, cpar * t.z), 0.0);
+    out4[2 * b + 1] = make_double4(m.z * tx, m.z * ty, m.z * tz, 0.0);
+  }
+}
+
+__device__ __forceinline__ void block_reduce4(double v[4], double* red /* [4][kT] smem */) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) red[k * kT + t] = v[k];
+  __syncthreads();
+  for (int w = kT / 2; w > 0; w >>= 1) {
+    if (t < w) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) red[k * kT + t] += red[k * kT + t + w];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = red[k * kT];
+}
+
+enum DtMode { kDtIter = 0, kDtAlpha0 = 1, kDtG0 = 2, kDtInitQ = 3 };
+
+// One CTA per chunk c in [c0, c0 + gridDim.x).
+template <int KIND, int MODE>
+__global__ void __launch_bounds__(kT) dt_kernel(
+    const int32_t* __restrict__ first_ptr, int64_t n, int64_t c0, const int32_t* __restrict__ ci,
+    const int32_t* __restrict__ cj, const double4* __restrict__ nrm4, const double4* __restrict__ rxn4,
+    const double4* __restrict__ u4, const double* __restrict__ q, const double* __restrict__ gam_new,
+    const double* __restrict__ gam_old, const double* __restrict__ g_old, double* __restrict__ g_out,
+    double* __restrict__ part, const int32_t* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  __shared__ double red[4 * kT];
+  const int64_t c = c0 + blockIdx.x;
+  int64_t blo = c * kChunkBodies, bhi = blo + kChunkBodies;
+  if (blo > n) blo = n;
+  if (bhi > n) bhi = n;
+  const int32_t l0 = first_ptr[blo], l1 = first_ptr[bhi];
+  double p[4] = {0, 0, 0, 0};
+  for (int32_t l = l0 + threadIdx.x; l < l1; l += kT) {
+    double v = 0.0;
+    if (MODE != kDtInitQ) {
+      const int32_t i = ci[l], j = cj[l];
+      const double4 nv = nrm4[l];
+      if (KIND == kSpheres) {
+        const double4 ui = u4[i], uj = u4[j];
+        v = fma(nv.z, ui.z - uj.z, fma(nv.y, ui.y - uj.y, nv.x * (ui.x - uj.x)));
+      } else {
+        const double4 ui = u4[2 * i], uj = u4[2 * j], wi = u4[2 * i + 1], wj = u4[2 * j + 1];
+        const double4 ra = rxn4[2 * l], rb = rxn4[2 * l + 1];
+        v = fma(nv.z, ui.z - uj.z, fma(nv.y, ui.y - uj.y, nv.x * (ui.x - uj.x)));
+        v += fma(ra.z, wi.z, fma(ra.y, wi.y, ra.x * wi.x)) - fma(rb.z, wj.z, fma(rb.y, wj.y, rb.x * wj.x));
+      }
+    }
+    if (MODE == kDtIter) {
+      const double g = v + q[l];
+      g_out[l] = g;
+      const double gn = gam_new[l];
+      const double s = gn - gam_old[l];
+      const double y = g - g_old[l];
+      const double m = gn < g ? gn : g;
+      p[0] = fma(s, s, p[0]);
+      p[1] = fma(s, y, p[1]);
+      p[2] = fma(y, y, p[2]);
+      p[3] = fma(m, m, p[3]);
+    } else if (MODE == kDtAlpha0) {
+      const double g0 = g_old[l];
+      p[0] = fma(g0, g0, p[0]);
+      p[1] = fma(g0, v, p[1]);
+    } else {  // kDtG0 (warm start: g0 = D^T U + q) / kDtInitQ (gamma0 = 0: g0 = q)
+      const double g = (MODE == kDtG0 ? v : 0.0) + q[l];
+      g_out[l] = g;
+      const double gn = gam_new[l];
+      const double m = gn < g ? gn : g;
+      p[3] = fma(m, m, p[3]);
+    }
+  }
+  block_reduce4(p, red);
+  if (threadIdx.x < 4) part[c * 4 + threadIdx.x] = p[threadIdx.x];
+}
+
+// Sums chunk partials in fixed order and advances the BBPGD scalars.
+// mode 0: after Step 10 of iteration j; mode 1: alpha_0 (Step 6); mode 2: phi_0 (Step 3).
+__global__ void __launch_bounds__(kT) finalize_kernel(const double* __restrict__ part, int64_t nchunks, int mode,
+                                                      DevScalars* __restrict__ s) {
+  if (s->done) return;
+  __shared__ double red[4 * kT];
+  double p[4] = {0, 0, 0, 0};
+  for (int64_t c = threadIdx.x; c < nchunks; c += kT) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p[k] += part[c * 4 + k];
+  }
+  block_reduce4(p, red);
+  if (threadIdx.x != 0) return;
+  for (int k = 0; k < 4; ++k) s->p[k] = p[k];
+  if (mode == 1) {
+    const double a = p[0] / p[1];  // alpha_0 = g0.g0 / g0.M g0
+    if (!(isfinite(a) && a > 0.0)) {
+      s->nonfinite = 1;
+      s->done = 1;
+    } else {
+      s->alpha = a;
+    }
+    return;
+  }
+  const double phi = sqrt(p[3]);
+  s->phi = phi;
+  if (!isfinite(phi)) {
+    s->nonfinite = 1;
+    s->done = 1;
+    return;
+  }
+  s->conv = phi < s->tol ? 1 : 0;
+  if (mode == 2) {
+    if (s->conv) s->done = 1;
+    return;
+  }
+  const int j = s->iter + 1;
+  s->iter = j;
+  if (s->fixed) {
+    if (j >= s->max_iter) {
+      s->done = 1;
+      return;
+    }
+  } else if (s->conv || j >= s->max_iter) {
+    s->done = 1;
+    return;
+  }
+  const bool bb2 = s->bb_mode == 1 || (s->bb_mode == 2 && (j % 2 == 0));
+  const double a_new = bb2 ? p[1] / p[2] : p[0] / p[1];
+  if (p[1] > 0.0 && isfinite(a_new) && a_new > 0.0) {
+    s->alpha = a_new;
+  } else {
+    s->breakdowns += 1;  // reading A5: keep the previous alpha
+  }
+}
+
+__global__ void proj_own_kernel(const double* __restrict__ gam_old, const double* __restrict__ g_old,
+                                double* __restrict__ gam_new, const DevScalars* __restrict__ dsc, int64_t l0,
+                                int64_t l1) {
+  if (dsc->done) return;
+  const int64_t l = l0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (l >= l1) return;
+  const double x = __dsub_rn(gam_old[l], __dmul_rn(dsc->alpha, g_old[l]));
+  gam_new[l] = x > 0.0 ? x : 0.0;
+}
+
+__global__ void pack_ft_kernel(const double* __restrict__ FT, int64_t n, int64_t npad, double4* __restrict__ f4,
+                               double4* __restrict__ t4) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= npad) return;
+  if (b < n) {
+    const double* f = FT + 6 * b;
+    f4[b] = make_double4(f[0], f[1], f[2], 0.0);
+    t4[b] = make_double4(f[3], f[4], f[5], 0.0);
+  } else {
+    f4[b] = make_double4(0, 0, 0, 0);
+    t4[b] = make_double4(0, 0, 0, 0);
+  }
+}
+
+__global__ void unpack_spheres_kernel(const double4* __restrict__ u4, const double4* __restrict__ t4,
+                                      const double4* __restrict__ pos4, double rot_scale, int64_t n,
+                                      double* __restrict__ UW) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  const double4 u = u4[b];
+  const double a = 2.0 * pos4[b].w;
+  const double r = rot_scale / (a * a * a);  // W = T / (8 pi mu a^3)
+  double* o = UW + 6 * b;
+  o[0] = u.x; o[1] = u.y; o[2] = u.z;
+  if (t4 != nullptr) {
+    const double4 t = t4[b];
+    o[3] = r * t.x; o[4] = r * t.y; o[5] = r * t.z;
+  } else {
+    o[3] = 0.0; o[4] = 0.0; o[5] = 0.0;
+  }
+}
+
+__global__ void rod_drag_user_kernel(const double* __restrict__ FT, const double4* __restrict__ dir4,
+                                     const double4* __restrict__ mob4, int64_t n, double* __restrict__ UW) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  const double* f = FT + 6 * b;
+  const double4 t = dir4[b];
+  const double4 m = mob4[b];
+  const double tf = fma(t.z, f[2], fma(t.y, f[1], t.x * f[0]));
+  const double cpar = (m.x - m.y) * tf;
+  double* o = UW + 6 * b;
+  o[0] = fma(m.y, f[0], cpar * t.x);
+  o[1] = fma(m.y, f[1], cpar * t.y);
+  o[2] = fma(m.y, f[2], cpar * t.z);
+  o[3] = m.z * f[3];
+  o[4] = m.z * f[4];
+  o[5] = m.z * f[5];
+}
+
+__global__ void rod_unpack_kernel(const double4* __restrict__ u4, int64_t n, double* __restrict__ UW) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  const double4 u = u4[2 * b], w = u4[2 * b + 1];
+  double* o = UW + 6 * b;
+  o[0] = u.x; o[1] = u.y; o[2] = u.z; o[3] = w.x; o[4] = w.y; o[5] = w.z;
+}
+
+// out_l = D_l^T UW (+ gap_l * qscale if addq)
+template <int KIND>
+__global__ void dt_user_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj,
+                               const double4* __restrict__ nrm4, const double4* __restrict__ rxn4,
+                               const double* __restrict__ UW, int64_t nc, int addgap, double inv_dt,
+                               double* __restrict__ out) {
+  const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (l >= nc) return;
+  const double* ui = UW + 6 * static_cast<int64_t>(ci[l]);
+  const double* uj = UW + 6 * static_cast<int64_t>(cj[l]);
+  const double4 nv = nrm4[l];
+  double v = nv.x * (ui[0] - uj[0]) + nv.y * (ui[1] - uj[1]) + nv.z * (ui[2] - uj[2]);
+  if (KIND == kRods) {
+    const double4 ra = rxn4[2 * l], rb = rxn4[2 * l + 1];
+    v += (ra.x * ui[3] + ra.y * ui[4] + ra.z * ui[5]) - (rb.x * uj[3] + rb.y * uj[4] + rb.z * uj[5]);
+  }
+  out[l] = addgap ? nv.w * inv_dt + v : v;  // q = Phi/dt + D^T U_nc
+}
+
+__global__ void count_active_kernel(const double* __restrict__ gam, int64_t nc, int32_t* __restrict__ out) {
+  __shared__ int32_t s;
+  if (threadIdx.x == 0) s = 0;
+  __syncthreads();
+  int32_t c = 0;
+  for (int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; l < nc;
+       l += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    c += gam[l] > 0.0 ? 1 : 0;
+  atomicAdd(&s, c);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(out, s);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+int launch_gather_proj(sc_ctx* ctx, const double* gam_old, const double* g_old, double* gam_new, double mu) {
+  (void)mu;
+  const int32_t* done = &ctx->dsc->done;
+  timer_begin(ctx, SC_K_GATHER);
+  if (ctx->kind == kSpheres)
+    gather_kernel<kSpheres, kProj, kOutF4><<<nblk(ctx->npad), kT, 0, ctx->stream>>>(
+        ctx->row_ptr.p, ctx->inc.p, ctx->nrm4.p, nullptr, gam_old, g_old, gam_new, ctx->dsc, ctx->n, ctx->npad,
+        nullptr, nullptr, ctx->f4.p, nullptr, done);
+  else
+    gather_kernel<kRods, kProj, kOutRodU><<<nblk(ctx->npad), kT, 0, ctx->stream>>>(
+        ctx->row_ptr.p, ctx->inc.p, ctx->nrm4.p, ctx->rxn4.p, gam_old, g_old, gam_new, ctx->dsc, ctx->n,
+        ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done);
+  timer_end(ctx, SC_K_GATHER);
+  return check_launch(ctx, "gather_proj");
+}
+
+int launch_gather_raw(sc_ctx* ctx, const double* v, double mu, double* FT_user) {
+  (void)mu;
+  timer_begin(ctx, SC_K_GATHER);
+  if (FT_user != nullptr) {
+    if (ctx->kind == kSpheres)
+      gather_kernel<kSpheres, kRaw, kOutFT><<<nblk(ctx->n), kT, 0, ctx->stream>>>(
+          ctx->row_ptr.p, ctx->inc.p, ctx->nrm4.p, nullptr, v, nullptr, nullptr, ctx->dsc, ctx->n, ctx->n,
+          nullptr, nullptr, nullptr, FT_user, nullptr);
+    else
+      gather_kernel<kRods, kRaw, kOutFT><<<nblk(ctx->n), kT, 0, ctx->stream>>>(
+          ctx->row_ptr.p, ctx->inc.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n, ctx->n,
+          nullptr, nullptr, nullptr, FT_user, nullptr);
+  } else {
+    const int32_t* done = &ctx->dsc->done;
+    if (ctx->kind == kSpheres)
+      gather_kernel<kSpheres, kRaw, kOutF4><<<nblk(ctx->npad), kT, 0, ctx->stream>>>(
+          ctx->row_ptr.p, ctx->inc.p, ctx->nrm4.p, nullptr, v, nullptr, nullptr, ctx->dsc, ctx->n, ctx->npad,
+          nullptr, nullptr, ctx->f4.p, nullptr, done);
+    else
+      gather_kernel<kRods, kRaw, kOutRodU><<<nblk(ctx->npad), kT, 0, ctx->stream>>>(
+          ctx->row_ptr.p, ctx->inc.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n,
+          ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done);
+  }
+  timer_end(ctx, SC_K_GATHER);
+  return check_launch(ctx, "gather_raw");
+}
+
+int launch_proj_own(sc_ctx* ctx, const double* gam_old, const double* g_old, double* gam_new, int64_t l0,
+                    int64_t l1) {
+  if (l1 <= l0) return 0;
+  timer_begin(ctx, SC_K_GATHER);
+  proj_own_kernel<<<nblk(l1 - l0), kT, 0, ctx->stream>>>(gam_old, g_old, gam_new, ctx->dsc, l0, l1);
+  timer_end(ctx, SC_K_GATHER);
+  return check_launch(ctx, "proj_own");
+}
+
+int launch_dt(sc_ctx* ctx, int mode, const double* gam_new, const double* gam_old, const double* g_old,
+              double* g_out, int64_t c0, int64_t c1) {
+  if (c1 <= c0) return 0;
+  const unsigned grid = static_cast<unsigned>(c1 - c0);
+  const int32_t* done = &ctx->dsc->done;
+  const double4* u4 = ctx->u4.p;
+  double* part = ctx->chunk_part.p;
+  const double* q = ctx->q.p;
+#define SC_DT(KIND, MODE)                                                                                      \
+  dt_kernel<KIND, MODE><<<grid, kT, 0, ctx->stream>>>(ctx->first_ptr.p, ctx->n, c0, ctx->ci.p, ctx->cj.p,      \
+                                                      ctx->nrm4.p, ctx->rxn4.p, u4, q, gam_new, gam_old, g_old, \
+                                                      g_out, part, done)
+  timer_begin(ctx, SC_K_DT);
+  if (ctx->kind == kSpheres) {
+    switch (mode) {
+      case kDtIter: SC_DT(kSpheres, kDtIter); break;
+      case kDtAlpha0: SC_DT(kSpheres, kDtAlpha0); break;
+      case kDtG0: SC_DT(kSpheres, kDtG0); break;
+      default: SC_DT(kSpheres, kDtInitQ); break;
+    }
+  } else {
+    switch (mode) {
+      case kDtIter: SC_DT(kRods, kDtIter); break;
+      case kDtAlpha0: SC_DT(kRods, kDtAlpha0); break;
+      case kDtG0: SC_DT(kRods, kDtG0); break;
+      default: SC_DT(kRods, kDtInitQ); break;
+    }
+  }
+#undef SC_DT
+  timer_end(ctx, SC_K_DT);
+  return check_launch(ctx, "dt");
+}
+
+int launch_finalize(sc_ctx* ctx, int mode, const double* part) {
+  timer_begin(ctx, SC_K_FINALIZE);
+  finalize_kernel<<<1, kT, 0, ctx->stream>>>(part, ctx->nchunks, mode, ctx->dsc);
+  timer_end(ctx, SC_K_FINALIZE);
+  return check_launch(ctx, "finalize");
+}
+
+int launch_pack_ft(sc_ctx* ctx, const double* FT, double4* f4, double4* t4) {
+  timer_begin(ctx, SC_K_MISC);
+  pack_ft_kernel<<<nblk(ctx->npad), kT, 0, ctx->stream>>>(FT, ctx->n, ctx->npad, f4, t4);
+  timer_end(ctx, SC_K_MISC);
+  return check_launch(ctx, "pack_ft");
+}
+
+int launch_unpack_uw_spheres(sc_ctx* ctx, const double4* u4, const double4* t4, double mu, double* UW) {
+  if (ctx->n == 0) return 0;
+  const double rot = 1.0 / (8.0 * 3.14159265358979323846 * mu);
+  timer_begin(ctx, SC_K_MISC);
+  unpack_spheres_kernel<<<nblk(ctx->n), kT, 0, ctx->stream>>>(u4, t4, ctx->pos4.p, rot, ctx->n, UW);
+  timer_end(ctx, SC_K_MISC);
+  return check_launch(ctx, "unpack_spheres");
+}
+
+int launch_rod_drag_user(sc_ctx* ctx, const double* FT, double mu, double* UW) {
+  (void)mu;
+  if (ctx->n == 0) return 0;
+  timer_begin(ctx, SC_K_MISC);
+  rod_drag_user_kernel<<<nblk(ctx->n), kT, 0, ctx->stream>>>(FT, ctx->dir4.p, ctx->rodmob4.p, ctx->n, UW);
+  timer_end(ctx, SC_K_MISC);
+  return check_launch(ctx, "rod_drag_user");
+}
+
+int launch_rod_unpack(sc_ctx* ctx, const double4* u4, double* UW) {
+  if (ctx->n == 0) return 0;
+  timer_begin(ctx, SC_K_MISC);
+  rod_unpack_kernel<<<nblk(ctx->n), kT, 0, ctx->stream>>>(u4, ctx->n, UW);
+  timer_end(ctx, SC_K_MISC);
+  return check_launch(ctx, "rod_unpack");
+}
+
+int launch_dt_user(sc_ctx* ctx, const double* UW, double* out, const double* addq, double qscale) {
+  if (ctx->nc == 0) return 0;
+  const int addgap = addq != nullptr ? 1 : 0;
+  timer_begin(ctx, SC_K_DT);
+  if (ctx->kind == kSpheres)
+    dt_user_kernel<kSpheres><<<nblk(ctx->nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, ctx->nrm4.p, nullptr,
+                                                                     UW, ctx->nc, addgap, qscale, out);
+  else
+    dt_user_kernel<kRods><<<nblk(ctx->nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, ctx->nrm4.p,
+                                                                  ctx->rxn4.p, UW, ctx->nc, addgap, qscale, out);
+  timer_end(ctx, SC_K_DT);
+  return check_launch(ctx, "dt_user");
+}
+
+int launch_count_active(sc_ctx* ctx, const double* gam, int32_t* out) {
+  if (ctx->nc == 0) return 0;
+  timer_begin(ctx, SC_K_MISC);
+  count_active_kernel<<<148, kT, 0, ctx->stream>>>(gam, ctx->nc, out);
+  timer_end(ctx, SC_K_MISC);
+  return check_launch(ctx, "count_active");
+}
+
+}  // namespace sc

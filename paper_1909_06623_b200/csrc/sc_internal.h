@@ -1,0 +1,197 @@
+// sc_internal.h -- internal declarations of libstokescol (B200, sm_100a, FP64).
+// Not part of the C ABI (see include/stokescol.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "stokescol.h"
+
+namespace sc {
+
+constexpr int kRpyThreads = 128;        // threads per RPY CTA
+constexpr int kRpyTpt = 2;              // targets per thread
+constexpr int kRpyRows = kRpyThreads * kRpyTpt;  // 256 target rows per CTA
+constexpr int kRpyTile = 128;           // sources per shared-memory tile
+constexpr int kChunkBodies = 256;       // B_c: bodies per reduction chunk
+constexpr int kPartials = 4;            // doubles per chunk partial
+
+enum BodyKind { kNone = -1, kSpheres = 0, kRods = 1 };
+
+// Device-side solver scalars (one struct in device memory; mirrored to pinned host).
+struct DevScalars {
+  double alpha;      // current BB step alpha_{j}
+  double phi;        // last residual
+  double p[4];       // last reduced partials
+  double tol;
+  int32_t iter;      // GD steps done
+  int32_t done;      // 1: stop (converged, j_max or error)
+  int32_t conv;      // phi < tol at the last evaluation
+  int32_t breakdowns;
+  int32_t nonfinite;
+  int32_t max_iter;
+  int32_t bb_mode;
+  int32_t fixed;
+  int32_t err;       // contact degeneracy etc.
+  int32_t pad;
+};
+
+struct KernelTimer {
+  bool enabled = false;
+  std::vector<cudaEvent_t> ev[SC_K_COUNT];  // pairs (start, stop)
+  double total_ms[SC_K_COUNT] = {};
+  int64_t launches[SC_K_COUNT] = {};
+  std::vector<cudaEvent_t> pool;
+};
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;  // capacity in elements
+};
+
+}  // namespace sc
+
+struct sc_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int64_t launch_count = 0;
+  sc::KernelTimer timer;
+
+  // multi-GPU
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+
+  // bodies
+  int kind = sc::kNone;
+  int64_t n = 0, npad = 0;      // npad: multiple of kRpyRows * world
+  int poly = 0;                 // spheres: radii not all equal
+  double a_const = 1.0;
+  double rod_b = 0.5;
+  sc::DBuf<double4> pos4;       // spheres: (x,y,z,a/2); rods: (x,y,z,L)
+  sc::DBuf<double4> dir4;       // rods: (tx,ty,tz,0)
+  sc::DBuf<double4> rodmob4;    // rods: (1/zeta_par, 1/zeta_perp, 1/zeta_rot, mu) for rod_mu
+  double rod_mu = -1.0;
+
+  // contacts (sorted by (i,j))
+  int64_t nc = 0;
+  sc::DBuf<int32_t> ci, cj;
+  sc::DBuf<double4> nrm4;       // (nx,ny,nz,gap)
+  sc::DBuf<double4> lev4;       // rods: [2*l] = r_i, [2*l+1] = r_j (w = 0)
+  sc::DBuf<double4> rxn4;       // rods: [2*l] = r_i x n, [2*l+1] = r_j x n
+  bool assembled = false;
+  sc::DBuf<int32_t> row_ptr;    // n+1
+  sc::DBuf<int32_t> inc;        // 2*nc: (l << 1) | side
+  sc::DBuf<int32_t> first_ptr;  // n+1: constraints with first body < b start at first_ptr[b]
+  int64_t nchunks = 0;
+  std::vector<int32_t> h_first_ptr;  // host copy (chunk bounds, ownership)
+
+  // LCP state
+  bool have_q = false;
+  sc::DBuf<double> q;
+  sc::DBuf<double> gam[2], g[2], w, gam_user;
+  sc::DBuf<double> chunk_part;  // nchunks * 4
+  sc::DBuf<double> chunk_red;   // reduced (allreduce output)
+  sc::DBuf<double4> f4;         // sources: (Fx,Fy,Fz,0) [npad]
+  sc::DBuf<double4> t4;         // torques for the public mobility apply [npad]
+  sc::DBuf<double4> u4;         // velocities (Ux,Uy,Uz,0) [npad] (spheres) or [2*npad] (rods: U, W)
+  sc::DBuf<double> rpy_part;    // nsplit * rows * 3
+  int nsplit = 1;
+  sc::DevScalars* dsc = nullptr;   // device scalars
+  sc::DevScalars* hsc = nullptr;   // pinned mirror
+  int32_t* derr = nullptr;         // device error flag
+  int32_t* herr = nullptr;         // pinned mirror
+
+  // scratch for contacts
+  sc::DBuf<double> bbox_part;
+  sc::DBuf<int32_t> cell_of, cell_cnt, cell_start, sorted_idx, pair_cnt, pair_off, scan_tmp;
+  sc::DBuf<double4> sorted4, sorted_dir4;
+
+  // staging for host pointers
+  sc::DBuf<char> stage;
+};
+
+namespace sc {
+
+// ---- error helpers -------------------------------------------------------
+int fail(sc_ctx* c, int code, const std::string& msg);
+int cuda_fail(sc_ctx* c, cudaError_t e, const char* what);
+#define SC_CUDA(call)                                        \
+  do {                                                       \
+    cudaError_t e_ = (call);                                 \
+    if (e_ != cudaSuccess) return sc::cuda_fail(ctx, e_, #call); \
+  } while (0)
+
+template <typename T>
+int ensure(sc_ctx* ctx, DBuf<T>& b, size_t n) {
+  if (b.n >= n && b.p) return 0;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.n = 0;
+  size_t want = n > 0 ? n : 1;
+  cudaError_t e = cudaMalloc(&b.p, want * sizeof(T));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc");
+  b.n = want;
+  return 0;
+}
+template <typename T>
+void release(DBuf<T>& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.n = 0;
+}
+
+// ---- launch accounting ---------------------------------------------------
+void timer_begin(sc_ctx* ctx, int family);
+void timer_end(sc_ctx* ctx, int family);
+int check_launch(sc_ctx* ctx, const char* what);
+
+// ---- scans (scan.cu) -------------------------------------------------------
+// exclusive scan of n int32 into out (out[n] = total); tmp sized by scan_tmp_size(n).
+size_t scan_tmp_size(int64_t n);
+int exclusive_scan_i32(sc_ctx* ctx, const int32_t* in, int32_t* out, int64_t n, int32_t* tmp);
+
+// ---- contacts (contacts.cu) ----------------------------------------------
+int build_contacts_spheres(sc_ctx* ctx, double gap_abs, double gap_rel);
+int build_contacts_rods(sc_ctx* ctx, double gap_thresh);
+
+// ---- assemble (assemble.cu) ----------------------------------------------
+int assemble(sc_ctx* ctx);
+
+// ---- mobility (rpy.cu) ----------------------------------------------------
+// U4[rows row0 .. row0+nrows) = scale * sum_j T_ij f4_j (+ self), from packed
+// sources f4 [npad]; nrows multiple of kRpyRows.  done: optional device flag.
+int rpy_apply_rows(sc_ctx* ctx, const double4* f4, int64_t row0, int64_t nrows, double mu,
+                   double4* u4, const int32_t* done);
+int choose_nsplit(int64_t npad, int world);
+
+// ---- LCP kernels (lcp.cu) -------------------------------------------------
+// gather F = D v (mode raw) or F = D max(0, gam_old - alpha g_old) with the owner
+// writing gam_new (mode proj).  Output: f4 (spheres) or u4 after the drag (rods, fused)
+// or a user FT (n x 6).
+int launch_gather_proj(sc_ctx* ctx, const double* gam_old, const double* g_old, double* gam_new,
+                       double mu);
+int launch_gather_raw(sc_ctx* ctx, const double* v, double mu, double* FT_user /*nullable*/);
+int launch_proj_own(sc_ctx* ctx, const double* gam_old, const double* g_old, double* gam_new,
+                    int64_t l0, int64_t l1);
+// D^T: mode 0 iteration (g_new = D^T U + q, partials ss,sy,yy,mm), mode 1 alpha0
+// (w = D^T U, partials g.g, g.w), mode 2 (g = D^T U + q, partial mm) ; chunks [c0,c1)
+int launch_dt(sc_ctx* ctx, int mode, const double* gam_new, const double* gam_old,
+              const double* g_old, double* g_out, int64_t c0, int64_t c1);
+int launch_dt_user(sc_ctx* ctx, const double* UW, double* out, const double* addq, double qscale);
+int launch_finalize(sc_ctx* ctx, int mode, const double* part);
+int launch_init_g0(sc_ctx* ctx, const double* q, double* g0, int64_t c0, int64_t c1);
+int launch_pack_ft(sc_ctx* ctx, const double* FT, double4* f4, double4* t4);
+int launch_unpack_uw_spheres(sc_ctx* ctx, const double4* u4, const double4* t4, double mu, double* UW);
+int launch_rod_drag_user(sc_ctx* ctx, const double* FT, double mu, double* UW);
+int launch_rod_unpack(sc_ctx* ctx, const double4* u4, double* UW);
+int launch_count_active(sc_ctx* ctx, const double* gam, int32_t* out);
+int launch_q(sc_ctx* ctx, double dt, const double* dtu, double* q);
+
+}  // namespace sc

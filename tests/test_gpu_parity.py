@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * contact pair set, gaps and normals: bit-exact;
+  * mobility apply: relative L2 <= 1e-12;
+  * final gamma: relative L2 <= 1e-6, and D gamma too (reading A19);
+    complementarity residual phi <= 1e-8 on both sides.
+Small cases span several 256-row tiles with a ragged tail; full BASELINE sizes
+are checked on sampled outputs the oracle computes one by one.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1909_06623_b200 import Context, ScError
+from paper_1909_06623_b200.synthetic import make_problem
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def _cuda(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _relL2(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300))
+
+
+def _gpu_contacts(ctx, p):
+    if p.kind == "spheres":
+        ctx.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+        return ctx.get_contacts()
+    ctx.build_contacts_rods(_cuda(p.pos), _cuda(p.direction), _cuda(p.length), p.rod_radius, p.gap_abs)
+    return ctx.get_contacts(lever=True)
+
+
+def _assert_contacts_equal(g, o):
+    assert g["i"].shape[0] == o.nc
+    np.testing.assert_array_equal(_np(g["i"]), o.i)
+    np.testing.assert_array_equal(_np(g["j"]), o.j)
+    # bit-exact (reading A20): compare the raw bits
+    np.testing.assert_array_equal(_np(g["gap"]).view(np.int64), o.gap.view(np.int64))
+    np.testing.assert_array_equal(_np(g["normal"]).view(np.int64), o.normal.view(np.int64))
+    if o.lever is not None:
+        np.testing.assert_array_equal(_np(g["lever"]).view(np.int64), o.lever.view(np.int64))
+
+
+# ---------------------------------------------------------------- (a1)
+@pytest.mark.parametrize("name,n", [("C1", None), ("C2", None), ("C3", None), ("C5", None), ("C2", 1000),
+                                    ("C1", 1), ("C1", 2), ("C3", 777)])
+def test_contacts_bit_exact_spheres(ctx, name, n):
+    p = make_problem(name, n=n)
+    g = _gpu_contacts(ctx, p)
+    o = oracle.contacts_spheres(p.pos, p.radius, p.gap_abs, p.gap_rel, method="grid")
+    _assert_contacts_equal(g, o)
+
+
+@pytest.mark.parametrize("n", [3000, 50000])
+def test_contacts_bit_exact_rods(ctx, n):
+    p = make_problem("C4", n=n)
+    g = _gpu_contacts(ctx, p)
+    o = oracle.contacts_rods(p.pos, p.direction, p.length, p.rod_radius, p.gap_abs)
+    _assert_contacts_equal(g, o)
+
+
+def test_contacts_hand_cases_and_errors(ctx):
+    pos = np.array([[0.0, 0, 0], [2.05, 0, 0], [4.1, 0, 0]])
+    nc = ctx.build_contacts_spheres(_cuda(pos), _cuda(np.ones(3)), 0.0, 0.1)
+    c = ctx.get_contacts()
+    assert nc == 2 and _np(c["i"]).tolist() == [0, 1] and _np(c["j"]).tolist() == [1, 2]
+    # host (numpy) pointers are accepted by the same entry point
+    assert ctx.build_contacts_spheres(pos, np.ones(3), 0.0, 0.1) == 2
+    # empty body set
+    assert ctx.build_contacts_spheres(_cuda(np.zeros((0, 3))), None, 0.0, 0.1) == 0
+    # coincident centres -> SC_EDEGENERATE
+    with pytest.raises(ScError) as e:
+        ctx.build_contacts_spheres(_cuda(np.zeros((2, 3))), None, 0.0, 0.1)
+    assert e.value.code == -2
+    with pytest.raises(ScError) as e:
+        ctx.build_contacts_spheres(_cuda(np.zeros((2, 3))), _cuda(np.array([1.0, -1.0])), 0.0, 0.1)
+    assert e.value.code == -1
+
+
+# ---------------------------------------------------------------- (a2)
+@pytest.mark.parametrize("name,n", [("C2", 3000), ("C4", 20000)])
+def test_apply_D_DT_and_q(ctx, name, n):
+    p = make_problem(name, n=n)
+    _gpu_contacts(ctx, p)
+    ctx.assemble_D()
+    sysm = oracle.system_for(p)
+    rng = np.random.default_rng(1)
+    gam = rng.uniform(0, 3, sysm.ct.nc)
+    F = _np(ctx.apply_D(_cuda(gam)))
+    Fo = oracle.apply_D(p.n, sysm.ct, gam)
+    np.testing.assert_allclose(F, Fo, rtol=0, atol=1e-13 * np.abs(Fo).max())
+    U = rng.normal(size=(p.n, 6))
+    w = _np(ctx.apply_DT(_cuda(U)))
+    wo = oracle.apply_DT(p.n, sysm.ct, U)
+    np.testing.assert_allclose(w, wo, rtol=0, atol=1e-13 * np.abs(wo).max())
+    q = _np(ctx.lcp_q(p.dt, _cuda(U)))
+    qo = sysm.lcp_q(p.dt, U)
+    np.testing.assert_allclose(q, qo, rtol=0, atol=1e-13 * np.abs(qo).max())
+
+
+# ---------------------------------------------------------------- (a4)
+@pytest.mark.parametrize("name,n", [("C1", None), ("C2", None), ("C1", 1000), ("C2", 300), ("C1", 1)])
+def test_mobility_full_parity(ctx, name, n):
+    p = make_problem(name, n=n)
+    _gpu_contacts(ctx, p)
+    rng = np.random.default_rng(4)
+    FT = rng.normal(size=(p.n, 6))
+    U = _np(ctx.mobility_apply(_cuda(FT), mu=p.mu))
+    Uo = oracle.rpy_apply(p.pos, p.radius, p.mu, FT)
+    assert _relL2(U[:, :3], Uo[:, :3]) <= 1e-12
+    assert _relL2(U[:, 3:], Uo[:, 3:]) <= 1e-14
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_mobility_full_size_sampled_rows(ctx, name):
+    """Full BASELINE size, the launch configuration the bench times; oracle rows one by one."""
+    p = make_problem(name)
+    _gpu_contacts(ctx, p)
+    FT = p.force.copy()
+    U = _np(ctx.mobility_apply(_cuda(FT), mu=p.mu))
+    rows = sorted(set([0, 1, 255, 256, p.n // 2, p.n - 257, p.n - 1] +
+                      np.random.default_rng(0).integers(0, p.n, 25).tolist()))
+    for r in rows:
+        Uo = oracle.rpy_apply_rows(p.pos, p.radius, p.mu, FT, r, r + 1)[0]
+        assert np.linalg.norm(U[r, :3] - Uo[:3]) <= 1e-12 * np.linalg.norm(Uo[:3]), r
+        np.testing.assert_allclose(U[r, 3:], Uo[3:], rtol=1e-14, atol=1e-300)
+
+
+def test_mobility_rods(ctx):
+    p = make_problem("C4", n=5000)
+    _gpu_contacts(ctx, p)
+    FT = np.random.default_rng(2).normal(size=(p.n, 6))
+    U = _np(ctx.mobility_apply(_cuda(FT)))
+    Uo = oracle.rod_drag_apply(p.direction, p.length, p.rod_radius, p.mu, FT)
+    assert _relL2(U, Uo) <= 1e-14
+
+
+def test_mobility_two_far_spheres_finite(ctx):
+    pos = np.array([[0.0, 0, 0], [10.0, 0, 0]])
+    ctx.build_contacts_spheres(_cuda(pos), None, 0.0, 0.1)
+    ok = ctx.mobility_apply(_cuda(np.ones((2, 6))))
+    assert torch.isfinite(ok).all()
+
+
+# ---------------------------------------------------------------- (a3-a6)
+def _gpu_solve(ctx, p, **kw):
+    _gpu_contacts(ctx, p)
+    ctx.assemble_D()
+    U = ctx.mobility_apply(_cuda(p.force), mu=p.mu)
+    ctx.lcp_q(p.dt, U)
+    fixed = kw.pop("fixed_iters", p.fixed_iters)
+    jmax = kw.pop("max_iter", fixed if fixed else p.max_iter)
+    return ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=jmax, fixed_iters=bool(fixed), **kw)
+
+
+@pytest.mark.parametrize("name,n", [("C1", None), ("C2", 2048), ("C3", 2000), ("C5", 3000), ("C4", 20000)])
+def test_bbpgd_converged_parity(ctx, name, n):
+    p = make_problem(name, n=n, fixed_iters=0)
+    r = _gpu_solve(ctx, p)
+    o = oracle.solve_problem(p)
+    assert o["status"] == 0 and o["residual"] < 1e-8
+    assert r["status"] == 0 and r["converged"] == 1 and r["residual"] < 1e-8
+    gam = _np(r["gamma"])
+    assert gam.min() >= 0.0
+    assert _relL2(gam, o["gamma"]) <= 1e-6
+    assert _relL2(_np(r["Fc"]), o["Fc"]) <= 1e-6
+    assert _relL2(_np(r["Uc"]), o["Uc"]) <= 1e-6
+    assert r["mvops"] == r["iters"] + 2
+    # the GPU's g is the gradient at its gamma (oracle MVOP on the GPU's gamma: certificate)
+    sysm = o["system"]
+    g_cert = sysm.mvop(gam) + o["q"]
+    scale = np.abs(o["q"]).max()
+    np.testing.assert_allclose(_np(r["g"]), g_cert, rtol=0, atol=1e-10 * scale)
+    assert oracle.minmap_residual(gam, g_cert) < 1e-8
+    # iteration counts: parity unpinned (BB is non-monotone and roundoff-sensitive);
+    # only a gross mismatch fails
+    assert r["iters"] <= 2 * o["iters"] + 20 and o["iters"] <= 2 * r["iters"] + 20
+    assert r["active"] == int(np.sum(gam > 0))
+
+
+@pytest.mark.parametrize("name,n", [("C2", 2048), ("C4", 20000)])
+def test_bbpgd_lockstep_fixed_iterations(ctx, name, n):
+    p = make_problem(name, n=n)
+    r = _gpu_solve(ctx, p, fixed_iters=1, max_iter=12)
+    o = oracle.solve_problem(p, max_iter=12, fixed_iters=1)
+    assert r["iters"] == 12 and r["mvops"] == 14 and r["status"] == 0
+    assert _relL2(_np(r["gamma"]), o["gamma"]) <= 1e-9
+    assert abs(r["residual"] - o["residual"]) <= 1e-6 * o["residual"]
+
+
+def test_bbpgd_closed_form_headon(ctx):
+    # two unit spheres at r = 2.05, +-200 along the line (tests/golden/headon_two_sphere.txt)
+    pos = np.array([[0.0, 0, 0], [2.05, 0, 0]])
+    F = np.zeros((2, 6)); F[0, 0] = 200.0; F[1, 0] = -200.0
+    ctx.build_contacts_spheres(_cuda(pos), None, 0.0, 0.1)
+    ctx.assemble_D()
+    ctx.lcp_q(0.01, ctx.mobility_apply(_cuda(F)))
+    r = ctx.bbpgd_solve(tol=1e-10)
+    assert _np(r["gamma"])[0] == pytest.approx(77.398904942398094, rel=1e-12)
+    assert r["iters"] <= 1
+    # q >= 0: gamma = 0 after one MVOP
+    F[0, 0], F[1, 0] = 100.0, -100.0
+    ctx.lcp_q(0.01, ctx.mobility_apply(_cuda(F)))
+    r = ctx.bbpgd_solve(tol=1e-10)
+    assert r["mvops"] == 1 and r["iters"] == 0 and _np(r["gamma"])[0] == 0.0
+
+
+def test_bbpgd_no_contacts_and_warm_start(ctx):
+    pos = np.array([[0.0, 0, 0], [5.0, 0, 0]])
+    ctx.build_contacts_spheres(_cuda(pos), None, 0.0, 0.1)
+    ctx.assemble_D()
+    ctx.lcp_q(0.01, _cuda(np.zeros((2, 6))))
+    r = ctx.bbpgd_solve()
+    assert r["converged"] == 1 and r["mvops"] == 0
+    assert float(r["Fc"].abs().max()) == 0.0
+    # warm start from the converged gamma: 1 MVOP
+    p = make_problem("C1")
+    r = _gpu_solve(ctx, p)
+    r2 = ctx.bbpgd_solve(mu=p.mu, tol=p.tol, gamma0=r["gamma"].clone())
+    assert r2["iters"] <= 3 and r2["converged"] == 1
+
+
+def test_collision_step_host_buffers(ctx):
+    """The e2e entry point with host (numpy) buffers equals the device path."""
+    p = make_problem("C1")
+    Fc = np.zeros((p.n, 6)); Uc = np.zeros((p.n, 6))
+    r = ctx.collision_step("spheres", p.pos, p.force, radius=p.radius, gap_abs=p.gap_abs, gap_rel=p.gap_rel,
+                           mu=p.mu, dt=p.dt, tol=p.tol, max_iter=p.max_iter, Fc_out=Fc, Uc_out=Uc)
+    o = oracle.solve_problem(p)
+    assert r["status"] == 0 and r["nc"] == o["system"].ct.nc
+    assert _relL2(Fc, o["Fc"]) <= 1e-6 and _relL2(Uc, o["Uc"]) <= 1e-6
+
+
+def test_c5_bench_configuration_certificate(ctx):
+    """C5 at full size, fixed 50 iterations (the bench's launch configuration):
+    sampled constraints' gradients against the oracle's rows, plus invariants."""
+    p = make_problem("C5")
+    r = _gpu_solve(ctx, p)
+    assert r["iters"] == 50 and r["mvops"] == 52 and r["status"] == 0
+    gam = _np(r["gamma"])
+    assert gam.min() >= 0.0
+    ct = oracle.contacts_spheres(p.pos, p.radius, p.gap_abs, p.gap_rel)
+    F = oracle.apply_D(p.n, ct, gam)
+    np.testing.assert_allclose(_np(r["Fc"]), F, rtol=0, atol=1e-12 * np.abs(F).max())
+    # Newton's third law on F_c
+    assert np.abs(F[:, :3].sum(0)).max() < 1e-9 * np.abs(F).sum()
+    # sampled g_l = n.(U_i - U_j) + q_l: U rows from the oracle's RPY on F_c + F_ext
+    rng = np.random.default_rng(5)
+    ls = rng.choice(ct.nc, 24, replace=False)
+    bodies = sorted(set(ct.i[ls].tolist()) | set(ct.j[ls].tolist()))
+    FT = F + p.force
+    Uo = {b: oracle.rpy_apply_rows(p.pos, p.radius, p.mu, FT, b, b + 1)[0] for b in bodies}
+    g = _np(r["g"])
+    for l in ls:
+        i, j = ct.i[l], ct.j[l]
+        go = float(np.dot(ct.normal[l], Uo[i][:3] - Uo[j][:3])) + ct.gap[l] / p.dt
+        assert abs(g[l] - go) <= 1e-9 * (1 + abs(go)) + 1e-9, (l, g[l], go)
