@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdio>
 
+#include "rpy_common.cuh"
 #include "sc_internal.h"
 
 namespace sc {
@@ -247,6 +248,43 @@ __global__ void pair_search(const double4* __restrict__ s4, const double4* __res
   if (!EMIT) cnt[i] = count;
 }
 
+// Near list for the RPY overlap branch: every j != i with r_ij < 2 abar (the predicate of
+// rpy_common.cuh, bit-identical to the far-field kernel's).  Pass 1 counts, pass 2 emits;
+// one thread per cell-sorted body, output indexed by the body's own index.
+template <bool EMIT>
+__global__ void near_search(const double4* __restrict__ s4, const int32_t* __restrict__ sidx,
+                            const int32_t* __restrict__ cell_start, int64_t n, Grid g, bool poly,
+                            long long near_bits, int32_t* __restrict__ cnt, const int32_t* __restrict__ off,
+                            int32_t* __restrict__ out) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const double4 pi = s4[s];
+  const int32_t i = sidx[s];
+  const int kx = cell_coord(pi.x, g.lo[0], g.inv_h, g.m[0]);
+  const int ky = cell_coord(pi.y, g.lo[1], g.inv_h, g.m[1]);
+  const int kz = cell_coord(pi.z, g.lo[2], g.inv_h, g.m[2]);
+  int32_t count = 0;
+  int32_t o = EMIT ? off[i] : 0;
+  for (int z = max(kz - 1, 0); z <= min(kz + 1, g.m[2] - 1); ++z)
+    for (int y = max(ky - 1, 0); y <= min(ky + 1, g.m[1] - 1); ++y) {
+      const int crow = (z * g.m[1] + y) * g.m[0];
+      const int t0 = cell_start[crow + max(kx - 1, 0)], t1 = cell_start[crow + min(kx + 1, g.m[0] - 1) + 1];
+      for (int t = t0; t < t1; ++t) {
+        const int32_t j = sidx[t];
+        if (j == i) continue;
+        const double4 pj = s4[t];
+        double dx, dy, dz;
+        const double r2 = rpy_r2(pi, pj, dx, dy, dz);
+        if (!rpy_is_near(r2, pi.w + pj.w, poly, near_bits)) continue;
+        if (EMIT)
+          out[o++] = j;
+        else
+          ++count;
+      }
+    }
+  if (!EMIT) cnt[i] = count;
+}
+
 // Sort each body's partner list by j (lists are short: insertion sort in place).
 __global__ void sort_partners(const int32_t* __restrict__ off, int64_t n, int32_t* __restrict__ cj) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -448,6 +486,35 @@ int build_common(sc_ctx* ctx, SphereTest st, RodTest rt) {
                                                       ctx->nrm4.p, ctx->lev4.p, ctx->derr);
     timer_end(ctx, SC_K_CONTACTS);
     if (int rc = check_launch(ctx, "geometry")) return rc;
+  }
+  if (kind == kSpheres) {
+    // near list (pairs in the RPY overlap branch), both directions, sorted per body
+    if (int rc = ensure(ctx, ctx->near_ptr, n + 1)) return rc;
+    const double a0 = ctx->a_const;
+    const double n2 = 4.0 * (a0 * a0);
+    const long long nb = *reinterpret_cast<const long long*>(&n2);
+    timer_begin(ctx, SC_K_CONTACTS);
+    near_search<false><<<nblk(n), kT, 0, ctx->stream>>>(ctx->sorted4.p, ctx->sorted_idx.p, ctx->cell_start.p, n,
+                                                        g, ctx->poly != 0, nb, ctx->pair_cnt.p, nullptr, nullptr);
+    timer_end(ctx, SC_K_CONTACTS);
+    if (int rc = check_launch(ctx, "near_count")) return rc;
+    if (int rc = exclusive_scan_i32(ctx, ctx->pair_cnt.p, ctx->near_ptr.p, n, ctx->scan_tmp.p)) return rc;
+    int32_t nn = 0;
+    SC_CUDA(cudaMemcpyAsync(&nn, ctx->near_ptr.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    SC_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (int rc = ensure(ctx, ctx->near_idx, nn)) return rc;
+    if (nn > 0) {
+      timer_begin(ctx, SC_K_CONTACTS);
+      near_search<true><<<nblk(n), kT, 0, ctx->stream>>>(ctx->sorted4.p, ctx->sorted_idx.p, ctx->cell_start.p, n,
+                                                         g, ctx->poly != 0, nb, nullptr, ctx->near_ptr.p,
+                                                         ctx->near_idx.p);
+      timer_end(ctx, SC_K_CONTACTS);
+      if (int rc = check_launch(ctx, "near_emit")) return rc;
+      timer_begin(ctx, SC_K_CONTACTS);
+      sort_partners<<<nblk(n), kT, 0, ctx->stream>>>(ctx->near_ptr.p, n, ctx->near_idx.p);
+      timer_end(ctx, SC_K_CONTACTS);
+      if (int rc = check_launch(ctx, "near_sort")) return rc;
+    }
   }
   ctx->h_first_ptr.resize(n + 1);
   SC_CUDA(cudaMemcpyAsync(ctx->h_first_ptr.data(), ctx->first_ptr.p, sizeof(int32_t) * (n + 1),

@@ -24,6 +24,7 @@
 //    compensated (TwoSum) add of each tile sum.
 #include <cstdio>
 
+#include "rpy_common.cuh"
 #include "sc_internal.h"
 
 namespace sc {
@@ -60,25 +61,6 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
-__device__ __forceinline__ double rsqrt_dp(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  // cubic correction: e = 1 - x y^2, y' = y (1 + e/2 + 3 e^2/8)  (error 2^-20 -> ~2^-52)
-  double h = x * y;
-  double e = fma(-h, y, 1.0);
-  double p = fma(0.375, e, 0.5);
-  double t = y * e;
-  return fma(t, p, y);
-}
-
-__device__ __forceinline__ void two_sum_acc(double& hi, double& lo, double v) {
-  double s = hi + v;
-  double bp = s - hi;
-  double err = (hi - (s - bp)) + (v - bp);
-  hi = s;
-  lo += err;
-}
-
 struct Consts {
   double k23a2;   // (2/3) a^2          (mono)
   double m2a2;    // -2 a^2             (mono)
@@ -88,65 +70,98 @@ struct Consts {
   long long near_bits;  // bits of (2a)^2  (mono)
 };
 
-// One (target, source) pair: acc += c1 f + c2 (d.f) d.
-template <bool POLY>
-__device__ __forceinline__ void rpy_pair(const double4& pi, const double4& pj, const double4& fj,
-                                         const Consts& k, int64_t i, int64_t j, double& ax, double& ay,
-                                         double& az, int32_t* err) {
-  const double dx = pj.x - pi.x;
-  const double dy = pj.y - pi.y;
-  const double dz = pj.z - pi.z;
-  const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-  const double rinv = rsqrt_dp(r2);
-  const double rinv2 = rinv * rinv;
-  const double rinv3 = rinv * rinv2;
-  double c1, c2;
-  bool near;
-  double abar = 0.0, abar2 = 0.0;
+// Far-field contributions of TPT targets x SU sources, branch-free and written stage by
+// stage over the KK = TPT*SU independent pair chains so the FP64 instruction stream
+// interleaves them (the pipe is latency-bound on a single chain):
+//   acc_t += c1 f + c2 (d.f) d  with the far coefficients, or nothing when the pair is
+//   "near" (r < 2 abar, which includes the self pair r = 0).  Near pairs are in the
+//   near list built with the contacts (same predicate, rpy_common.cuh); rpy_combine adds
+//   their overlap-branch contribution.  c1 = c2 = 0 is selected with FSEL (not the FP64
+//   pipe), which also discards the NaN that rsqrt(0) produces for the self pair.
+template <bool POLY, int TPT, int SU>
+__device__ __forceinline__ void rpy_far_block(const double4 (&p)[TPT], const double4* __restrict__ tp,
+                                              const double4* __restrict__ tf, int q, const Consts& k,
+                                              double (&ax)[TPT], double (&ay)[TPT], double (&az)[TPT]) {
+  constexpr int KK = TPT * SU;
+  double4 pj[SU], fj[SU];
+#pragma unroll
+  for (int u = 0; u < SU; ++u) {
+    pj[u] = tp[q + u];
+    fj[u] = tf[q + u];
+  }
+  double dx[KK], dy[KK], dz[KK], r2[KK], y[KK], h[KK], e[KK], c1[KK], c2[KK];
+#pragma unroll
+  for (int c = 0; c < KK; ++c) {
+    const int t = c % TPT, u = c / TPT;
+    r2[c] = rpy_r2(p[t], pj[u], dx[c], dy[c], dz[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < KK; ++c) asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y[c]) : "d"(r2[c]));
+  // cubic correction e = 1 - r2 y^2, rinv = y + y e (1/2 + 3e/8): 2^-20 -> 2^-52
+#pragma unroll
+  for (int c = 0; c < KK; ++c) h[c] = r2[c] * y[c];
+#pragma unroll
+  for (int c = 0; c < KK; ++c) e[c] = fma(-h[c], y[c], 1.0);
+#pragma unroll
+  for (int c = 0; c < KK; ++c) {
+    h[c] = fma(0.375, e[c], 0.5);
+    e[c] = y[c] * e[c];
+  }
+#pragma unroll
+  for (int c = 0; c < KK; ++c) y[c] = fma(e[c], h[c], y[c]);  // rinv
+#pragma unroll
+  for (int c = 0; c < KK; ++c) h[c] = y[c] * y[c];  // rinv^2
+#pragma unroll
+  for (int c = 0; c < KK; ++c) e[c] = y[c] * h[c];  // rinv^3
+  bool nr[KK];
   if (POLY) {
-    abar = pi.w + pj.w;  // (a_i + a_j)/2 from stored half radii
-    abar2 = abar * abar;
-    const double s = abar2 * rinv2;
-    c1 = rinv * fma(s, 2.0 / 3.0, 1.0);
-    c2 = rinv3 * fma(s, -2.0, 1.0);
-    near = r2 < 4.0 * abar2;
+#pragma unroll
+    for (int c = 0; c < KK; ++c) {
+      const int t = c % TPT, u = c / TPT;
+      const double abar = p[t].w + pj[u].w;  // (a_i + a_j)/2 from stored half radii
+      const double abar2 = abar * abar;
+      const double s = abar2 * h[c];
+      c1[c] = y[c] * fma(s, 2.0 / 3.0, 1.0);
+      c2[c] = e[c] * fma(s, -2.0, 1.0);
+      nr[c] = rpy_is_near(r2[c], abar, true, 0);
+    }
   } else {
-    c1 = fma(k.k23a2, rinv3, rinv);
-    c2 = rinv3 * fma(k.m2a2, rinv2, 1.0);
-    near = __double_as_longlong(r2) < k.near_bits;  // r2 >= 0: integer order == numeric order
-  }
-  if (near) {  // overlapping pair or the self pair (rare: warp-divergent branch)
-    double r, rs;
-    if (r2 > 0.0) {
-      r = r2 * rinv;
-      rs = rinv;
-    } else {
-      r = 0.0;
-      rs = 0.0;
-      if (j != i) atomicExch(err, 1);  // coincident centres (reading A12)
-    }
-    if (POLY) {
-      const double ia = 1.0 / abar;
-      c1 = (4.0 / 3.0) * ia * fma(-9.0 / 32.0 * ia, r, 1.0);
-      c2 = 0.125 * ia * ia * rs;
-    } else {
-      c1 = k.kn1 * fma(k.kn2, r, 1.0);
-      c2 = k.kn3 * rs;
+#pragma unroll
+    for (int c = 0; c < KK; ++c) {
+      c1[c] = fma(k.k23a2, e[c], y[c]);
+      c2[c] = e[c] * fma(k.m2a2, h[c], 1.0);
+      nr[c] = rpy_is_near(r2[c], 0.0, false, k.near_bits);
     }
   }
-  const double rf = fma(dz, fj.z, fma(dy, fj.y, dx * fj.x));
-  const double t = c2 * rf;
-  ax = fma(t, dx, fma(c1, fj.x, ax));
-  ay = fma(t, dy, fma(c1, fj.y, ay));
-  az = fma(t, dz, fma(c1, fj.z, az));
+#pragma unroll
+  for (int c = 0; c < KK; ++c) {
+    c1[c] = nr[c] ? 0.0 : c1[c];
+    c2[c] = nr[c] ? 0.0 : c2[c];
+  }
+#pragma unroll
+  for (int c = 0; c < KK; ++c) {
+    const int u = c / TPT;
+    h[c] = fma(dz[c], fj[u].z, fma(dy[c], fj[u].y, dx[c] * fj[u].x));  // d.f
+  }
+#pragma unroll
+  for (int c = 0; c < KK; ++c) c2[c] *= h[c];
+#pragma unroll
+  for (int c = 0; c < KK; ++c) {
+    const int t = c % TPT, u = c / TPT;
+    ax[t] = fma(c2[c], dx[c], fma(c1[c], fj[u].x, ax[t]));
+    ay[t] = fma(c2[c], dy[c], fma(c1[c], fj[u].y, ay[t]));
+    az[t] = fma(c2[c], dz[c], fma(c1[c], fj[u].z, az[t]));
+  }
 }
 
-// grid: (row blocks, nsplit).  block: kRpyThreads.  dynamic smem: 2 stages x 2 x kRpyTile double4 + bars.
+// grid: (row blocks of kRpyRows, nsplit).  block: kRpyThreads (= kRpyRows / kRpyTpt).
+// dynamic smem: 2 stages x (positions, forces) x kRpyTile double4 + 2 mbarriers.
 template <bool POLY>
-__global__ void __launch_bounds__(kRpyThreads, 3)
-    rpy_partial_kernel(const double4* __restrict__ pos4, const double4* __restrict__ f4, int64_t npad,
+__global__ void __launch_bounds__(kRpyThreads)
+    rpy_partial_kernel(const double4* __restrict__ pos4, const double4* __restrict__ f4, int64_t npad, int64_t n,
                        int64_t src_per_split, int64_t row0, int64_t nrows, Consts k,
                        double* __restrict__ part, const int32_t* __restrict__ done, int32_t* err) {
+  constexpr int TPT = kRpyTpt, NT = kRpyThreads, SU = kRpySu;
   if (done != nullptr && *done) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double4* sp = reinterpret_cast<double4*>(smem_raw);        // [2][kRpyTile] positions
@@ -156,15 +171,14 @@ __global__ void __launch_bounds__(kRpyThreads, 3)
   const int tid = threadIdx.x;
   const int split = blockIdx.y;
   const int64_t rloc = static_cast<int64_t>(blockIdx.x) * kRpyRows;  // row offset within [row0, row0+nrows)
-  const int64_t i0 = row0 + rloc + tid;
-  const int64_t i1 = i0 + kRpyThreads;
   const int64_t s0 = static_cast<int64_t>(split) * src_per_split;
   int64_t s1 = s0 + src_per_split;
   if (s1 > npad) s1 = npad;
   const int ntiles = s0 < s1 ? static_cast<int>((s1 - s0) / kRpyTile) : 0;
 
-  const double4 p0 = pos4[i0];
-  const double4 p1 = pos4[i1];
+  double4 p[TPT];
+#pragma unroll
+  for (int t = 0; t < TPT; ++t) p[t] = pos4[row0 + rloc + tid + t * NT];
   constexpr uint32_t kTileBytes = kRpyTile * sizeof(double4);
 
   if (tid == 0) {
@@ -181,31 +195,28 @@ __global__ void __launch_bounds__(kRpyThreads, 3)
     }
   }
 
-  double hx0 = 0, hy0 = 0, hz0 = 0, lx0 = 0, ly0 = 0, lz0 = 0;
-  double hx1 = 0, hy1 = 0, hz1 = 0, lx1 = 0, ly1 = 0, lz1 = 0;
-  for (int t = 0; t < ntiles; ++t) {
-    const int st = t & 1;
-    mbar_wait(&bar[st], (t >> 1) & 1);
+  double hx[TPT], hy[TPT], hz[TPT], lx[TPT], ly[TPT], lz[TPT];
+#pragma unroll
+  for (int t = 0; t < TPT; ++t) hx[t] = hy[t] = hz[t] = lx[t] = ly[t] = lz[t] = 0.0;
+  for (int tl = 0; tl < ntiles; ++tl) {
+    const int st = tl & 1;
+    mbar_wait(&bar[st], (tl >> 1) & 1);
     const double4* tp = sp + st * kRpyTile;
     const double4* tf = sf + st * kRpyTile;
-    const int64_t jb = s0 + static_cast<int64_t>(t) * kRpyTile;
-    double ax0 = 0, ay0 = 0, az0 = 0, ax1 = 0, ay1 = 0, az1 = 0;
-#pragma unroll 2
-    for (int q = 0; q < kRpyTile; ++q) {
-      const double4 pj = tp[q];
-      const double4 fj = tf[q];
-      rpy_pair<POLY>(p0, pj, fj, k, i0, jb + q, ax0, ay0, az0, err);
-      rpy_pair<POLY>(p1, pj, fj, k, i1, jb + q, ax1, ay1, az1, err);
+    double ax[TPT], ay[TPT], az[TPT];
+#pragma unroll
+    for (int t = 0; t < TPT; ++t) ax[t] = ay[t] = az[t] = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < kRpyTile; q += SU) rpy_far_block<POLY, TPT, SU>(p, tp, tf, q, k, ax, ay, az);
+#pragma unroll
+    for (int t = 0; t < TPT; ++t) {
+      two_sum_acc(hx[t], lx[t], ax[t]);
+      two_sum_acc(hy[t], ly[t], ay[t]);
+      two_sum_acc(hz[t], lz[t], az[t]);
     }
-    two_sum_acc(hx0, lx0, ax0);
-    two_sum_acc(hy0, ly0, ay0);
-    two_sum_acc(hz0, lz0, az0);
-    two_sum_acc(hx1, lx1, ax1);
-    two_sum_acc(hy1, ly1, ay1);
-    two_sum_acc(hz1, lz1, az1);
     __syncthreads();  // every thread is done with stage st
-    if (tid == 0 && t + 2 < ntiles) {
-      const int64_t sb = s0 + static_cast<int64_t>(t + 2) * kRpyTile;
+    if (tid == 0 && tl + 2 < ntiles) {
+      const int64_t sb = s0 + static_cast<int64_t>(tl + 2) * kRpyTile;
       mbar_expect_tx(&bar[st], 2 * kTileBytes);
       tma_load_1d(sp + st * kRpyTile, pos4 + sb, kTileBytes, &bar[st]);
       tma_load_1d(sf + st * kRpyTile, f4 + sb, kTileBytes, &bar[st]);
@@ -213,18 +224,26 @@ __global__ void __launch_bounds__(kRpyThreads, 3)
   }
   // partial layout: [split][row][3], row relative to row0
   double* o = part + (static_cast<int64_t>(split) * nrows + rloc) * 3;
-  o[tid * 3 + 0] = hx0 + lx0;
-  o[tid * 3 + 1] = hy0 + ly0;
-  o[tid * 3 + 2] = hz0 + lz0;
-  o[(tid + kRpyThreads) * 3 + 0] = hx1 + lx1;
-  o[(tid + kRpyThreads) * 3 + 1] = hy1 + ly1;
-  o[(tid + kRpyThreads) * 3 + 2] = hz1 + lz1;
+#pragma unroll
+  for (int t = 0; t < TPT; ++t) {
+    const int r = tid + t * NT;
+    o[r * 3 + 0] = hx[t] + lx[t];
+    o[r * 3 + 1] = hy[t] + ly[t];
+    o[r * 3 + 2] = hz[t] + lz[t];
+  }
 }
 
-// U4[row0 + r] = scale * sum_s part[s][r] in fixed split order (compensated).
+// U4[row0 + r] = scale * (sum_s part[s][r]  +  self term  +  overlap-branch terms of the
+// near list), summed in a fixed order with TwoSum.  Near pair (r < 2 abar):
+//   T = (1/(6 pi mu abar)) [(1 - 9r/(32 abar)) I + (3/(32 abar)) d d^T / r]
+// i.e. with the 1/(8 pi mu) factor hoisted, c1 = (4/(3 abar))(1 - 9r/(32 abar)),
+// c2 = 1/(8 abar^2 r); the self pair (r = 0) gives c1 = 4/(3 a_i), the self mobility.
+template <bool POLY>
 __global__ void rpy_combine_kernel(const double* __restrict__ part, int nsplit, int64_t row0, int64_t nrows,
-                                   int64_t n, double scale, double4* __restrict__ u4,
-                                   const int32_t* __restrict__ done) {
+                                   int64_t n, double scale, const double4* __restrict__ pos4,
+                                   const double4* __restrict__ f4, const int32_t* __restrict__ near_ptr,
+                                   const int32_t* __restrict__ near_idx, double4* __restrict__ u4,
+                                   const int32_t* __restrict__ done, int32_t* __restrict__ err) {
   if (done != nullptr && *done) return;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= nrows) return;
@@ -236,13 +255,42 @@ __global__ void rpy_combine_kernel(const double* __restrict__ part, int nsplit, 
     two_sum_acc(hz, lz, p[2]);
   }
   const int64_t row = row0 + r;
-  double4 u;
-  if (row < n) {
-    u = make_double4(scale * (hx + lx), scale * (hy + ly), scale * (hz + lz), 0.0);
-  } else {
-    u = make_double4(0.0, 0.0, 0.0, 0.0);
+  if (row >= n) {
+    u4[row] = make_double4(0.0, 0.0, 0.0, 0.0);
+    return;
   }
-  u4[row] = u;
+  const double4 pi = pos4[row];
+  const double4 fi = f4[row];
+  const double cs = (2.0 / 3.0) / pi.w;  // 4/(3 a_i), w = a_i/2
+  two_sum_acc(hx, lx, cs * fi.x);
+  two_sum_acc(hy, ly, cs * fi.y);
+  two_sum_acc(hz, lz, cs * fi.z);
+  const double a_mono = 2.0 * pi.w;
+  const long long near_bits = __double_as_longlong(4.0 * (a_mono * a_mono));
+  for (int32_t e = near_ptr[row]; e < near_ptr[row + 1]; ++e) {
+    const int32_t j = near_idx[e];
+    const double4 pj = pos4[j];
+    const double4 fj = f4[j];
+    double dx, dy, dz;
+    const double r2 = rpy_r2(pi, pj, dx, dy, dz);
+    const double abar = POLY ? pi.w + pj.w : a_mono;
+    if (!rpy_is_near(r2, abar, POLY, near_bits)) continue;  // (list built with the same predicate)
+    double rr = 0.0, rs = 0.0;
+    if (r2 > 0.0) {
+      rs = rsqrt_dp(r2);
+      rr = r2 * rs;
+    } else {
+      atomicExch(err, 1);  // coincident centres (reading A12)
+    }
+    const double ia = 1.0 / abar;
+    const double c1 = (4.0 / 3.0) * ia * fma(-9.0 / 32.0 * ia, rr, 1.0);
+    const double c2 = 0.125 * ia * ia * rs;
+    const double t = c2 * fma(dz, fj.z, fma(dy, fj.y, dx * fj.x));
+    two_sum_acc(hx, lx, fma(t, dx, c1 * fj.x));
+    two_sum_acc(hy, ly, fma(t, dy, c1 * fj.y));
+    two_sum_acc(hz, lz, fma(t, dz, c1 * fj.z));
+  }
+  u4[row] = make_double4(scale * (hx + lx), scale * (hy + ly), scale * (hz + lz), 0.0);
 }
 
 constexpr size_t kRpySmem = 4 * kRpyTile * sizeof(double4) + 2 * sizeof(uint64_t);
@@ -284,16 +332,22 @@ int rpy_apply_rows(sc_ctx* ctx, const double4* f4, int64_t row0, int64_t nrows, 
   timer_begin(ctx, SC_K_RPY);
   if (ctx->poly)
     rpy_partial_kernel<true><<<grid, kRpyThreads, kRpySmem, ctx->stream>>>(
-        ctx->pos4.p, f4, ctx->npad, per, row0, nrows, k, ctx->rpy_part.p, done, ctx->derr);
+        ctx->pos4.p, f4, ctx->npad, ctx->n, per, row0, nrows, k, ctx->rpy_part.p, done, ctx->derr);
   else
     rpy_partial_kernel<false><<<grid, kRpyThreads, kRpySmem, ctx->stream>>>(
-        ctx->pos4.p, f4, ctx->npad, per, row0, nrows, k, ctx->rpy_part.p, done, ctx->derr);
+        ctx->pos4.p, f4, ctx->npad, ctx->n, per, row0, nrows, k, ctx->rpy_part.p, done, ctx->derr);
   timer_end(ctx, SC_K_RPY);
   if (int rc = check_launch(ctx, "rpy_partial")) return rc;
   const double scale = 1.0 / (8.0 * 3.14159265358979323846 * mu);
   timer_begin(ctx, SC_K_COMBINE);
-  rpy_combine_kernel<<<static_cast<unsigned>((nrows + 255) / 256), 256, 0, ctx->stream>>>(
-      ctx->rpy_part.p, ns, row0, nrows, ctx->n, scale, u4, done);
+  if (ctx->poly)
+    rpy_combine_kernel<true><<<static_cast<unsigned>((nrows + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->rpy_part.p, ns, row0, nrows, ctx->n, scale, ctx->pos4.p, f4, ctx->near_ptr.p, ctx->near_idx.p, u4,
+        done, ctx->derr);
+  else
+    rpy_combine_kernel<false><<<static_cast<unsigned>((nrows + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->rpy_part.p, ns, row0, nrows, ctx->n, scale, ctx->pos4.p, f4, ctx->near_ptr.p, ctx->near_idx.p, u4,
+        done, ctx->derr);
   timer_end(ctx, SC_K_COMBINE);
   return check_launch(ctx, "rpy_combine");
 }

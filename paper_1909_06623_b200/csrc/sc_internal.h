@@ -13,8 +13,9 @@
 
 namespace sc {
 
-constexpr int kRpyThreads = 128;        // threads per RPY CTA
-constexpr int kRpyTpt = 2;              // targets per thread
+constexpr int kRpyThreads = 64;         // threads per RPY CTA
+constexpr int kRpyTpt = 4;              // targets per thread
+constexpr int kRpySu = 2;               // sources interleaved per step (ILP: TPT*SU pair chains)
 constexpr int kRpyRows = kRpyThreads * kRpyTpt;  // 256 target rows per CTA
 constexpr int kRpyTile = 128;           // sources per shared-memory tile
 constexpr int kChunkBodies = 256;       // B_c: bodies per reduction chunk
@@ -89,6 +90,7 @@ struct sc_ctx {
   sc::DBuf<int32_t> row_ptr;    // n+1
   sc::DBuf<int32_t> inc;        // 2*nc: (l << 1) | side
   sc::DBuf<int32_t> first_ptr;  // n+1: constraints with first body < b start at first_ptr[b]
+  sc::DBuf<int32_t> near_ptr, near_idx;  // spheres: RPY overlap-branch partners per body (CSR)
   int64_t nchunks = 0;
   std::vector<int32_t> h_first_ptr;  // host copy (chunk bounds, ownership)
 
