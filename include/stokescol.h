@@ -187,6 +187,14 @@ int64_t sc_launch_count(const sc_ctx* ctx);
  * [256c, 256c+256). */
 int sc_plan_partition(int64_t n, int world, int rank, int64_t* out7);
 
+/* Testing hook: make a 1-GPU context run the multi-GPU decomposition of `world`
+ * ranks (every rank's share of every step in turn, on this GPU).  The NCCL
+ * collectives become their shared-memory equivalents (broadcast and all-gather
+ * are in place already; the all-reduce of the zero-padded chunk partials is a
+ * copy), so results must be bitwise identical to world = 1.  world = 1 turns it
+ * off.  Errors: SC_EINVAL on a multi-GPU context or world < 1. */
+int sc_set_emulated_world(sc_ctx* ctx, int world);
+
 #ifdef __cplusplus
 }
 #endif

@@ -215,6 +215,10 @@ class Context:
             out[name] = (ms.value, cnt.value)
         return out
 
+    def set_emulated_world(self, world: int):
+        """Testing hook: run the multi-GPU decomposition of `world` ranks on this one GPU."""
+        self._rc(self.lib.sc_set_emulated_world(self._h, int(world)))
+
     def launch_count(self) -> int:
         return int(self.lib.sc_launch_count(self._h))
 

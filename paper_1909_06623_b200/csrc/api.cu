@@ -161,25 +161,23 @@ static void plan_rows(int64_t npad, int world, int rank, int64_t* rpr, int64_t* 
   *hi = std::min(npad, (rank + 1) * *rpr);
 }
 
-static Part partition(const sc_ctx* ctx) {
+static Part partition(const sc_ctx* ctx, int world, int rank) {
   Part p;
   const int64_t n = ctx->n;
   auto fp = [&](int64_t b) -> int64_t { return ctx->h_first_ptr[std::min(b, n)]; };
-  plan_rows(ctx->npad, ctx->world, ctx->rank, &p.rpr, &p.row_lo, &p.row_hi);
+  plan_rows(ctx->npad, world, rank, &p.rpr, &p.row_lo, &p.row_hi);
   p.c0 = p.row_lo / kChunkBodies;
   p.c1 = p.row_hi / kChunkBodies;
   p.l0 = fp(p.row_lo);
   p.l1 = fp(p.row_hi);
-  for (int r = 0; r < ctx->world; ++r) {
+  for (int r = 0; r < world; ++r) {
     int64_t rpr, lo, hi;
-    plan_rows(ctx->npad, ctx->world, r, &rpr, &lo, &hi);
+    plan_rows(ctx->npad, world, r, &rpr, &lo, &hi);
     p.loff.push_back(fp(lo));
     p.lcnt.push_back(fp(hi) - fp(lo));
   }
   return p;
 }
-
-static bool dist_spheres(const sc_ctx* ctx) { return ctx->world > 1 && ctx->kind == kSpheres; }
 
 #define NCCL_CHECK(call)                                                                        \
   do {                                                                                          \
@@ -187,28 +185,85 @@ static bool dist_spheres(const sc_ctx* ctx) { return ctx->world > 1 && ctx->kind
     if (r_ != ncclSuccess) return fail(ctx, SC_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
   } while (0)
 
-// every rank's slice of a length-nc vector -> full vector on every rank
-static int bcast_slices(sc_ctx* ctx, const Part& p, double* v) {
-  NCCL_CHECK(ncclGroupStart());
-  for (int r = 0; r < ctx->world; ++r) {
-    if (p.lcnt[r] == 0) continue;
-    NCCL_CHECK(ncclBroadcast(v + p.loff[r], v + p.loff[r], p.lcnt[r], ncclDouble, r, ctx->comm, ctx->stream));
+// The multi-GPU decomposition.  With world > 1 (NCCL) this
+// process runs its own rank's share and the collectives move data between GPUs.  With an
+// emulated world (sc_set_emulated_world, one GPU) this process runs every rank's share in
+// turn on shared buffers; the collectives become what they amount to on shared memory:
+// broadcast/all-gather are no-ops (every slice is already in place) and the all-reduce of
+// the zero-padded chunk partials is a copy.  No kernel ever waits on another.
+struct Dist {
+  sc_ctx* ctx = nullptr;
+  bool on = false, emul = false;
+  int W = 1;
+  std::vector<Part> parts;
+  std::vector<int> mine;  // ranks computed by this process
+
+  explicit Dist(sc_ctx* c) : ctx(c) {
+    const int ew = c->emul_world;
+    emul = c->world == 1 && ew > 1;
+    W = emul ? ew : c->world;
+    on = W > 1 && c->kind == kSpheres;
+    if (!on) W = 1;
+    for (int r = 0; r < W; ++r) parts.push_back(partition(c, W, r));
+    if (emul || !on)
+      for (int r = 0; r < W; ++r) mine.push_back(r);
+    else
+      mine.push_back(c->rank);
   }
-  NCCL_CHECK(ncclGroupEnd());
-  return 0;
-}
-
-static int allgather_u4(sc_ctx* ctx, const Part& p) {
-  double* base = reinterpret_cast<double*>(ctx->u4.p);
-  NCCL_CHECK(ncclAllGather(base + ctx->rank * p.rpr * 4, base, p.rpr * 4, ncclDouble, ctx->comm, ctx->stream));
-  return 0;
-}
-
-static int allreduce_chunks(sc_ctx* ctx) {
-  NCCL_CHECK(ncclAllReduce(ctx->chunk_part.p, ctx->chunk_red.p, ctx->nchunks * kPartials, ncclDouble, ncclSum,
-                           ctx->comm, ctx->stream));
-  return 0;
-}
+  const Part& own() const { return parts[emul || !on ? 0 : ctx->rank]; }
+  int proj_own(const double* gmo, const double* go, double* gmn) {
+    for (int r : mine)
+      if (int rc = launch_proj_own(ctx, gmo, go, gmn, parts[r].l0, parts[r].l1)) return rc;
+    return 0;
+  }
+  // every rank's constraint slice of v -> full vector on every rank
+  int bcast(double* v) {
+    if (!on || emul) return 0;
+    const Part& p = own();
+    NCCL_CHECK(ncclGroupStart());
+    for (int r = 0; r < W; ++r) {
+      if (p.lcnt[r] == 0) continue;
+      NCCL_CHECK(ncclBroadcast(v + p.loff[r], v + p.loff[r], p.lcnt[r], ncclDouble, r, ctx->comm, ctx->stream));
+    }
+    NCCL_CHECK(ncclGroupEnd());
+    return 0;
+  }
+  // u4 = RPY(f4): own target rows, then all-gather of the rows
+  int rpy(double mu, const int32_t* done) {
+    if (!on) return rpy_apply_rows(ctx, ctx->f4.p, 0, ctx->npad, mu, ctx->u4.p, done);
+    for (int r : mine) {
+      const Part& p = parts[r];
+      if (int rc = rpy_apply_rows(ctx, ctx->f4.p, p.row_lo, p.row_hi - p.row_lo, mu, ctx->u4.p, done)) return rc;
+    }
+    if (emul) return 0;
+    double* base = reinterpret_cast<double*>(ctx->u4.p);
+    const int64_t cnt = own().rpr * 4;
+    NCCL_CHECK(ncclAllGather(base + ctx->rank * cnt, base, cnt, ncclDouble, ctx->comm, ctx->stream));
+    return 0;
+  }
+  int dt(int mode, const double* gam_new, const double* gam_old, const double* g_old, double* g_out) {
+    if (!on) return launch_dt(ctx, mode, gam_new, gam_old, g_old, g_out, 0, ctx->nchunks);
+    for (int r : mine)
+      if (int rc = launch_dt(ctx, mode, gam_new, gam_old, g_old, g_out, parts[r].c0, parts[r].c1)) return rc;
+    return 0;
+  }
+  // chunk partials -> reduced vector; returns the buffer K-FINALIZE reads
+  const double* reduce_chunks() {
+    if (!on) return ctx->chunk_part.p;
+    return ctx->chunk_red.p;
+  }
+  int allreduce() {
+    if (!on) return 0;
+    const size_t cnt = static_cast<size_t>(ctx->nchunks) * kPartials;
+    if (emul) {
+      SC_CUDA(cudaMemcpyAsync(ctx->chunk_red.p, ctx->chunk_part.p, cnt * sizeof(double), cudaMemcpyDeviceToDevice,
+                              ctx->stream));
+      return 0;
+    }
+    NCCL_CHECK(ncclAllReduce(ctx->chunk_part.p, ctx->chunk_red.p, cnt, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    return 0;
+  }
+};
 
 // ------------------------------------------------------------ bodies
 __global__ void set_spheres_kernel(const double* __restrict__ pos, const double* __restrict__ radius, int64_t n,
@@ -309,15 +364,6 @@ static int ensure_rod_mob(sc_ctx* ctx, double mu) {
   }
   ctx->rod_mu = mu;
   return 0;
-}
-
-// spheres: u4 = RPY(f4) for all rows (own rows + all-gather when distributed)
-static int rpy_all(sc_ctx* ctx, const Part& p, double mu, const int32_t* done) {
-  if (dist_spheres(ctx)) {
-    if (int rc = rpy_apply_rows(ctx, ctx->f4.p, p.row_lo, p.row_hi - p.row_lo, mu, ctx->u4.p, done)) return rc;
-    return allgather_u4(ctx, p);
-  }
-  return rpy_apply_rows(ctx, ctx->f4.p, 0, ctx->npad, mu, ctx->u4.p, done);
 }
 
 }  // namespace sc
@@ -625,11 +671,8 @@ int sc_mobility_apply(sc_ctx* ctx, double mu, const double* FT, double* UW) {
   if (int rc = st.out(UW, 6 * ctx->n, &dU)) return rc;
   if (ctx->kind == kSpheres) {
     if (int rc = launch_pack_ft(ctx, dF, ctx->f4.p, ctx->t4.p)) return rc;
-    Part p;
-    if (dist_spheres(ctx)) {
-      plan_rows(ctx->npad, ctx->world, ctx->rank, &p.rpr, &p.row_lo, &p.row_hi);
-    }
-    if (int rc = rpy_all(ctx, p, mu, nullptr)) return rc;
+    Dist D(ctx);
+    if (int rc = D.rpy(mu, nullptr)) return rc;
     if (int rc = launch_unpack_uw_spheres(ctx, ctx->u4.p, ctx->t4.p, mu, dU)) return rc;
     if (int rc = check_flag(ctx, SC_EDEGENERATE, "coincident centres in the RPY sum")) return rc;
   } else {
@@ -701,11 +744,9 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     if (stats) *stats = stt;
     return SC_OK;
   }
-  const Part p = partition(ctx);
-  const bool dist = dist_spheres(ctx);
+  Dist D(ctx);
+  const bool dist = D.on;
   const bool spheres = ctx->kind == kSpheres;
-  const int64_t c0 = dist ? p.c0 : 0, c1 = dist ? p.c1 : ctx->nchunks;
-  const double* red = dist ? ctx->chunk_red.p : ctx->chunk_part.p;
   const int32_t* done = &ctx->dsc->done;
 
   DevScalars h;
@@ -721,14 +762,12 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
   // mvop(v): u4 = Mobility(D v)  (spheres: f4 then RPY; rods: fused gather + drag)
   auto mvop_raw = [&](const double* v) -> int {
     if (int rc = launch_gather_raw(ctx, v, mu, nullptr)) return rc;
-    if (spheres) return rpy_all(ctx, p, mu, done);
+    if (spheres) return D.rpy(mu, done);
     return 0;
   };
   auto reduce = [&](int mode) -> int {
-    if (dist) {
-      if (int rc = allreduce_chunks(ctx)) return rc;
-    }
-    return launch_finalize(ctx, mode, red);
+    if (int rc = D.allreduce()) return rc;
+    return launch_finalize(ctx, mode, D.reduce_chunks());
   };
 
   // Steps 1-5: gamma_0, g_0 = M gamma_0 + q, phi_0
@@ -738,13 +777,11 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     // projection onto gamma >= 0 via the proj kernel with alpha = 0 (Step 1)
     if (int rc = launch_proj_own(ctx, gam0, gam0, gam0, 0, nc)) return rc;
     if (int rc = mvop_raw(gam0)) return rc;
-    if (int rc = launch_dt(ctx, 2, gam0, nullptr, nullptr, ctx->g[0].p, c0, c1)) return rc;
+    if (int rc = D.dt(2, gam0, nullptr, nullptr, ctx->g[0].p)) return rc;
   } else {
     SC_CUDA(cudaMemsetAsync(gam0, 0, nc * sizeof(double), ctx->stream));
-    SC_CUDA(cudaMemsetAsync(ctx->u4.p, 0, sizeof(double4) * (spheres ? std::max(ctx->npad, p.rpr * ctx->world)
-                                                                       : 2 * ctx->npad),
-                            ctx->stream));
-    if (int rc = launch_dt(ctx, 3, gam0, nullptr, nullptr, ctx->g[0].p, c0, c1)) return rc;
+    SC_CUDA(cudaMemsetAsync(ctx->u4.p, 0, sizeof(double4) * ctx->u4.n, ctx->stream));
+    if (int rc = D.dt(3, gam0, nullptr, nullptr, ctx->g[0].p)) return rc;
   }
   if (int rc = reduce(2)) return rc;
   stt.mvops = 1;
@@ -754,15 +791,13 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
   if (ctx->hsc->nonfinite) return fail(ctx, SC_ENONFINITE, "non-finite initial gradient");
   if (!ctx->hsc->done) {
     // Step 6: alpha_0 = g0.g0 / g0.M g0 (second MVOP, on the full g_0)
-    if (dist) {
-      if (int rc = bcast_slices(ctx, p, ctx->g[0].p)) return rc;
-    }
+    if (int rc = D.bcast(ctx->g[0].p)) return rc;
     if (int rc = mvop_raw(ctx->g[0].p)) return rc;
-    if (int rc = launch_dt(ctx, 1, nullptr, nullptr, ctx->g[0].p, nullptr, c0, c1)) return rc;
+    if (int rc = D.dt(1, nullptr, nullptr, ctx->g[0].p, nullptr)) return rc;
     if (int rc = reduce(1)) return rc;
     stt.mvops = 2;
     // Steps 7-16
-    const int batch = (n >= 32768 || dist) ? 1 : (n >= 4096 ? 4 : 16);
+    const int batch = (n >= 32768 || (dist && !D.emul)) ? 1 : (n >= 4096 ? 4 : 16);
     int enq = 0;
     while (enq < opts->max_iter) {
       const int nb = std::min(batch, opts->max_iter - enq);
@@ -772,17 +807,17 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
         double* gmo = ctx->gam[pp].p;
         double* gmn = ctx->gam[pp ^ 1].p;
         double* gn = ctx->g[pp ^ 1].p;
-        if (dist) {
-          if (int rc = launch_proj_own(ctx, gmo, go, gmn, p.l0, p.l1)) return rc;
-          if (int rc = bcast_slices(ctx, p, gmn)) return rc;
+        if (dist) {  // Steps 8-9 on own constraints, then every rank needs the full gamma_j
+          if (int rc = D.proj_own(gmo, go, gmn)) return rc;
+          if (int rc = D.bcast(gmn)) return rc;
           if (int rc = mvop_raw(gmn)) return rc;
-        } else {
+        } else {  // Steps 8-9 fused into the D-gather
           if (int rc = launch_gather_proj(ctx, gmo, go, gmn, mu)) return rc;
           if (spheres) {
-            if (int rc = rpy_all(ctx, p, mu, done)) return rc;
+            if (int rc = D.rpy(mu, done)) return rc;
           }
         }
-        if (int rc = launch_dt(ctx, 0, gmn, gmo, go, gn, c0, c1)) return rc;
+        if (int rc = D.dt(0, gmn, gmo, go, gn)) return rc;  // Steps 10-15
         if (int rc = reduce(0)) return rc;
       }
       enq += nb;
@@ -802,9 +837,7 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
   if (!s.conv && !opts->fixed_iters) rc_final = SC_NOT_CONVERGED;
   double* gfin = ctx->gam[parity].p;
   double* gradfin = ctx->g[parity].p;
-  if (dist) {
-    if (int rc = bcast_slices(ctx, p, gradfin)) return rc;
-  }
+  if (int rc = D.bcast(gradfin)) return rc;
   if (int rc = check_flag(ctx, SC_EDEGENERATE, "coincident centres in the RPY sum")) return rc;
   // outputs
   SC_CUDA(cudaMemcpyAsync(dgam, gfin, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
@@ -886,5 +919,12 @@ int sc_reset_timing(sc_ctx* ctx) {
   return SC_OK;
 }
 int64_t sc_launch_count(const sc_ctx* ctx) { return ctx ? ctx->launch_count : -1; }
+
+int sc_set_emulated_world(sc_ctx* ctx, int world) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (world < 1 || ctx->world > 1) return fail(ctx, SC_EINVAL, "emulated world needs a 1-GPU context and world >= 1");
+  ctx->emul_world = world;
+  return SC_OK;
+}
 
 }  // extern "C"

@@ -67,6 +67,7 @@ struct sc_ctx {
 
   // multi-GPU
   int rank = 0, world = 1;
+  int emul_world = 1;           // testing: run the multi-GPU decomposition of this many ranks on one GPU
   ncclComm_t comm = nullptr;
 
   // bodies

@@ -1,0 +1,142 @@
+"""CPU test (world size 2, gloo) of the multi-GPU decomposition.
+
+Each process plays one rank of the NCCL design with torch.distributed/gloo standing in
+for NCCL and the oracle standing in for the kernels (test infrastructure):
+  * rank r owns the RPY target rows plan_partition(n, P, r) gives it and the
+    constraints whose first body it owns (the paper's smaller-index rule);
+  * per iteration: projection of own constraints -> broadcast of every rank's slice;
+    F = D gamma locally; RPY of own rows -> all-gather of the rows; D^T + chunk partials
+    of own 256-body chunks -> all-reduce of the zero-padded partial vector; fixed-order
+    final sums -> identical alpha / phi / stop decision on every rank.
+The distributed BBPGD must reach the single-process oracle's gamma.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_1909_06623_b200 import plan_partition
+from paper_1909_06623_b200.synthetic import make_problem
+
+WORLD = 2
+CHUNK = 256
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _first_ptr(ct, n):
+    fp = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(fp, ct.i.astype(np.int64) + 1, 1)
+    return np.cumsum(fp)
+
+
+def _rank_main(rank, world, port, name, n, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p = make_problem(name, n=n)
+    n = p.n
+    ct = oracle.contacts_spheres(p.pos, p.radius, p.gap_abs, p.gap_rel)
+    fp = _first_ptr(ct, n)
+    parts = [plan_partition(n, world, r) for r in range(world)]
+    me = parts[rank]
+    npad, nch = me["npad"], me["npad"] // CHUNK
+    clip = lambda b: min(b, n)
+    lo, hi = clip(me["row_lo"]), clip(me["row_hi"])
+    l0, l1 = fp[lo], fp[hi]
+    slices = [(fp[clip(q["row_lo"])], fp[clip(q["row_hi"])]) for q in parts]
+
+    def bcast_slices(v):
+        for r, (a, b) in enumerate(slices):
+            t = torch.from_numpy(v[a:b].copy())
+            dist.broadcast(t, src=r)
+            v[a:b] = t.numpy()
+
+    def rpy_rows_allgather(FT):
+        own = oracle.rpy_apply_rows(p.pos, p.radius, p.mu, FT, lo, hi) if hi > lo else np.zeros((0, 6))
+        rpr = me["rows_per_rank"]
+        buf = np.zeros((rpr, 6))
+        buf[: hi - lo] = own
+        out = [torch.zeros(rpr, 6, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(out, torch.from_numpy(buf))
+        return torch.cat(out).numpy()[:n]
+
+    def chunk_sums(vals):  # vals: (nc, k) own rows valid -> fixed-order global sums
+        part = np.zeros((nch, vals.shape[1]))
+        for c in range(me["chunk_lo"], me["chunk_hi"]):
+            a, b = fp[clip(c * CHUNK)], fp[clip(c * CHUNK + CHUNK)]
+            part[c] = vals[a:b].sum(0)
+        t = torch.from_numpy(part)
+        dist.all_reduce(t)
+        return t.numpy().sum(0)
+
+    # U_ext and q (own constraints)
+    U = rpy_rows_allgather(p.force)
+    q = np.zeros(ct.nc)
+    q[l0:l1] = (ct.gap / p.dt + oracle.apply_DT(n, ct, U))[l0:l1]
+    bcast_slices(q)  # (for the final comparison only)
+
+    def grad_own(gam_full):  # own slice of M gamma (no q)
+        F = oracle.apply_D(n, ct, gam_full)
+        Ufull = rpy_rows_allgather(F)
+        return oracle.apply_DT(n, ct, Ufull)
+
+    gam = np.zeros(ct.nc)
+    g = q.copy()  # gamma_0 = 0: g_0 = q (Step 2, one counted MVOP)
+    phi = np.sqrt(chunk_sums(np.minimum(gam, g)[:, None] ** 2)[0])
+    iters = 0
+    if not phi < p.tol:
+        bcast_slices(g)
+        w = grad_own(g)
+        s2 = chunk_sums(np.stack([g * g, g * w], 1))
+        alpha = s2[0] / s2[1]  # Step 6
+        for j in range(1, p.max_iter + 1):
+            gnew = np.zeros(ct.nc)
+            gnew[l0:l1] = np.maximum(gam[l0:l1] - alpha * g[l0:l1], 0.0)  # Steps 8-9 (own)
+            bcast_slices(gnew)
+            gg = np.zeros(ct.nc)
+            gg[l0:l1] = grad_own(gnew)[l0:l1] + q[l0:l1]  # Step 10 (own)
+            s = gnew - gam
+            y = gg - g
+            sums = chunk_sums(np.stack([s * s, s * y, y * y, np.minimum(gnew, gg) ** 2], 1))
+            gam, g = gnew, gg
+            iters = j
+            phi = np.sqrt(sums[3])
+            if phi < p.tol:
+                break
+            if sums[1] > 0:
+                alpha = sums[0] / sums[1]  # BB1, Step 15
+    bcast_slices(g)
+    np.save(os.path.join(outdir, f"gamma{rank}.npy"), gam)
+    np.save(os.path.join(outdir, f"meta{rank}.npy"), np.array([iters, phi, l0, l1]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,n", [("C1", 512), ("C2", 700)])
+def test_gloo_world2_bbpgd_matches_oracle(tmp_path, name, n):
+    port = _free_port()
+    mp.spawn(_rank_main, args=(WORLD, port, name, n, str(tmp_path)), nprocs=WORLD, join=True)
+    g0 = np.load(tmp_path / "gamma0.npy")
+    g1 = np.load(tmp_path / "gamma1.npy")
+    m0, m1 = np.load(tmp_path / "meta0.npy"), np.load(tmp_path / "meta1.npy")
+    # every rank ends with the same full gamma and took the same decisions
+    np.testing.assert_array_equal(g0, g1)
+    assert m0[0] == m1[0] and m0[1] == m1[1] and m0[1] < 1e-8
+    # ownership: the two ranks' constraint slices tile [0, n_c) with no overlap
+    assert m0[2] == 0 and m0[3] == m1[2]
+    ref = oracle.solve_problem(make_problem(name, n=n))
+    assert m1[3] == ref["system"].ct.nc
+    rel = np.linalg.norm(g0 - ref["gamma"]) / np.linalg.norm(ref["gamma"])
+    assert rel < 1e-8, rel

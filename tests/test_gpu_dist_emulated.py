@@ -1,0 +1,62 @@
+"""The multi-GPU decomposition run on one GPU.
+
+An emulated world of P ranks executes every rank's share of every step (own
+constraints' projection, own RPY target rows, own reduction chunks) with the
+collectives replaced by their shared-buffer equivalents.  The design claims the
+results are BITWISE identical to P = 1 (nsplit, the chunking and every reduction
+order depend on N only); these tests hold it to that.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_1909_06623_b200 import Context
+from paper_1909_06623_b200.synthetic import make_problem
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def _cuda(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+
+
+def _solve(ctx, p, world, max_iter, fixed):
+    ctx.set_emulated_world(world)
+    ctx.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+    ctx.assemble_D()
+    U = ctx.mobility_apply(_cuda(p.force), mu=p.mu)
+    ctx.lcp_q(p.dt, U)
+    r = ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=max_iter, fixed_iters=fixed)
+    r["U_ext"] = U
+    ctx.set_emulated_world(1)
+    return r
+
+
+@pytest.mark.parametrize("name,n,max_iter,fixed", [("C1", None, 2000, False), ("C2", 3000, 5000, False),
+                                                    ("C5", 9000, 25, True), ("C3", 2500, 5000, False)])
+def test_emulated_ranks_bitwise_equal(ctx, name, n, max_iter, fixed):
+    p = make_problem(name, n=n)
+    ref = _solve(ctx, p, 1, max_iter, fixed)
+    for world in (2, 3, 8):
+        r = _solve(ctx, p, world, max_iter, fixed)
+        assert r["iters"] == ref["iters"] and r["mvops"] == ref["mvops"], world
+        assert r["residual"] == ref["residual"]
+        for k in ("gamma", "g", "Fc", "Uc", "U_ext"):
+            assert torch.equal(r[k], ref[k]), (world, k)
+
+
+def test_emulated_world_more_ranks_than_blocks(ctx):
+    """P larger than the number of 256-row blocks: idle ranks own nothing."""
+    p = make_problem("C1", n=300)  # 2 row blocks
+    ref = _solve(ctx, p, 1, 2000, False)
+    r = _solve(ctx, p, 5, 2000, False)
+    assert torch.equal(r["gamma"], ref["gamma"]) and torch.equal(r["Uc"], ref["Uc"])
