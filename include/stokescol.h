@@ -195,6 +195,14 @@ int sc_plan_partition(int64_t n, int world, int rank, int64_t* out7);
  * off.  Errors: SC_EINVAL on a multi-GPU context or world < 1. */
 int sc_set_emulated_world(sc_ctx* ctx, int world);
 
+/* Choice of the RPY apply kernel: 0 = automatic (the
+ * symmetric pair-tile kernel on a 1-GPU context with N >= 4096, else the
+ * target-row kernel), 1 = target-row kernel (the multi-GPU sharding unit;
+ * bitwise identical for any number of ranks), 2 = symmetric pair-tile kernel
+ * (each unordered pair evaluated once).  Both compute the same sum; they differ
+ * in rounding only.  Errors: SC_EINVAL for another mode. */
+int sc_set_rpy_kernel(sc_ctx* ctx, int mode);
+
 #ifdef __cplusplus
 }
 #endif

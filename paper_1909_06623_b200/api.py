@@ -219,6 +219,10 @@ class Context:
         """Testing hook: run the multi-GPU decomposition of `world` ranks on this one GPU."""
         self._rc(self.lib.sc_set_emulated_world(self._h, int(world)))
 
+    def set_rpy_kernel(self, mode: int):
+        """0 automatic, 1 target-row kernel (multi-GPU unit), 2 symmetric pair-tile kernel."""
+        self._rc(self.lib.sc_set_rpy_kernel(self._h, int(mode)))
+
     def launch_count(self) -> int:
         return int(self.lib.sc_launch_count(self._h))
 

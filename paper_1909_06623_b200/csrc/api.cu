@@ -230,7 +230,10 @@ struct Dist {
   }
   // u4 = RPY(f4): own target rows, then all-gather of the rows
   int rpy(double mu, const int32_t* done) {
-    if (!on) return rpy_apply_rows(ctx, ctx->f4.p, 0, ctx->npad, mu, ctx->u4.p, done);
+    if (!on) {
+      if (rpy_use_sym(ctx)) return rpy_apply_sym(ctx, ctx->f4.p, mu, ctx->u4.p, done);
+      return rpy_apply_rows(ctx, ctx->f4.p, 0, ctx->npad, mu, ctx->u4.p, done);
+    }
     for (int r : mine) {
       const Part& p = parts[r];
       if (int rc = rpy_apply_rows(ctx, ctx->f4.p, p.row_lo, p.row_hi - p.row_lo, mu, ctx->u4.p, done)) return rc;
@@ -322,7 +325,7 @@ static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 static int prepare_bodies(sc_ctx* ctx, int kind, int64_t n) {
   ctx->kind = kind;
   ctx->n = n;
-  ctx->npad = round_up(std::max<int64_t>(n, 1), kRpyRows);
+  ctx->npad = round_up(std::max<int64_t>(n, 1), kNpadQuantum);
   ctx->nsplit = choose_nsplit(ctx->npad, ctx->world);
   ctx->nc = 0;
   ctx->assembled = false;
@@ -451,7 +454,7 @@ void sc_destroy(sc_ctx* ctx) {
   release(ctx->row_ptr); release(ctx->inc); release(ctx->first_ptr); release(ctx->near_ptr); release(ctx->near_idx);
   release(ctx->q); release(ctx->gam[0]); release(ctx->gam[1]); release(ctx->g[0]); release(ctx->g[1]);
   release(ctx->w); release(ctx->gam_user); release(ctx->chunk_part); release(ctx->chunk_red);
-  release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);
+  release(ctx->sym_pairs); release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);
   release(ctx->bbox_part); release(ctx->cell_of); release(ctx->cell_cnt); release(ctx->cell_start);
   release(ctx->sorted_idx); release(ctx->pair_cnt); release(ctx->pair_off); release(ctx->scan_tmp);
   release(ctx->sorted4); release(ctx->sorted_dir4); release(ctx->stage);
@@ -471,7 +474,7 @@ void* sc_stream(const sc_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream
 
 int sc_plan_partition(int64_t n, int world, int rank, int64_t* out7) {
   if (n < 0 || world < 1 || rank < 0 || rank >= world || out7 == nullptr) return SC_EINVAL;
-  const int64_t npad = round_up(std::max<int64_t>(n, 1), kRpyRows);
+  const int64_t npad = round_up(std::max<int64_t>(n, 1), kNpadQuantum);
   int64_t rpr, lo, hi;
   plan_rows(npad, world, rank, &rpr, &lo, &hi);
   out7[0] = npad;
@@ -919,6 +922,13 @@ int sc_reset_timing(sc_ctx* ctx) {
   return SC_OK;
 }
 int64_t sc_launch_count(const sc_ctx* ctx) { return ctx ? ctx->launch_count : -1; }
+
+int sc_set_rpy_kernel(sc_ctx* ctx, int mode) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (mode < 0 || mode > 2) return fail(ctx, SC_EINVAL, "rpy kernel mode must be 0, 1 or 2");
+  ctx->rpy_mode = mode;
+  return SC_OK;
+}
 
 int sc_set_emulated_world(sc_ctx* ctx, int world) {
   if (ctx == nullptr) return SC_EINVAL;

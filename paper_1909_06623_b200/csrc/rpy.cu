@@ -23,6 +23,7 @@
 //    GPUs).  Inside a split: plain FP64 sums over a 128-source tile, then a
 //    compensated (TwoSum) add of each tile sum.
 #include <cstdio>
+#include <vector>
 
 #include "rpy_common.cuh"
 #include "sc_internal.h"
@@ -295,6 +296,235 @@ __global__ void rpy_combine_kernel(const double* __restrict__ part, int nsplit, 
 
 constexpr size_t kRpySmem = 4 * kRpyTile * sizeof(double4) + 2 * sizeof(uint64_t);
 
+// ---------------------------------------------------------------------------------------
+// Symmetric variant (1 GPU): the RPY pair block is symmetric, T_ij = T_ji (it depends on
+// d d^T and |d|), so each unordered pair is evaluated ONCE and feeds both bodies:
+//   U_i += c1 f_j + c2 (d.f_j) d,   U_j += c1 f_i + c2 (d.f_i) d.
+// 36 FP64 instructions per unordered pair instead of 2 x 26.
+//
+// Work unit: a pair (SI, SJ), SI <= SJ, of super-blocks of kSymSB = 512 bodies.  A CTA of
+// 4 warps holds the SI targets in registers (lane l of warp w: rows (w + 4m)*32 + l,
+// m = 0..3) and the SJ sources (positions, forces) in shared memory (one TMA bulk copy).
+// Phase p (16 of them): warp w pairs its 4 row sub-blocks with source sub-block
+// cj = (w + p) mod 16 -- distinct across warps -- through 32 rotation steps: at step k lane l
+// meets source (l + k) mod 32 and carries that source's accumulator U_j, passed to lane
+// l - 1 by one warp shuffle per step; after 32 steps lane l holds source l's sum and adds it
+// to the CTA's shared accumulator (no two warps touch one sub-block in a phase).
+// SI == SJ: forward contributions only (every ordered pair of the super-block once).
+//
+// Output: part[slot][row][3] with slot = the partner super-block: rows of SI get slot SJ
+// (forward), rows of SJ get slot SI (reverse), so every (slot, row) is written exactly
+// once per apply and rpy_combine sums the NS slots of a row in a fixed order.
+constexpr int kSymThreads = 128;
+constexpr int kSymTpt = 4;
+constexpr int kSymSB = kSymThreads * kSymTpt;  // 512 bodies per super-block
+constexpr int kSymNsub = kSymSB / 32;          // 16 sub-blocks of 32
+constexpr size_t kSymSmem = 2 * kSymSB * sizeof(double4) + 3 * kSymSB * sizeof(double) + 16;
+
+template <bool POLY>
+__global__ void __launch_bounds__(kSymThreads, 3)
+    rpy_sym_kernel(const double4* __restrict__ pos4, const double4* __restrict__ f4, const int2* __restrict__ pairs,
+                   int64_t npad, Consts k, double* __restrict__ part, const int32_t* __restrict__ done) {
+  constexpr int TPT = kSymTpt;
+  if (done != nullptr && *done) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double4* sp = reinterpret_cast<double4*>(smem_raw);  // SJ positions
+  double4* sf = sp + kSymSB;                           // SJ forces
+  double* sacc = reinterpret_cast<double*>(sf + kSymSB);  // SJ reverse accumulators [kSymSB][3]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sacc + 3 * kSymSB);
+
+  const int2 pr = pairs[blockIdx.x];
+  const int64_t SI = pr.x, SJ = pr.y;
+  const bool rev = SI != SJ;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  constexpr uint32_t kBytes = kSymSB * sizeof(double4);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_expect_tx(bar, 2 * kBytes);
+    tma_load_1d(sp, pos4 + SJ * kSymSB, kBytes, bar);
+    tma_load_1d(sf, f4 + SJ * kSymSB, kBytes, bar);
+  }
+  double4 p[TPT];
+  double fx[TPT], fy[TPT], fz[TPT], ax[TPT], ay[TPT], az[TPT];
+#pragma unroll
+  for (int m = 0; m < TPT; ++m) {
+    const int64_t row = SI * kSymSB + (w + 4 * m) * 32 + lane;
+    p[m] = pos4[row];
+    const double4 f = f4[row];
+    fx[m] = f.x;
+    fy[m] = f.y;
+    fz[m] = f.z;
+    ax[m] = ay[m] = az[m] = 0.0;
+  }
+  for (int q = tid; q < 3 * kSymSB; q += kSymThreads) sacc[q] = 0.0;
+  mbar_wait(bar, 0);
+  __syncthreads();
+
+#pragma unroll 1
+  for (int ph = 0; ph < kSymNsub; ++ph) {
+    const int cj = (w + ph) & (kSymNsub - 1);
+    const double4* tp = sp + cj * 32;
+    const double4* tf = sf + cj * 32;
+    double rx = 0.0, ry = 0.0, rz = 0.0;  // accumulator of the source this lane meets
+#pragma unroll 1
+    for (int st = 0; st < 32; ++st) {
+      const int s = (lane + st) & 31;
+      const double4 pj = tp[s];
+      const double4 fj = tf[s];
+      double dx[TPT], dy[TPT], dz[TPT], r2[TPT], y[TPT], h[TPT], e[TPT], c1[TPT], c2[TPT];
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) r2[m] = rpy_r2(p[m], pj, dx[m], dy[m], dz[m]);
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y[m]) : "d"(r2[m]));
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) h[m] = r2[m] * y[m];
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) e[m] = fma(-h[m], y[m], 1.0);
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) {
+        h[m] = fma(0.375, e[m], 0.5);
+        e[m] = y[m] * e[m];
+      }
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) y[m] = fma(e[m], h[m], y[m]);  // rinv
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) h[m] = y[m] * y[m];  // rinv^2
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) e[m] = y[m] * h[m];  // rinv^3
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) {
+        bool nr;
+        if (POLY) {
+          const double abar = p[m].w + pj.w;
+          const double s2 = (abar * abar) * h[m];
+          c1[m] = y[m] * fma(s2, 2.0 / 3.0, 1.0);
+          c2[m] = e[m] * fma(s2, -2.0, 1.0);
+          nr = rpy_is_near(r2[m], abar, true, 0);
+        } else {
+          c1[m] = fma(k.k23a2, e[m], y[m]);
+          c2[m] = e[m] * fma(k.m2a2, h[m], 1.0);
+          nr = rpy_is_near(r2[m], 0.0, false, k.near_bits);
+        }
+        c1[m] = nr ? 0.0 : c1[m];
+        c2[m] = nr ? 0.0 : c2[m];
+      }
+      // forward: U_i += c1 f_j + c2 (d.f_j) d
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) {
+        const double t = c2[m] * fma(dz[m], fj.z, fma(dy[m], fj.y, dx[m] * fj.x));
+        ax[m] = fma(t, dx[m], fma(c1[m], fj.x, ax[m]));
+        ay[m] = fma(t, dy[m], fma(c1[m], fj.y, ay[m]));
+        az[m] = fma(t, dz[m], fma(c1[m], fj.z, az[m]));
+      }
+      if (rev) {  // reverse: U_j += c1 f_i + c2 (d.f_i) d  (same T: even in d)
+#pragma unroll
+        for (int m = 0; m < TPT; ++m) {
+          const double t = c2[m] * fma(dz[m], fz[m], fma(dy[m], fy[m], dx[m] * fx[m]));
+          rx = fma(t, dx[m], fma(c1[m], fx[m], rx));
+          ry = fma(t, dy[m], fma(c1[m], fy[m], ry));
+          rz = fma(t, dz[m], fma(c1[m], fz[m], rz));
+        }
+        const int src = (lane + 1) & 31;  // next step this lane meets the source lane+1 met now
+        rx = __shfl_sync(0xffffffffu, rx, src);
+        ry = __shfl_sync(0xffffffffu, ry, src);
+        rz = __shfl_sync(0xffffffffu, rz, src);
+      }
+    }
+    if (rev) {  // after 32 steps lane l holds source l's sum
+      double* a = sacc + (cj * 32 + lane) * 3;
+      a[0] += rx;
+      a[1] += ry;
+      a[2] += rz;
+      __syncthreads();
+    }
+  }
+  // forward sums: rows of SI, slot SJ
+#pragma unroll
+  for (int m = 0; m < TPT; ++m) {
+    const int64_t row = SI * kSymSB + (w + 4 * m) * 32 + lane;
+    double* o = part + (SJ * npad + row) * 3;
+    o[0] = ax[m];
+    o[1] = ay[m];
+    o[2] = az[m];
+  }
+  if (rev) {  // reverse sums: rows of SJ, slot SI
+    __syncthreads();
+    double* o = part + (SI * npad + SJ * kSymSB) * 3;
+    for (int q = tid; q < 3 * kSymSB; q += kSymThreads) o[q] = sacc[q];
+  }
+}
+
+}  // namespace
+
+bool rpy_use_sym(const sc_ctx* ctx) {
+  if (ctx->rpy_mode == 1) return false;
+  if (ctx->rpy_mode == 2) return true;
+  // auto: one GPU (real), enough super-blocks to fill the machine
+  return ctx->world == 1 && ctx->emul_world <= 1 && ctx->npad >= 8 * kSymSB;
+}
+
+int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done) {
+  const int64_t nsb = (ctx->npad + kSymSB - 1) / kSymSB;
+  const int64_t npad_sym = nsb * kSymSB;
+  if (npad_sym != ctx->npad) return fail(ctx, SC_EINVAL, "symmetric RPY needs npad % 512 == 0");
+  // pair table (SI <= SJ), rebuilt when the number of super-blocks changes
+  if (ctx->sym_nsb != nsb) {
+    std::vector<int2> tab;
+    tab.reserve(nsb * (nsb + 1) / 2);
+    for (int64_t i = 0; i < nsb; ++i)
+      for (int64_t j = i; j < nsb; ++j) tab.push_back(make_int2(static_cast<int>(i), static_cast<int>(j)));
+    if (int rc = ensure(ctx, ctx->sym_pairs, tab.size())) return rc;
+    SC_CUDA(cudaMemcpyAsync(ctx->sym_pairs.p, tab.data(), tab.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    SC_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->sym_nsb = nsb;
+  }
+  const int64_t npairs = nsb * (nsb + 1) / 2;
+  if (int rc = ensure(ctx, ctx->rpy_part, static_cast<size_t>(nsb) * ctx->npad * 3)) return rc;
+  const double a = ctx->a_const;
+  Consts k;
+  k.k23a2 = 2.0 / 3.0 * a * a;
+  k.m2a2 = -2.0 * a * a;
+  k.kn1 = 4.0 / (3.0 * a);
+  k.kn2 = -9.0 / (32.0 * a);
+  k.kn3 = 1.0 / (8.0 * a * a);
+  const double n2 = 4.0 * a * a;
+  k.near_bits = *reinterpret_cast<const long long*>(&n2);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(rpy_sym_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
+    cudaFuncSetAttribute(rpy_sym_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
+    attr_set = true;
+  }
+  timer_begin(ctx, SC_K_RPY);
+  if (ctx->poly)
+    rpy_sym_kernel<true><<<static_cast<unsigned>(npairs), kSymThreads, kSymSmem, ctx->stream>>>(
+        ctx->pos4.p, f4, ctx->sym_pairs.p, ctx->npad, k, ctx->rpy_part.p, done);
+  else
+    rpy_sym_kernel<false><<<static_cast<unsigned>(npairs), kSymThreads, kSymSmem, ctx->stream>>>(
+        ctx->pos4.p, f4, ctx->sym_pairs.p, ctx->npad, k, ctx->rpy_part.p, done);
+  timer_end(ctx, SC_K_RPY);
+  if (int rc = check_launch(ctx, "rpy_sym")) return rc;
+  const double scale = 1.0 / (8.0 * 3.14159265358979323846 * mu);
+  const int64_t nrows = ctx->npad;
+  timer_begin(ctx, SC_K_COMBINE);
+  if (ctx->poly)
+    rpy_combine_kernel<true><<<static_cast<unsigned>((nrows + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->rpy_part.p, static_cast<int>(nsb), 0, nrows, ctx->n, scale, ctx->pos4.p, f4, ctx->near_ptr.p,
+        ctx->near_idx.p, u4, done, ctx->derr);
+  else
+    rpy_combine_kernel<false><<<static_cast<unsigned>((nrows + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->rpy_part.p, static_cast<int>(nsb), 0, nrows, ctx->n, scale, ctx->pos4.p, f4, ctx->near_ptr.p,
+        ctx->near_idx.p, u4, done, ctx->derr);
+  timer_end(ctx, SC_K_COMBINE);
+  return check_launch(ctx, "rpy_combine_sym");
+}
+
+namespace {
 }  // namespace
 
 int choose_nsplit(int64_t npad, int world) {

@@ -18,6 +18,7 @@ constexpr int kRpyTpt = 4;              // targets per thread
 constexpr int kRpySu = 2;               // sources interleaved per step (ILP: TPT*SU pair chains)
 constexpr int kRpyRows = kRpyThreads * kRpyTpt;  // 256 target rows per CTA
 constexpr int kRpyTile = 128;           // sources per shared-memory tile
+constexpr int kNpadQuantum = 512;       // npad = N rounded up to this (RPY row blocks and super-blocks)
 constexpr int kChunkBodies = 256;       // B_c: bodies per reduction chunk
 constexpr int kPartials = 4;            // doubles per chunk partial
 
@@ -106,6 +107,9 @@ struct sc_ctx {
   sc::DBuf<double4> u4;         // velocities (Ux,Uy,Uz,0) [npad] (spheres) or [2*npad] (rods: U, W)
   sc::DBuf<double> rpy_part;    // nsplit * rows * 3
   int nsplit = 1;
+  int rpy_mode = 0;             // 0 auto, 1 target-row kernel, 2 symmetric pair-tile kernel
+  int64_t sym_nsb = -1;         // super-blocks the pair table was built for
+  sc::DBuf<int2> sym_pairs;     // (SI, SJ), SI <= SJ
   sc::DevScalars* dsc = nullptr;   // device scalars
   sc::DevScalars* hsc = nullptr;   // pinned mirror
   int32_t* derr = nullptr;         // device error flag
@@ -173,6 +177,8 @@ int assemble(sc_ctx* ctx);
 int rpy_apply_rows(sc_ctx* ctx, const double4* f4, int64_t row0, int64_t nrows, double mu,
                    double4* u4, const int32_t* done);
 int choose_nsplit(int64_t npad, int world);
+bool rpy_use_sym(const sc_ctx* ctx);
+int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done);
 
 // ---- LCP kernels (lcp.cu) -------------------------------------------------
 // gather F = D v (mode raw) or F = D max(0, gam_old - alpha g_old) with the owner

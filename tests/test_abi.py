@@ -51,7 +51,7 @@ def test_no_device_context_without_gpu():
 def test_partition_covers_rows_once(n, world):
     parts = [plan_partition(n, world, r) for r in range(world)]
     npad = parts[0]["npad"]
-    assert npad % 256 == 0 and npad >= n and npad - n < 256
+    assert npad % 512 == 0 and npad >= n and npad - n < 512
     covered = []
     for p in parts:
         assert p["row_lo"] % 256 == 0 and p["row_hi"] % 256 == 0

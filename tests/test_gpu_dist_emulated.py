@@ -30,6 +30,7 @@ def _cuda(a):
 
 
 def _solve(ctx, p, world, max_iter, fixed):
+    ctx.set_rpy_kernel(1)  # the target-row kernel is the multi-GPU sharding unit
     ctx.set_emulated_world(world)
     ctx.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
     ctx.assemble_D()
@@ -38,6 +39,7 @@ def _solve(ctx, p, world, max_iter, fixed):
     r = ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=max_iter, fixed_iters=fixed)
     r["U_ext"] = U
     ctx.set_emulated_world(1)
+    ctx.set_rpy_kernel(0)
     return r
 
 

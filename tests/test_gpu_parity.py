@@ -119,25 +119,38 @@ def test_apply_D_DT_and_q(ctx, name, n):
 
 
 # ---------------------------------------------------------------- (a4)
-@pytest.mark.parametrize("name,n", [("C1", None), ("C2", None), ("C1", 1000), ("C2", 300), ("C1", 1)])
-def test_mobility_full_parity(ctx, name, n):
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("name,n", [("C1", None), ("C2", None), ("C1", 1000), ("C2", 300), ("C1", 1),
+                                    ("C3", 5000)])
+def test_mobility_full_parity(ctx, name, n, kernel):
+    """Both RPY kernels (target-row, symmetric pair-tile) against the oracle."""
     p = make_problem(name, n=n)
     _gpu_contacts(ctx, p)
     rng = np.random.default_rng(4)
     FT = rng.normal(size=(p.n, 6))
-    U = _np(ctx.mobility_apply(_cuda(FT), mu=p.mu))
+    ctx.set_rpy_kernel(kernel)
+    try:
+        U = _np(ctx.mobility_apply(_cuda(FT), mu=p.mu))
+    finally:
+        ctx.set_rpy_kernel(0)
     Uo = oracle.rpy_apply(p.pos, p.radius, p.mu, FT)
     assert _relL2(U[:, :3], Uo[:, :3]) <= 1e-12
     assert _relL2(U[:, 3:], Uo[:, 3:]) <= 1e-14
 
 
+@pytest.mark.parametrize("kernel", [0, 1])
 @pytest.mark.parametrize("name", ["C3", "C5"])
-def test_mobility_full_size_sampled_rows(ctx, name):
-    """Full BASELINE size, the launch configuration the bench times; oracle rows one by one."""
+def test_mobility_full_size_sampled_rows(ctx, name, kernel):
+    """Full BASELINE size, the launch configuration the bench times (kernel 0 = automatic:
+    the symmetric kernel on one GPU; 1 = the multi-GPU row kernel); oracle rows one by one."""
     p = make_problem(name)
     _gpu_contacts(ctx, p)
     FT = p.force.copy()
-    U = _np(ctx.mobility_apply(_cuda(FT), mu=p.mu))
+    ctx.set_rpy_kernel(kernel)
+    try:
+        U = _np(ctx.mobility_apply(_cuda(FT), mu=p.mu))
+    finally:
+        ctx.set_rpy_kernel(0)
     rows = sorted(set([0, 1, 255, 256, p.n // 2, p.n - 257, p.n - 1] +
                       np.random.default_rng(0).integers(0, p.n, 25).tolist()))
     for r in rows:
