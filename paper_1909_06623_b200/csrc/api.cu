@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -228,12 +229,18 @@ struct Dist {
     NCCL_CHECK(ncclGroupEnd());
     return 0;
   }
-  // u4 = RPY(f4): own target rows, then all-gather of the rows
+  // u4 = RPY(f4).  Symmetric kernel: every rank evaluates its super-block pairs, combines
+  // the slots it wrote (owned rows also get the self and near terms) and the partial
+  // velocities are all-reduced.  Target-row kernel: own rows, then all-gather of the rows.
   int rpy(double mu, const int32_t* done) {
-    if (!on) {
-      if (rpy_use_sym(ctx)) return rpy_apply_sym(ctx, ctx->f4.p, mu, ctx->u4.p, done);
-      return rpy_apply_rows(ctx, ctx->f4.p, 0, ctx->npad, mu, ctx->u4.p, done);
+    if (rpy_use_sym(ctx)) {
+      if (!on) return rpy_apply_sym(ctx, ctx->f4.p, mu, ctx->u4.p, done, 1, mine, 0);
+      if (emul) return rpy_apply_sym(ctx, ctx->f4.p, mu, ctx->u4.p, done, W, mine, 1);
+      if (int rc = rpy_apply_sym(ctx, ctx->f4.p, mu, ctx->u4.p, done, W, mine, 2)) return rc;
+      NCCL_CHECK(ncclAllReduce(ctx->u4.p, ctx->u4.p, ctx->npad * 4, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+      return 0;
     }
+    if (!on) return rpy_apply_rows(ctx, ctx->f4.p, 0, ctx->npad, mu, ctx->u4.p, done);
     for (int r : mine) {
       const Part& p = parts[r];
       if (int rc = rpy_apply_rows(ctx, ctx->f4.p, p.row_lo, p.row_hi - p.row_lo, mu, ctx->u4.p, done)) return rc;
@@ -244,10 +251,12 @@ struct Dist {
     NCCL_CHECK(ncclAllGather(base + ctx->rank * cnt, base, cnt, ncclDouble, ctx->comm, ctx->stream));
     return 0;
   }
-  int dt(int mode, const double* gam_new, const double* gam_old, const double* g_old, double* g_out) {
-    if (!on) return launch_dt(ctx, mode, gam_new, gam_old, g_old, g_out, 0, ctx->nchunks);
+  // D^T over this process's chunks.  One GPU: fused with K-FINALIZE (returns fused = true).
+  int dt(int mode, const double* gam_new, const double* gam_old, const double* g_old, double* g_out, bool* fused) {
+    *fused = !on;
+    if (!on) return launch_dt(ctx, mode, gam_new, gam_old, g_old, g_out, 0, ctx->nchunks, true);
     for (int r : mine)
-      if (int rc = launch_dt(ctx, mode, gam_new, gam_old, g_old, g_out, parts[r].c0, parts[r].c1)) return rc;
+      if (int rc = launch_dt(ctx, mode, gam_new, gam_old, g_old, g_out, parts[r].c0, parts[r].c1, false)) return rc;
     return 0;
   }
   // chunk partials -> reduced vector; returns the buffer K-FINALIZE reads
@@ -402,12 +411,15 @@ static int create_common(sc_ctx** out, int device, void* stream) {
   if (cudaMalloc(&ctx->dsc, sizeof(DevScalars)) != cudaSuccess ||
       cudaMallocHost(&ctx->hsc, sizeof(DevScalars)) != cudaSuccess ||
       cudaMalloc(&ctx->derr, sizeof(int32_t)) != cudaSuccess ||
+      cudaMalloc(&ctx->dcount, sizeof(unsigned int)) != cudaSuccess ||
       cudaMallocHost(&ctx->herr, sizeof(int32_t)) != cudaSuccess) {
     sc_destroy(ctx);
     return SC_ENOMEM;
   }
   cudaMemset(ctx->derr, 0, sizeof(int32_t));
+  cudaMemset(ctx->dcount, 0, sizeof(unsigned int));
   cudaMemset(ctx->dsc, 0, sizeof(DevScalars));
+  if (const char* v = std::getenv("SC_SYM_VARIANT")) ctx->sym_variant = std::atoi(v);
   *ctx->herr = 0;
   *out = ctx;
   return SC_OK;
@@ -454,13 +466,14 @@ void sc_destroy(sc_ctx* ctx) {
   release(ctx->row_ptr); release(ctx->inc); release(ctx->first_ptr); release(ctx->near_ptr); release(ctx->near_idx);
   release(ctx->q); release(ctx->gam[0]); release(ctx->gam[1]); release(ctx->g[0]); release(ctx->g[1]);
   release(ctx->w); release(ctx->gam_user); release(ctx->chunk_part); release(ctx->chunk_red);
-  release(ctx->sym_pairs); release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);
+  release(ctx->sym_pairs); release(ctx->upart); release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);
   release(ctx->bbox_part); release(ctx->cell_of); release(ctx->cell_cnt); release(ctx->cell_start);
   release(ctx->sorted_idx); release(ctx->pair_cnt); release(ctx->pair_off); release(ctx->scan_tmp);
   release(ctx->sorted4); release(ctx->sorted_dir4); release(ctx->stage);
   if (ctx->dsc) cudaFree(ctx->dsc);
   if (ctx->hsc) cudaFreeHost(ctx->hsc);
   if (ctx->derr) cudaFree(ctx->derr);
+  if (ctx->dcount) cudaFree(ctx->dcount);
   if (ctx->herr) cudaFreeHost(ctx->herr);
   for (int f = 0; f < SC_K_COUNT; ++f)
     for (auto e : ctx->timer.ev[f]) cudaEventDestroy(e);
@@ -768,7 +781,9 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     if (spheres) return D.rpy(mu, done);
     return 0;
   };
+  bool fused = false;  // set by D.dt: the D^T kernel already ran K-FINALIZE
   auto reduce = [&](int mode) -> int {
+    if (fused) return 0;
     if (int rc = D.allreduce()) return rc;
     return launch_finalize(ctx, mode, D.reduce_chunks());
   };
@@ -780,11 +795,11 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     // projection onto gamma >= 0 via the proj kernel with alpha = 0 (Step 1)
     if (int rc = launch_proj_own(ctx, gam0, gam0, gam0, 0, nc)) return rc;
     if (int rc = mvop_raw(gam0)) return rc;
-    if (int rc = D.dt(2, gam0, nullptr, nullptr, ctx->g[0].p)) return rc;
+    if (int rc = D.dt(2, gam0, nullptr, nullptr, ctx->g[0].p, &fused)) return rc;
   } else {
     SC_CUDA(cudaMemsetAsync(gam0, 0, nc * sizeof(double), ctx->stream));
     SC_CUDA(cudaMemsetAsync(ctx->u4.p, 0, sizeof(double4) * ctx->u4.n, ctx->stream));
-    if (int rc = D.dt(3, gam0, nullptr, nullptr, ctx->g[0].p)) return rc;
+    if (int rc = D.dt(3, gam0, nullptr, nullptr, ctx->g[0].p, &fused)) return rc;
   }
   if (int rc = reduce(2)) return rc;
   stt.mvops = 1;
@@ -796,11 +811,15 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     // Step 6: alpha_0 = g0.g0 / g0.M g0 (second MVOP, on the full g_0)
     if (int rc = D.bcast(ctx->g[0].p)) return rc;
     if (int rc = mvop_raw(ctx->g[0].p)) return rc;
-    if (int rc = D.dt(1, nullptr, nullptr, ctx->g[0].p, nullptr)) return rc;
+    if (int rc = D.dt(1, nullptr, nullptr, ctx->g[0].p, nullptr, &fused)) return rc;
     if (int rc = reduce(1)) return rc;
     stt.mvops = 2;
     // Steps 7-16
-    const int batch = (n >= 32768 || (dist && !D.emul)) ? 1 : (n >= 4096 ? 4 : 16);
+    // iterations enqueued between two host reads of the scalars: enough to cover ~1 ms of
+    // device work (extra iterations after convergence are no-op launches)
+    const double t_iter = spheres ? 1.3e-12 * static_cast<double>(ctx->npad) * ctx->npad + 4e-5
+                                  : 2e-5 + 1.2e-10 * static_cast<double>(nc + n);
+    const int batch = (dist && !D.emul) ? 1 : std::max(1, std::min(32, static_cast<int>(1e-3 / t_iter)));
     int enq = 0;
     while (enq < opts->max_iter) {
       const int nb = std::min(batch, opts->max_iter - enq);
@@ -820,7 +839,7 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
             if (int rc = D.rpy(mu, done)) return rc;
           }
         }
-        if (int rc = D.dt(0, gmn, gmo, go, gn)) return rc;  // Steps 10-15
+        if (int rc = D.dt(0, gmn, gmo, go, gn, &fused)) return rc;  // Steps 10-15
         if (int rc = reduce(0)) return rc;
       }
       enq += nb;

@@ -51,18 +51,19 @@ __global__ void bbox_partial(const double4* __restrict__ p, int64_t n, int size_
   if (threadIdx.x < 7) out[blockIdx.x * 7 + threadIdx.x] = s[threadIdx.x][0];
 }
 
+// one warp per component: min of the 3 lower bounds, max of the 3 upper bounds and the size
 __global__ void bbox_final(double* __restrict__ part, int nb) {
-  if (threadIdx.x != 0) return;
-  double r[7];
-  for (int d = 0; d < 7; ++d) r[d] = part[d];
-  for (int b = 1; b < nb; ++b) {
-    for (int d = 0; d < 3; ++d) {
-      r[d] = fmin(r[d], part[b * 7 + d]);
-      r[3 + d] = fmax(r[3 + d], part[b * 7 + 3 + d]);
-    }
-    r[6] = fmax(r[6], part[b * 7 + 6]);
+  const int d = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (d >= 7) return;
+  const bool is_min = d < 3;
+  double r = is_min ? INFINITY : -INFINITY;
+  for (int b = lane; b < nb; b += 32) r = is_min ? fmin(r, part[b * 7 + d]) : fmax(r, part[b * 7 + d]);
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v = __shfl_xor_sync(0xffffffffu, r, o);
+    r = is_min ? fmin(r, v) : fmax(r, v);
   }
-  for (int d = 0; d < 7; ++d) part[d] = r[d];
+  __syncthreads();  // every warp has read its column before lane 0 overwrites row 0
+  if (lane == 0) part[d] = r;
 }
 
 struct Grid {
@@ -378,7 +379,7 @@ int build_common(sc_ctx* ctx, SphereTest st, RodTest rt) {
   timer_end(ctx, SC_K_CONTACTS);
   if (int rc = check_launch(ctx, "bbox_partial")) return rc;
   timer_begin(ctx, SC_K_CONTACTS);
-  bbox_final<<<1, 32, 0, ctx->stream>>>(ctx->bbox_part.p, kBboxBlocks);
+  bbox_final<<<1, 224, 0, ctx->stream>>>(ctx->bbox_part.p, kBboxBlocks);
   timer_end(ctx, SC_K_CONTACTS);
   if (int rc = check_launch(ctx, "bbox_final")) return rc;
   double bb[7];

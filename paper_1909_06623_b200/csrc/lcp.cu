@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(kT) gather_kernel(
   const double alpha = MODE == kProj ? dsc->alpha : 0.0;
   double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
   const int32_t e0 = row_ptr[b], e1 = row_ptr[b + 1];
+#pragma unroll 4
   for (int32_t e = e0; e < e1; ++e) {
     const int32_t v = inc[e];
     const int32_t l = v >> 1;
@@ -103,16 +104,80 @@ __device__ __forceinline__ void block_reduce4(double v[4], double* red /* [4][kT
   for (int k = 0; k < 4; ++k) v[k] = red[k * kT];
 }
 
+// Sums chunk partials in fixed order (thread t: chunks t, t+256, ...; then a fixed tree)
+// and advances the BBPGD scalars.  mode 0: after Step 10 of iteration j; mode 1: alpha_0
+// (Step 6); mode 2: phi_0 (Step 3).  Called by one whole CTA of kT threads.
+__device__ void finalize_block(const double* part, int64_t nchunks, int mode, DevScalars* s, double* red) {
+  double p[4] = {0, 0, 0, 0};
+  for (int64_t c = threadIdx.x; c < nchunks; c += kT) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p[k] += __ldcg(part + c * 4 + k);
+  }
+  block_reduce4(p, red);
+  if (threadIdx.x != 0) return;
+  for (int k = 0; k < 4; ++k) s->p[k] = p[k];
+  if (mode == 1) {
+    const double a = p[0] / p[1];  // alpha_0 = g0.g0 / g0.M g0
+    if (!(isfinite(a) && a > 0.0)) {
+      s->nonfinite = 1;
+      s->done = 1;
+    } else {
+      s->alpha = a;
+    }
+    return;
+  }
+  const double phi = sqrt(p[3]);
+  s->phi = phi;
+  if (!isfinite(phi)) {
+    s->nonfinite = 1;
+    s->done = 1;
+    return;
+  }
+  s->conv = phi < s->tol ? 1 : 0;
+  if (mode == 2) {
+    if (s->conv) s->done = 1;
+    return;
+  }
+  const int j = s->iter + 1;
+  s->iter = j;
+  if (s->fixed) {
+    if (j >= s->max_iter) {
+      s->done = 1;
+      return;
+    }
+  } else if (s->conv || j >= s->max_iter) {
+    s->done = 1;
+    return;
+  }
+  const bool bb2 = s->bb_mode == 1 || (s->bb_mode == 2 && (j % 2 == 0));
+  const double a_new = bb2 ? p[1] / p[2] : p[0] / p[1];
+  if (p[1] > 0.0 && isfinite(a_new) && a_new > 0.0) {
+    s->alpha = a_new;
+  } else {
+    s->breakdowns += 1;  // reading A5: keep the previous alpha
+  }
+}
+
+__global__ void __launch_bounds__(kT) finalize_kernel(const double* __restrict__ part, int64_t nchunks, int mode,
+                                                      DevScalars* __restrict__ s) {
+  if (s->done) return;
+  __shared__ double red[4 * kT];
+  finalize_block(part, nchunks, mode, s, red);
+}
+
 enum DtMode { kDtIter = 0, kDtAlpha0 = 1, kDtG0 = 2, kDtInitQ = 3 };
 
-// One CTA per chunk c in [c0, c0 + gridDim.x).
-template <int KIND, int MODE>
+// One CTA per chunk c in [c0, c0 + gridDim.x).  FUSE (1 GPU): the last CTA to finish
+// (threadfence + counter) also runs K-FINALIZE, saving a launch per iteration; the sums are
+// the same fixed-order sums as the separate finalize kernel.
+template <int KIND, int MODE, bool FUSE>
 __global__ void __launch_bounds__(kT) dt_kernel(
     const int32_t* __restrict__ first_ptr, int64_t n, int64_t c0, const int32_t* __restrict__ ci,
     const int32_t* __restrict__ cj, const double4* __restrict__ nrm4, const double4* __restrict__ rxn4,
     const double4* __restrict__ u4, const double* __restrict__ q, const double* __restrict__ gam_new,
     const double* __restrict__ gam_old, const double* __restrict__ g_old, double* __restrict__ g_out,
-    double* __restrict__ part, const int32_t* __restrict__ done) {
+    double* __restrict__ part, const int32_t* __restrict__ done, int64_t nchunks, DevScalars* __restrict__ sc,
+    unsigned int* __restrict__ counter) {
   if (done != nullptr && *done) return;
   __shared__ double red[4 * kT];
   const int64_t c = c0 + blockIdx.x;
@@ -161,61 +226,16 @@ __global__ void __launch_bounds__(kT) dt_kernel(
   }
   block_reduce4(p, red);
   if (threadIdx.x < 4) part[c * 4 + threadIdx.x] = p[threadIdx.x];
-}
-
-// Sums chunk partials in fixed order and advances the BBPGD scalars.
-// mode 0: after Step 10 of iteration j; mode 1: alpha_0 (Step 6); mode 2: phi_0 (Step 3).
-__global__ void __launch_bounds__(kT) finalize_kernel(const double* __restrict__ part, int64_t nchunks, int mode,
-                                                      DevScalars* __restrict__ s) {
-  if (s->done) return;
-  __shared__ double red[4 * kT];
-  double p[4] = {0, 0, 0, 0};
-  for (int64_t c = threadIdx.x; c < nchunks; c += kT) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) p[k] += part[c * 4 + k];
-  }
-  block_reduce4(p, red);
-  if (threadIdx.x != 0) return;
-  for (int k = 0; k < 4; ++k) s->p[k] = p[k];
-  if (mode == 1) {
-    const double a = p[0] / p[1];  // alpha_0 = g0.g0 / g0.M g0
-    if (!(isfinite(a) && a > 0.0)) {
-      s->nonfinite = 1;
-      s->done = 1;
-    } else {
-      s->alpha = a;
-    }
-    return;
-  }
-  const double phi = sqrt(p[3]);
-  s->phi = phi;
-  if (!isfinite(phi)) {
-    s->nonfinite = 1;
-    s->done = 1;
-    return;
-  }
-  s->conv = phi < s->tol ? 1 : 0;
-  if (mode == 2) {
-    if (s->conv) s->done = 1;
-    return;
-  }
-  const int j = s->iter + 1;
-  s->iter = j;
-  if (s->fixed) {
-    if (j >= s->max_iter) {
-      s->done = 1;
-      return;
-    }
-  } else if (s->conv || j >= s->max_iter) {
-    s->done = 1;
-    return;
-  }
-  const bool bb2 = s->bb_mode == 1 || (s->bb_mode == 2 && (j % 2 == 0));
-  const double a_new = bb2 ? p[1] / p[2] : p[0] / p[1];
-  if (p[1] > 0.0 && isfinite(a_new) && a_new > 0.0) {
-    s->alpha = a_new;
-  } else {
-    s->breakdowns += 1;  // reading A5: keep the previous alpha
+  if (FUSE) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    finalize_block(part, nchunks, MODE == kDtIter ? 0 : (MODE == kDtAlpha0 ? 1 : 2), sc, red);
+    if (threadIdx.x == 0) *counter = 0u;
   }
 }
 
@@ -375,17 +395,25 @@ int launch_proj_own(sc_ctx* ctx, const double* gam_old, const double* g_old, dou
 }
 
 int launch_dt(sc_ctx* ctx, int mode, const double* gam_new, const double* gam_old, const double* g_old,
-              double* g_out, int64_t c0, int64_t c1) {
+              double* g_out, int64_t c0, int64_t c1, bool fuse) {
   if (c1 <= c0) return 0;
+  if (fuse && (c0 != 0 || c1 != ctx->nchunks)) return fail(ctx, SC_EINVAL, "fused finalize needs all chunks");
   const unsigned grid = static_cast<unsigned>(c1 - c0);
   const int32_t* done = &ctx->dsc->done;
   const double4* u4 = ctx->u4.p;
   double* part = ctx->chunk_part.p;
   const double* q = ctx->q.p;
-#define SC_DT(KIND, MODE)                                                                                      \
-  dt_kernel<KIND, MODE><<<grid, kT, 0, ctx->stream>>>(ctx->first_ptr.p, ctx->n, c0, ctx->ci.p, ctx->cj.p,      \
-                                                      ctx->nrm4.p, ctx->rxn4.p, u4, q, gam_new, gam_old, g_old, \
-                                                      g_out, part, done)
+#define SC_DT(KIND, MODE)                                                                                       \
+  do {                                                                                                          \
+    if (fuse)                                                                                                   \
+      dt_kernel<KIND, MODE, true><<<grid, kT, 0, ctx->stream>>>(                                                \
+          ctx->first_ptr.p, ctx->n, c0, ctx->ci.p, ctx->cj.p, ctx->nrm4.p, ctx->rxn4.p, u4, q, gam_new, gam_old, \
+          g_old, g_out, part, done, ctx->nchunks, ctx->dsc, ctx->dcount);                                       \
+    else                                                                                                        \
+      dt_kernel<KIND, MODE, false><<<grid, kT, 0, ctx->stream>>>(                                               \
+          ctx->first_ptr.p, ctx->n, c0, ctx->ci.p, ctx->cj.p, ctx->nrm4.p, ctx->rxn4.p, u4, q, gam_new, gam_old, \
+          g_old, g_out, part, done, ctx->nchunks, ctx->dsc, ctx->dcount);                                       \
+  } while (0)
   timer_begin(ctx, SC_K_DT);
   if (ctx->kind == kSpheres) {
     switch (mode) {

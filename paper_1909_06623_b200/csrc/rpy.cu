@@ -22,6 +22,7 @@
 //    fixed order by rpy_combine (deterministic, independent of the number of
 //    GPUs).  Inside a split: plain FP64 sums over a 128-source tile, then a
 //    compensated (TwoSum) add of each tile sum.
+#include <algorithm>
 #include <cstdio>
 #include <vector>
 
@@ -315,17 +316,17 @@ constexpr size_t kRpySmem = 4 * kRpyTile * sizeof(double4) + 2 * sizeof(uint64_t
 // Output: part[slot][row][3] with slot = the partner super-block: rows of SI get slot SJ
 // (forward), rows of SJ get slot SI (reverse), so every (slot, row) is written exactly
 // once per apply and rpy_combine sums the NS slots of a row in a fixed order.
-constexpr int kSymThreads = 128;
-constexpr int kSymTpt = 4;
-constexpr int kSymSB = kSymThreads * kSymTpt;  // 512 bodies per super-block
+constexpr int kSymSB = 512;                    // bodies per super-block
+// (warps, targets per lane) variants with NW * TPT * 32 = kSymSB; ctx->sym_variant picks one
 constexpr int kSymNsub = kSymSB / 32;          // 16 sub-blocks of 32
 constexpr size_t kSymSmem = 2 * kSymSB * sizeof(double4) + 3 * kSymSB * sizeof(double) + 16;
 
-template <bool POLY>
-__global__ void __launch_bounds__(kSymThreads, 3)
+template <bool POLY, int NW, int TPT, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
     rpy_sym_kernel(const double4* __restrict__ pos4, const double4* __restrict__ f4, const int2* __restrict__ pairs,
                    int64_t npad, Consts k, double* __restrict__ part, const int32_t* __restrict__ done) {
-  constexpr int TPT = kSymTpt;
+  static_assert(NW * TPT * 32 == kSymSB, "super-block size");
+  constexpr int kSymThreads = NW * 32;
   if (done != nullptr && *done) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double4* sp = reinterpret_cast<double4*>(smem_raw);  // SJ positions
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(kSymThreads, 3)
   double fx[TPT], fy[TPT], fz[TPT], ax[TPT], ay[TPT], az[TPT];
 #pragma unroll
   for (int m = 0; m < TPT; ++m) {
-    const int64_t row = SI * kSymSB + (w + 4 * m) * 32 + lane;
+    const int64_t row = SI * kSymSB + (w + NW * m) * 32 + lane;
     p[m] = pos4[row];
     const double4 f = f4[row];
     fx[m] = f.x;
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(kSymThreads, 3)
   // forward sums: rows of SI, slot SJ
 #pragma unroll
   for (int m = 0; m < TPT; ++m) {
-    const int64_t row = SI * kSymSB + (w + 4 * m) * 32 + lane;
+    const int64_t row = SI * kSymSB + (w + NW * m) * 32 + lane;
     double* o = part + (SJ * npad + row) * 3;
     o[0] = ax[m];
     o[1] = ay[m];
@@ -463,29 +464,112 @@ __global__ void __launch_bounds__(kSymThreads, 3)
 bool rpy_use_sym(const sc_ctx* ctx) {
   if (ctx->rpy_mode == 1) return false;
   if (ctx->rpy_mode == 2) return true;
-  // auto: one GPU (real), enough super-blocks to fill the machine
-  return ctx->world == 1 && ctx->emul_world <= 1 && ctx->npad >= 8 * kSymSB;
+  // auto: enough super-blocks to fill the machine
+  return ctx->npad >= 8 * kSymSB;
 }
 
-int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done) {
-  const int64_t nsb = (ctx->npad + kSymSB - 1) / kSymSB;
-  const int64_t npad_sym = nsb * kSymSB;
-  if (npad_sym != ctx->npad) return fail(ctx, SC_EINVAL, "symmetric RPY needs npad % 512 == 0");
-  // pair table (SI <= SJ), rebuilt when the number of super-blocks changes
-  if (ctx->sym_nsb != nsb) {
-    std::vector<int2> tab;
-    tab.reserve(nsb * (nsb + 1) / 2);
-    for (int64_t i = 0; i < nsb; ++i)
-      for (int64_t j = i; j < nsb; ++j) tab.push_back(make_int2(static_cast<int>(i), static_cast<int>(j)));
-    if (int rc = ensure(ctx, ctx->sym_pairs, tab.size())) return rc;
-    SC_CUDA(cudaMemcpyAsync(ctx->sym_pairs.p, tab.data(), tab.size() * sizeof(int2), cudaMemcpyHostToDevice,
-                            ctx->stream));
-    SC_CUDA(cudaStreamSynchronize(ctx->stream));
-    ctx->sym_nsb = nsb;
+// Cyclic-half assignment of super-block pairs: super-block S evaluates (S, S) and
+// (S, S+d mod NS) for d in D(S) = {1 .. (NS-1)/2} (+ {NS/2} if NS is even and S < NS/2).
+// Every unordered pair appears exactly once and every S carries ~NS/2 pairs, so a
+// contiguous range of super-blocks per rank balances the ranks.  The orientation of a
+// pair (which side is "SI") depends on NS only, so the slot contents -- and with one GPU
+// or an emulated world the result -- are the same for any number of ranks.
+static bool sym_in_D(int64_t S, int64_t d, int64_t NS) {
+  if (d <= 0 || d >= NS) return false;
+  if (d <= (NS - 1) / 2) return true;
+  return NS % 2 == 0 && d == NS / 2 && S < NS / 2;
+}
+__device__ __forceinline__ bool sym_in_D_dev(int64_t S, int64_t d, int64_t NS) {
+  if (d <= 0 || d >= NS) return false;
+  if (d <= (NS - 1) / 2) return true;
+  return NS % 2 == 0 && d == NS / 2 && S < NS / 2;
+}
+static void sym_rank_range(int64_t NS, int W, int r, int64_t* s0, int64_t* s1) {
+  const int64_t spr = (NS + W - 1) / W;
+  *s0 = std::min<int64_t>(NS, r * spr);
+  *s1 = std::min<int64_t>(NS, (r + 1) * spr);
+}
+
+// Combine for the symmetric kernel: sums, in increasing slot order (TwoSum), the slots this
+// rank wrote for the row (all of them when s0 = 0, s1 = NS), adds the self and near-list
+// terms for owned rows, scales by 1/(8 pi mu).
+template <bool POLY>
+__global__ void rpy_sym_combine_kernel(const double* __restrict__ part, int64_t NS, int64_t s0, int64_t s1,
+                                       int64_t npad, int64_t n, double scale, const double4* __restrict__ pos4,
+                                       const double4* __restrict__ f4, const int32_t* __restrict__ near_ptr,
+                                       const int32_t* __restrict__ near_idx, double4* __restrict__ out,
+                                       const int32_t* __restrict__ done, int32_t* __restrict__ err) {
+  if (done != nullptr && *done) return;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= npad) return;
+  const int64_t T = row / kSymSB;
+  const bool own_row = T >= s0 && T < s1;
+  const bool all = s0 == 0 && s1 == NS;
+  double hx = 0, hy = 0, hz = 0, lx = 0, ly = 0, lz = 0;
+  for (int64_t s = 0; s < NS; ++s) {
+    if (!all) {
+      const bool fwd = own_row && (s == T || sym_in_D_dev(T, (s - T + NS) % NS, NS));
+      const bool rev = s >= s0 && s < s1 && s != T && sym_in_D_dev(s, (T - s + NS) % NS, NS);
+      if (!fwd && !rev) continue;
+    }
+    const double* p = part + (s * npad + row) * 3;
+    two_sum_acc(hx, lx, p[0]);
+    two_sum_acc(hy, ly, p[1]);
+    two_sum_acc(hz, lz, p[2]);
   }
-  const int64_t npairs = nsb * (nsb + 1) / 2;
-  if (int rc = ensure(ctx, ctx->rpy_part, static_cast<size_t>(nsb) * ctx->npad * 3)) return rc;
-  const double a = ctx->a_const;
+  if (row < n && own_row) {
+    const double4 pi = pos4[row];
+    const double4 fi = f4[row];
+    const double cs = (2.0 / 3.0) / pi.w;  // self: 4/(3 a_i)
+    two_sum_acc(hx, lx, cs * fi.x);
+    two_sum_acc(hy, ly, cs * fi.y);
+    two_sum_acc(hz, lz, cs * fi.z);
+    const double a_mono = 2.0 * pi.w;
+    const long long near_bits = __double_as_longlong(4.0 * (a_mono * a_mono));
+    for (int32_t e = near_ptr[row]; e < near_ptr[row + 1]; ++e) {
+      const int32_t j = near_idx[e];
+      const double4 pj = pos4[j];
+      const double4 fj = f4[j];
+      double dx, dy, dz;
+      const double r2 = rpy_r2(pi, pj, dx, dy, dz);
+      const double abar = POLY ? pi.w + pj.w : a_mono;
+      if (!rpy_is_near(r2, abar, POLY, near_bits)) continue;
+      double rr = 0.0, rs = 0.0;
+      if (r2 > 0.0) {
+        rs = rsqrt_dp(r2);
+        rr = r2 * rs;
+      } else {
+        atomicExch(err, 1);  // coincident centres (reading A12)
+      }
+      const double ia = 1.0 / abar;
+      const double c1 = (4.0 / 3.0) * ia * fma(-9.0 / 32.0 * ia, rr, 1.0);
+      const double c2 = 0.125 * ia * ia * rs;
+      const double t = c2 * fma(dz, fj.z, fma(dy, fj.y, dx * fj.x));
+      two_sum_acc(hx, lx, fma(t, dx, c1 * fj.x));
+      two_sum_acc(hy, ly, fma(t, dy, c1 * fj.y));
+      two_sum_acc(hz, lz, fma(t, dz, c1 * fj.z));
+    }
+  }
+  out[row] = row < n ? make_double4(scale * (hx + lx), scale * (hy + ly), scale * (hz + lz), 0.0)
+                     : make_double4(0.0, 0.0, 0.0, 0.0);
+}
+
+__global__ void sum_ranks_kernel(const double4* __restrict__ parts, int W, int64_t npad, double4* __restrict__ u4,
+                                 const int32_t* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= npad) return;
+  double4 s = parts[row];
+  for (int r = 1; r < W; ++r) {
+    const double4 v = parts[r * npad + row];
+    s.x += v.x;
+    s.y += v.y;
+    s.z += v.z;
+  }
+  u4[row] = s;
+}
+
+static Consts make_consts(double a) {
   Consts k;
   k.k23a2 = 2.0 / 3.0 * a * a;
   k.m2a2 = -2.0 * a * a;
@@ -494,34 +578,100 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
   k.kn3 = 1.0 / (8.0 * a * a);
   const double n2 = 4.0 * a * a;
   k.near_bits = *reinterpret_cast<const long long*>(&n2);
+  return k;
+}
+
+// u4 = RPY(f4) with the symmetric kernel.  ranks: the ranks whose pairs this process
+// evaluates (W = 1: everything).  mode 0: one GPU -> combine all slots into u4;
+// mode 1: emulated world -> per-rank combine into ctx->upart, rank-ordered sum into u4;
+// mode 2: real multi-GPU -> this rank's combine into u4 (the caller all-reduces it).
+int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done, int W,
+                  const std::vector<int>& ranks, int mode) {
+  const int64_t NS = ctx->npad / kSymSB;
+  if (NS * kSymSB != ctx->npad) return fail(ctx, SC_EINVAL, "symmetric RPY needs npad % 512 == 0");
+  if (ctx->sym_nsb != NS || ctx->sym_world != W) {  // pair tables of every rank, concatenated
+    std::vector<int2> tab;
+    std::vector<int64_t> off(1, 0);
+    for (int r = 0; r < W; ++r) {
+      int64_t a0, a1;
+      sym_rank_range(NS, W, r, &a0, &a1);
+      for (int64_t S = a0; S < a1; ++S) {
+        tab.push_back(make_int2(static_cast<int>(S), static_cast<int>(S)));
+        for (int64_t d = 1; d < NS; ++d)
+          if (sym_in_D(S, d, NS)) tab.push_back(make_int2(static_cast<int>(S), static_cast<int>((S + d) % NS)));
+      }
+      off.push_back(static_cast<int64_t>(tab.size()));
+    }
+    if (int rc = ensure(ctx, ctx->sym_pairs, tab.size())) return rc;
+    SC_CUDA(cudaMemcpyAsync(ctx->sym_pairs.p, tab.data(), tab.size() * sizeof(int2), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    SC_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->sym_nsb = NS;
+    ctx->sym_world = W;
+    ctx->sym_off = off;
+  }
+  if (int rc = ensure(ctx, ctx->rpy_part, static_cast<size_t>(NS) * ctx->npad * 3)) return rc;
+  const Consts k = make_consts(ctx->a_const);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(rpy_sym_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
-    cudaFuncSetAttribute(rpy_sym_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem);
+#define SC_ATTR(P, NW, TPT, MINB) \
+  cudaFuncSetAttribute(rpy_sym_kernel<P, NW, TPT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem)
+    SC_ATTR(false, 4, 4, 3); SC_ATTR(true, 4, 4, 3); SC_ATTR(false, 8, 2, 2); SC_ATTR(true, 8, 2, 2);
+    SC_ATTR(false, 4, 4, 4); SC_ATTR(true, 4, 4, 4); SC_ATTR(false, 16, 1, 1); SC_ATTR(true, 16, 1, 1);
+#undef SC_ATTR
     attr_set = true;
   }
-  timer_begin(ctx, SC_K_RPY);
-  if (ctx->poly)
-    rpy_sym_kernel<true><<<static_cast<unsigned>(npairs), kSymThreads, kSymSmem, ctx->stream>>>(
-        ctx->pos4.p, f4, ctx->sym_pairs.p, ctx->npad, k, ctx->rpy_part.p, done);
-  else
-    rpy_sym_kernel<false><<<static_cast<unsigned>(npairs), kSymThreads, kSymSmem, ctx->stream>>>(
-        ctx->pos4.p, f4, ctx->sym_pairs.p, ctx->npad, k, ctx->rpy_part.p, done);
-  timer_end(ctx, SC_K_RPY);
-  if (int rc = check_launch(ctx, "rpy_sym")) return rc;
+  for (int r : ranks) {
+    const int64_t p0 = ctx->sym_off[r], np = ctx->sym_off[r + 1] - p0;
+    if (np == 0) continue;
+    const unsigned g = static_cast<unsigned>(np);
+    const int2* pt = ctx->sym_pairs.p + p0;
+    timer_begin(ctx, SC_K_RPY);
+#define SC_SYM(P, NW, TPT, MINB)                                                                   \
+  rpy_sym_kernel<P, NW, TPT, MINB><<<g, NW * 32, kSymSmem, ctx->stream>>>(ctx->pos4.p, f4, pt, ctx->npad, k, \
+                                                                         ctx->rpy_part.p, done)
+    switch (ctx->sym_variant) {
+      case 1: if (ctx->poly) SC_SYM(true, 8, 2, 2); else SC_SYM(false, 8, 2, 2); break;
+      case 2: if (ctx->poly) SC_SYM(true, 4, 4, 4); else SC_SYM(false, 4, 4, 4); break;
+      case 3: if (ctx->poly) SC_SYM(true, 16, 1, 1); else SC_SYM(false, 16, 1, 1); break;
+      default: if (ctx->poly) SC_SYM(true, 4, 4, 3); else SC_SYM(false, 4, 4, 3); break;
+    }
+#undef SC_SYM
+    timer_end(ctx, SC_K_RPY);
+    if (int rc = check_launch(ctx, "rpy_sym")) return rc;
+  }
   const double scale = 1.0 / (8.0 * 3.14159265358979323846 * mu);
-  const int64_t nrows = ctx->npad;
+  const int64_t npad = ctx->npad;
+  const unsigned nb = static_cast<unsigned>((npad + 255) / 256);
+  auto combine = [&](int64_t s0, int64_t s1, double4* out) -> int {
+    timer_begin(ctx, SC_K_COMBINE);
+    if (ctx->poly)
+      rpy_sym_combine_kernel<true><<<nb, 256, 0, ctx->stream>>>(ctx->rpy_part.p, NS, s0, s1, npad, ctx->n, scale,
+                                                               ctx->pos4.p, f4, ctx->near_ptr.p, ctx->near_idx.p,
+                                                               out, done, ctx->derr);
+    else
+      rpy_sym_combine_kernel<false><<<nb, 256, 0, ctx->stream>>>(ctx->rpy_part.p, NS, s0, s1, npad, ctx->n, scale,
+                                                                ctx->pos4.p, f4, ctx->near_ptr.p, ctx->near_idx.p,
+                                                                out, done, ctx->derr);
+    timer_end(ctx, SC_K_COMBINE);
+    return check_launch(ctx, "rpy_sym_combine");
+  };
+  if (mode == 0) return combine(0, NS, u4);
+  if (mode == 2) {
+    int64_t a0, a1;
+    sym_rank_range(NS, W, ranks.front(), &a0, &a1);
+    return combine(a0, a1, u4);
+  }
+  if (int rc = ensure(ctx, ctx->upart, static_cast<size_t>(W) * npad)) return rc;
+  for (int r = 0; r < W; ++r) {
+    int64_t a0, a1;
+    sym_rank_range(NS, W, r, &a0, &a1);
+    if (int rc = combine(a0, a1, ctx->upart.p + r * npad)) return rc;
+  }
   timer_begin(ctx, SC_K_COMBINE);
-  if (ctx->poly)
-    rpy_combine_kernel<true><<<static_cast<unsigned>((nrows + 255) / 256), 256, 0, ctx->stream>>>(
-        ctx->rpy_part.p, static_cast<int>(nsb), 0, nrows, ctx->n, scale, ctx->pos4.p, f4, ctx->near_ptr.p,
-        ctx->near_idx.p, u4, done, ctx->derr);
-  else
-    rpy_combine_kernel<false><<<static_cast<unsigned>((nrows + 255) / 256), 256, 0, ctx->stream>>>(
-        ctx->rpy_part.p, static_cast<int>(nsb), 0, nrows, ctx->n, scale, ctx->pos4.p, f4, ctx->near_ptr.p,
-        ctx->near_idx.p, u4, done, ctx->derr);
+  sum_ranks_kernel<<<nb, 256, 0, ctx->stream>>>(ctx->upart.p, W, npad, u4, done);
   timer_end(ctx, SC_K_COMBINE);
-  return check_launch(ctx, "rpy_combine_sym");
+  return check_launch(ctx, "sum_ranks");
 }
 
 namespace {

@@ -108,11 +108,16 @@ struct sc_ctx {
   sc::DBuf<double> rpy_part;    // nsplit * rows * 3
   int nsplit = 1;
   int rpy_mode = 0;             // 0 auto, 1 target-row kernel, 2 symmetric pair-tile kernel
-  int64_t sym_nsb = -1;         // super-blocks the pair table was built for
-  sc::DBuf<int2> sym_pairs;     // (SI, SJ), SI <= SJ
+  int sym_variant = 0;          // tuning: (warps, targets/lane) of the symmetric kernel (env SC_SYM_VARIANT)
+  int64_t sym_nsb = -1;         // super-blocks the pair tables were built for
+  int sym_world = -1;           // ... and the number of ranks
+  sc::DBuf<int2> sym_pairs;     // (SI, SJ) of every rank, concatenated (cyclic-half assignment)
+  std::vector<int64_t> sym_off; // rank r's pairs: [sym_off[r], sym_off[r+1])
+  sc::DBuf<double4> upart;      // emulated world: per-rank partial velocities
   sc::DevScalars* dsc = nullptr;   // device scalars
   sc::DevScalars* hsc = nullptr;   // pinned mirror
   int32_t* derr = nullptr;         // device error flag
+  unsigned int* dcount = nullptr;  // last-CTA counter of the fused D^T + finalize
   int32_t* herr = nullptr;         // pinned mirror
 
   // scratch for contacts
@@ -178,7 +183,8 @@ int rpy_apply_rows(sc_ctx* ctx, const double4* f4, int64_t row0, int64_t nrows, 
                    double4* u4, const int32_t* done);
 int choose_nsplit(int64_t npad, int world);
 bool rpy_use_sym(const sc_ctx* ctx);
-int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done);
+int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done, int W,
+                  const std::vector<int>& ranks, int mode);
 
 // ---- LCP kernels (lcp.cu) -------------------------------------------------
 // gather F = D v (mode raw) or F = D max(0, gam_old - alpha g_old) with the owner
@@ -192,7 +198,7 @@ int launch_proj_own(sc_ctx* ctx, const double* gam_old, const double* g_old, dou
 // D^T: mode 0 iteration (g_new = D^T U + q, partials ss,sy,yy,mm), mode 1 alpha0
 // (w = D^T U, partials g.g, g.w), mode 2 (g = D^T U + q, partial mm) ; chunks [c0,c1)
 int launch_dt(sc_ctx* ctx, int mode, const double* gam_new, const double* gam_old,
-              const double* g_old, double* g_out, int64_t c0, int64_t c1);
+              const double* g_old, double* g_out, int64_t c0, int64_t c1, bool fuse);
 int launch_dt_user(sc_ctx* ctx, const double* UW, double* out, const double* addq, double qscale);
 int launch_finalize(sc_ctx* ctx, int mode, const double* part);
 int launch_init_g0(sc_ctx* ctx, const double* q, double* g0, int64_t c0, int64_t c1);

@@ -62,3 +62,33 @@ def test_emulated_world_more_ranks_than_blocks(ctx):
     ref = _solve(ctx, p, 1, 2000, False)
     r = _solve(ctx, p, 5, 2000, False)
     assert torch.equal(r["gamma"], ref["gamma"]) and torch.equal(r["Uc"], ref["Uc"])
+
+
+@pytest.mark.parametrize("name,n,max_iter,fixed", [("C5", 9000, 25, True), ("C3", 6000, 40, True)])
+def test_emulated_ranks_symmetric_kernel(ctx, name, n, max_iter, fixed):
+    """The symmetric RPY kernel's multi-GPU unit: ranks evaluate disjoint super-block pairs,
+    combine the slots they wrote and the partial velocities are summed (all-reduce).  Equal to
+    one GPU up to the grouping of that final sum."""
+    p = make_problem(name, n=n)
+
+    def solve(world):
+        ctx.set_rpy_kernel(2)
+        ctx.set_emulated_world(world)
+        ctx.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+        ctx.assemble_D()
+        U = ctx.mobility_apply(_cuda(p.force), mu=p.mu)
+        ctx.lcp_q(p.dt, U)
+        r = ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=max_iter, fixed_iters=fixed)
+        r["U_ext"] = U
+        ctx.set_emulated_world(1)
+        ctx.set_rpy_kernel(0)
+        return r
+
+    ref = solve(1)
+    for world in (2, 3, 8):
+        r = solve(world)
+        du = (r["U_ext"] - ref["U_ext"]).norm() / ref["U_ext"].norm()
+        assert du <= 1e-14, (world, float(du))
+        dg = (r["gamma"] - ref["gamma"]).norm() / ref["gamma"].norm()
+        assert dg <= 1e-9, (world, float(dg))
+        assert r["iters"] == ref["iters"]
