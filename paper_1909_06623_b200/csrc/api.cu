@@ -463,7 +463,7 @@ void sc_destroy(sc_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   release(ctx->pos4); release(ctx->dir4); release(ctx->rodmob4);
   release(ctx->ci); release(ctx->cj); release(ctx->nrm4); release(ctx->lev4); release(ctx->rxn4);
-  release(ctx->row_ptr); release(ctx->inc); release(ctx->first_ptr); release(ctx->near_ptr); release(ctx->near_idx);
+  release(ctx->row_ptr); release(ctx->inc); release(ctx->icol4); release(ctx->first_ptr); release(ctx->near_ptr); release(ctx->near_idx);
   release(ctx->q); release(ctx->gam[0]); release(ctx->gam[1]); release(ctx->g[0]); release(ctx->g[1]);
   release(ctx->w); release(ctx->gam_user); release(ctx->chunk_part); release(ctx->chunk_red);
   release(ctx->sym_pairs); release(ctx->upart); release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);

@@ -46,6 +46,23 @@ __global__ void incidence_sort(const int32_t* __restrict__ row_ptr, int64_t n, i
   }
 }
 
+// Signed D_l block of every incidence, in incidence (per-body) order, so the spheres'
+// D-gather streams it: sigma n, sigma = +1 on i, -1 on j.
+template <int KIND>
+__global__ void incidence_columns(const int32_t* __restrict__ inc, int64_t ninc, const double4* __restrict__ nrm4,
+                                  const double4* __restrict__ /*rxn4*/, double4* __restrict__ icol4) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= ninc) return;
+  const int32_t v = inc[e];
+  const int32_t l = v >> 1;
+  const int side = v & 1;
+  const double sg = side ? -1.0 : 1.0;
+  const double4 n = nrm4[l];
+  if (KIND == kSpheres) {
+    icol4[e] = make_double4(sg * n.x, sg * n.y, sg * n.z, 0.0);
+  }
+}
+
 __global__ void rod_columns(const double4* __restrict__ nrm4, const double4* __restrict__ lev4, int64_t nc,
                             double4* __restrict__ rxn4) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -91,6 +108,15 @@ int assemble(sc_ctx* ctx) {
       rod_columns<<<nblk(nc), kT, 0, ctx->stream>>>(ctx->nrm4.p, ctx->lev4.p, nc, ctx->rxn4.p);
       timer_end(ctx, SC_K_ASSEMBLE);
       if (int rc = check_launch(ctx, "rod_columns")) return rc;
+    }
+    if (ctx->kind == kSpheres) {  // (rods gather from the per-constraint columns)
+      const int64_t ninc = 2 * nc;
+      if (int rc = ensure(ctx, ctx->icol4, ninc)) return rc;
+      timer_begin(ctx, SC_K_ASSEMBLE);
+      incidence_columns<kSpheres><<<nblk(ninc), kT, 0, ctx->stream>>>(ctx->inc.p, ninc, ctx->nrm4.p, nullptr,
+                                                                      ctx->icol4.p);
+      timer_end(ctx, SC_K_ASSEMBLE);
+      if (int rc = check_launch(ctx, "incidence_columns")) return rc;
     }
   }
   ctx->nchunks = ctx->npad / kChunkBodies;

@@ -679,7 +679,7 @@ namespace {
 
 int choose_nsplit(int64_t npad, int world) {
   (void)world;  // must not depend on the number of GPUs (bitwise P-invariance)
-  int64_t s = npad / 512;
+  int64_t s = npad / 128;  // >= one 128-source tile per split; small N still fills several SMs
   int ns = 1;
   while (ns * 2 <= s && ns < 32) ns *= 2;
   return ns;

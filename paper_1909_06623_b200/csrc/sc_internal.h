@@ -91,6 +91,7 @@ struct sc_ctx {
   bool assembled = false;
   sc::DBuf<int32_t> row_ptr;    // n+1
   sc::DBuf<int32_t> inc;        // 2*nc: (l << 1) | side
+  sc::DBuf<double4> icol4;      // signed D blocks per incidence (spheres 1, rods 2 double4)
   sc::DBuf<int32_t> first_ptr;  // n+1: constraints with first body < b start at first_ptr[b]
   sc::DBuf<int32_t> near_ptr, near_idx;  // spheres: RPY overlap-branch partners per body (CSR)
   int64_t nchunks = 0;
