@@ -420,6 +420,7 @@ static int create_common(sc_ctx** out, int device, void* stream) {
   cudaMemset(ctx->dcount, 0, sizeof(unsigned int));
   cudaMemset(ctx->dsc, 0, sizeof(DevScalars));
   if (const char* v = std::getenv("SC_SYM_VARIANT")) ctx->sym_variant = std::atoi(v);
+  if (const char* v = std::getenv("SC_NO_GRAPHS")) ctx->use_graphs = std::atoi(v) == 0;
   *ctx->herr = 0;
   *out = ctx;
   return SC_OK;
@@ -820,32 +821,72 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     const double t_iter = spheres ? 1.3e-12 * static_cast<double>(ctx->npad) * ctx->npad + 4e-5
                                   : 2e-5 + 1.2e-10 * static_cast<double>(nc + n);
     const int batch = (dist && !D.emul) ? 1 : std::max(1, std::min(32, static_cast<int>(1e-3 / t_iter)));
+    auto enqueue_iter = [&](int pp) -> int {
+      double* go = ctx->g[pp].p;
+      double* gmo = ctx->gam[pp].p;
+      double* gmn = ctx->gam[pp ^ 1].p;
+      double* gn = ctx->g[pp ^ 1].p;
+      if (dist) {  // Steps 8-9 on own constraints, then every rank needs the full gamma_j
+        if (int rc = D.proj_own(gmo, go, gmn)) return rc;
+        if (int rc = D.bcast(gmn)) return rc;
+        if (int rc = mvop_raw(gmn)) return rc;
+      } else {  // Steps 8-9 fused into the D-gather
+        if (int rc = launch_gather_proj(ctx, gmo, go, gmn, mu)) return rc;
+        if (spheres) {
+          if (int rc = D.rpy(mu, done)) return rc;
+        }
+      }
+      if (int rc = D.dt(0, gmn, gmo, go, gn, &fused)) return rc;  // Steps 10-15
+      return reduce(0);
+    };
+    // Small problems (several iterations per host read, one GPU, no per-launch timing): the
+    // two-iteration kernel sequence (even + odd buffer parity) is captured once into a CUDA
+    // graph and replayed, removing per-kernel launch gaps.
+    cudaGraphExec_t gexec = nullptr;
+    int64_t graph_kernels = 0;
+    if (batch >= 4 && !dist && !ctx->timer.enabled && ctx->use_graphs) {
+      cudaGraph_t graph = nullptr;
+      const int64_t l0 = ctx->launch_count;
+      SC_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      int rc0 = enqueue_iter(0);
+      if (rc0 == 0) rc0 = enqueue_iter(1);
+      cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+      if (rc0 != 0) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc0;
+      }
+      if (ce != cudaSuccess) return cuda_fail(ctx, ce, "cudaStreamEndCapture");
+      ce = cudaGraphInstantiate(&gexec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess) return cuda_fail(ctx, ce, "cudaGraphInstantiate");
+      graph_kernels = ctx->launch_count - l0;
+      ctx->launch_count = l0;
+    }
     int enq = 0;
     while (enq < opts->max_iter) {
-      const int nb = std::min(batch, opts->max_iter - enq);
-      for (int k = 0; k < nb; ++k) {
-        const int pp = (enq + k) & 1;
-        double* go = ctx->g[pp].p;
-        double* gmo = ctx->gam[pp].p;
-        double* gmn = ctx->gam[pp ^ 1].p;
-        double* gn = ctx->g[pp ^ 1].p;
-        if (dist) {  // Steps 8-9 on own constraints, then every rank needs the full gamma_j
-          if (int rc = D.proj_own(gmo, go, gmn)) return rc;
-          if (int rc = D.bcast(gmn)) return rc;
-          if (int rc = mvop_raw(gmn)) return rc;
-        } else {  // Steps 8-9 fused into the D-gather
-          if (int rc = launch_gather_proj(ctx, gmo, go, gmn, mu)) return rc;
-          if (spheres) {
-            if (int rc = D.rpy(mu, done)) return rc;
+      int nb = std::min(batch, opts->max_iter - enq);
+      if (gexec) {
+        nb = (nb + 1) & ~1;  // whole graph replays; iterations past j_max are no-ops (done flag)
+        for (int k = 0; k < nb; k += 2) {
+          cudaError_t ce = cudaGraphLaunch(gexec, ctx->stream);
+          if (ce != cudaSuccess) {
+            cudaGraphExecDestroy(gexec);
+            return cuda_fail(ctx, ce, "cudaGraphLaunch");
           }
+          ctx->launch_count += graph_kernels;
         }
-        if (int rc = D.dt(0, gmn, gmo, go, gn, &fused)) return rc;  // Steps 10-15
-        if (int rc = reduce(0)) return rc;
+      } else {
+        for (int k = 0; k < nb; ++k)
+          if (int rc = enqueue_iter((enq + k) & 1)) return rc;
       }
       enq += nb;
-      if (int rc = read_scalars(ctx)) return rc;
+      if (int rc = read_scalars(ctx)) {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        return rc;
+      }
       if (ctx->hsc->done) break;
     }
+    if (gexec) cudaGraphExecDestroy(gexec);
     parity = ctx->hsc->iter & 1;
     stt.iters = ctx->hsc->iter;
     stt.mvops = 2 + ctx->hsc->iter;

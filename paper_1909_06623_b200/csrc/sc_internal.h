@@ -109,6 +109,7 @@ struct sc_ctx {
   sc::DBuf<double> rpy_part;    // nsplit * rows * 3
   int nsplit = 1;
   int rpy_mode = 0;             // 0 auto, 1 target-row kernel, 2 symmetric pair-tile kernel
+  bool use_graphs = true;       // CUDA-graph replay of small-problem iteration batches (env SC_NO_GRAPHS=1: off)
   int sym_variant = 0;          // tuning: (warps, targets/lane) of the symmetric kernel (env SC_SYM_VARIANT)
   int64_t sym_nsb = -1;         // super-blocks the pair tables were built for
   int sym_world = -1;           // ... and the number of ranks
