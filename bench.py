@@ -249,10 +249,18 @@ def main():
     rpy_avg_ms = rpy_ms / max(rpy_n, 1)
     flops_launch = FLOPS_PER_PAIR * rows_here * (n - 1)
     achieved = flops_launch / (rpy_avg_ms / 1e3) / 1e12
+    kern = "rpy_sym_kernel" if n >= 4096 else "rpy_partial_kernel"
+    prof = ncu_profile_summary(kern)
     roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                "kernel": "rpy_partial_kernel", "avg_launch_ms": rpy_avg_ms, "launches_timed": rpy_n,
-                "peak_note": "FP64 derived: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (measured DFMA microbench 34.24)"}
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": prof.get("traffic_bytes"),
+                "kernel": kern, "avg_launch_ms": rpy_avg_ms, "launches_timed": rpy_n,
+                "algorithmic_flops_per_pair": FLOPS_PER_PAIR,
+                "hw_fp64_instr_per_ordered_pair": 18 if kern == "rpy_sym_kernel" else 26,
+                "ncu_fp64_pipe_active_pct": prof.get("fp64_pipe_pct"), "ncu_profile": prof.get("file"),
+                "peak_note": "FP64 derived from unit counts: 148 SM x 64 FP64 lanes x 2 flop x 1.965 GHz "
+                             "(DFMA microbenchmark on this pool: 34.24 TFLOP/s); the symmetric kernel evaluates "
+                             "each unordered pair once, so 37 algorithmic flops per ordered pair cost 18 FP64 "
+                             "instructions"}
     share = {k: v[0] / max(ms_total, 1e-9) for k, v in tim.items()}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
@@ -287,6 +295,35 @@ def main():
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def ncu_profile_summary(kernel):
+    """dram bytes per launch and FP64-pipe utilisation of `kernel` from the committed ncu
+    summaries (profiles/*/*_ncu.txt, written by tools/summarize_ncu.py from --set full captures)."""
+    import glob
+    best = {}
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "*_ncu.txt"))):
+        cur = None
+        vals = {}
+        for line in open(f):
+            if line.startswith("== "):
+                cur = line
+                continue
+            if cur is None or kernel not in cur:
+                continue
+            parts = line.split()
+            if len(parts) >= 2:
+                vals[parts[0]] = (parts[1], parts[2] if len(parts) > 2 else "")
+        if vals:
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            tb = 0.0
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                if k in vals:
+                    tb += float(vals[k][0]) * scale.get(vals[k][1], 1)
+            best = {"file": os.path.relpath(f, ROOT), "traffic_bytes": tb or None}
+            if "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active" in vals:
+                best["fp64_pipe_pct"] = float(vals["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"][0])
+    return best
 
 
 def ctx_rows(n, world, rank):
