@@ -617,7 +617,7 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
 #define SC_ATTR(P, NW, TPT, MINB) \
   cudaFuncSetAttribute(rpy_sym_kernel<P, NW, TPT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem)
     SC_ATTR(false, 4, 4, 3); SC_ATTR(true, 4, 4, 3); SC_ATTR(false, 8, 2, 2); SC_ATTR(true, 8, 2, 2);
-    SC_ATTR(false, 4, 4, 4); SC_ATTR(true, 4, 4, 4); SC_ATTR(false, 16, 1, 1); SC_ATTR(true, 16, 1, 1);
+    SC_ATTR(false, 16, 1, 1); SC_ATTR(true, 16, 1, 1);
 #undef SC_ATTR
     attr_set = true;
   }
@@ -632,7 +632,6 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
                                                                          ctx->rpy_part.p, done)
     switch (ctx->sym_variant) {
       case 1: if (ctx->poly) SC_SYM(true, 8, 2, 2); else SC_SYM(false, 8, 2, 2); break;
-      case 2: if (ctx->poly) SC_SYM(true, 4, 4, 4); else SC_SYM(false, 4, 4, 4); break;
       case 3: if (ctx->poly) SC_SYM(true, 16, 1, 1); else SC_SYM(false, 16, 1, 1); break;
       default: if (ctx->poly) SC_SYM(true, 4, 4, 3); else SC_SYM(false, 4, 4, 3); break;
     }
