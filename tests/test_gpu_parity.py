@@ -288,3 +288,49 @@ def test_c5_bench_configuration_certificate(ctx):
         i, j = ct.i[l], ct.j[l]
         go = float(np.dot(ct.normal[l], Uo[i][:3] - Uo[j][:3])) + ct.gap[l] / p.dt
         assert abs(g[l] - go) <= 1e-9 * (1 + abs(go)) + 1e-9, (l, g[l], go)
+
+
+# ---------------------------------------------------------------- full BASELINE sizes
+def test_c4_full_size_contacts_and_converged_solve(ctx):
+    """C4 at full size (200,000 rods): contacts bit-exact and the converged BBPGD against the
+    oracle's converged solve (drag mobility is O(N), so the oracle finishes in seconds)."""
+    p = make_problem("C4")
+    r = _gpu_solve(ctx, p)
+    c = ctx.get_contacts(lever=True)
+    o = oracle.solve_problem(p)
+    _assert_contacts_equal(c, o["system"].ct)
+    assert r["status"] == 0 and r["residual"] < 1e-8 and o["residual"] < 1e-8
+    assert _relL2(_np(r["gamma"]), o["gamma"]) <= 1e-6
+    assert _relL2(_np(r["Fc"]), o["Fc"]) <= 1e-6
+    assert _relL2(_np(r["Uc"]), o["Uc"]) <= 1e-6
+
+
+def test_c2_full_size_converged_solve(ctx):
+    """C2 at full size (8,192 polydisperse spheres): converged gamma and D gamma vs the oracle."""
+    p = make_problem("C2")
+    r = _gpu_solve(ctx, p)
+    o = oracle.solve_problem(p)
+    assert r["status"] == 0 and r["residual"] < 1e-8 and o["residual"] < 1e-8
+    assert _relL2(_np(r["gamma"]), o["gamma"]) <= 1e-6
+    assert _relL2(_np(r["Fc"]), o["Fc"]) <= 1e-6
+
+
+def test_c3_full_size_converged_certificate(ctx):
+    """C3 at full size, converged: the GPU's gamma certified by the oracle's RPY rows on sampled
+    constraints (g_l = n.(U_i - U_j) + q_l with U = RPY(F_ext + D gamma)); complementarity holds."""
+    p = make_problem("C3")
+    r = _gpu_solve(ctx, p)
+    assert r["status"] == 0 and r["converged"] == 1 and r["residual"] < 1e-8
+    gam = _np(r["gamma"])
+    ct = oracle.contacts_spheres(p.pos, p.radius, p.gap_abs, p.gap_rel)
+    F = oracle.apply_D(p.n, ct, gam) + p.force
+    rng = np.random.default_rng(8)
+    ls = rng.choice(ct.nc, 24, replace=False)
+    g = _np(r["g"])
+    for l in ls:
+        i, j = ct.i[l], ct.j[l]
+        ui = oracle.rpy_apply_rows(p.pos, p.radius, p.mu, F, i, i + 1)[0]
+        uj = oracle.rpy_apply_rows(p.pos, p.radius, p.mu, F, j, j + 1)[0]
+        go = float(np.dot(ct.normal[l], ui[:3] - uj[:3])) + ct.gap[l] / p.dt
+        assert abs(g[l] - go) <= 1e-8 * (1 + abs(go)), (l, g[l], go)
+        assert min(gam[l], go) > -1e-8 and (gam[l] == 0 or abs(go) < 1e-7 * (1 + gam[l]))
