@@ -164,6 +164,20 @@ typedef struct {
 int sc_collision_step(sc_ctx* ctx, const sc_problem* prob, const sc_bbpgd_opts* opts,
                       double* Fc_out, double* Uc_out, int64_t* n_c, sc_bbpgd_stats* stats);
 
+/* --------------------------------------------- NEXT row f1: one time step */
+/* The four steps of P:L480-L489: U_nc = Mobility(F_ext), contacts + D, the LCP
+ * (BBPGD) -> U_c, and the explicit Euler update of the configuration
+ * (P:L465-L470):
+ *   c' = c + dt (U_nc + U_c),
+ *   theta' = normalize(theta + dt Psi(theta) Omega), Psi = 1/2 [-p^T ; s I - [p]x],
+ *   rods: t' = normalize(t + dt Omega x t).
+ * pos_out: n x 3 (required); dir_out: n x 3 (rods, required for rods);
+ * quat: n x 4 quaternions (s, px, py, pz) updated in place (may be NULL);
+ * U_out: n x 6 total velocity U_nc + U_c (may be NULL).  Returns like
+ * sc_bbpgd_solve (SC_NOT_CONVERGED still updates the configuration). */
+int sc_time_step(sc_ctx* ctx, const sc_problem* prob, const sc_bbpgd_opts* opts, double* pos_out, double* dir_out,
+                 double* quat, double* U_out, int64_t* n_c, sc_bbpgd_stats* stats);
+
 /* ----------------------------------------------------------- measurement */
 /* Kernel families for timing/launch accounting. */
 enum {

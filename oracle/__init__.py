@@ -91,6 +91,7 @@ def _declare(L):
     L.orc_bbpgd_dense.argtypes = [i64, vp, vp, d, i32, i32, vp, vp, C.POINTER(Stats)]
     L.orc_minmap_residual.restype = d
     L.orc_minmap_residual.argtypes = [i64, vp, vp]
+    L.orc_euler_update.argtypes = [i64, d, vp, vp, vp, vp]
 
 
 def _p(a):
@@ -260,6 +261,26 @@ def bbpgd_dense(M, q, tol=1e-8, max_iter=5000, bb_mode=0):
 def minmap_residual(gamma, g):
     gamma, g = _f64(gamma), _f64(g)
     return float(lib().orc_minmap_residual(gamma.shape[0], _p(gamma), _p(g)))
+
+
+def euler_update(dt, UW, pos, quat=None, direction=None):
+    """Step 4: returns updated copies (pos, quat, direction)."""
+    UW = _f64(UW)
+    pos = _f64(pos).copy()
+    quat = None if quat is None else _f64(quat).copy()
+    direction = None if direction is None else _f64(direction).copy()
+    _check(lib().orc_euler_update(pos.shape[0], dt, _p(UW), _p(pos), _p(quat), _p(direction)), "euler_update")
+    return pos, quat, direction
+
+
+def time_step(problem, quat=None, max_iter=None):
+    """The four steps of P:L480-L489 on the CPU: U_nc, contacts + D, LCP, Euler update."""
+    res = solve_problem(problem, max_iter=max_iter, fixed_iters=0)
+    U = res["U_ext"] + res["Uc"]
+    pos, quat, direction = euler_update(problem.dt, U, problem.pos, quat,
+                                        problem.direction if problem.kind == "rods" else None)
+    res.update(pos=pos, quat=quat, direction=direction, U=U)
+    return res
 
 
 # ------------------------------------------------------ one-call pipeline

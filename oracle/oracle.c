@@ -670,3 +670,42 @@ int orc_bbpgd_dense(int64_t n, const double* M, const double* q, double tol, int
   dense_ctx d = {n, M};
   return bbpgd_core(n, dense_mv, &d, q, tol, max_iter, bb_mode, 0, gamma, g_out, st);
 }
+
+/* ------------------------------------------------------------------------ */
+/* Step 4 of the time step: C^{k+1} = C^k + G U dt (Eq. time-step,  */
+/* P:L468) with the quaternion kinematics theta' = Psi(theta) Omega          */
+/* and renormalisation of the quaternion.                     */
+/* ------------------------------------------------------------------------ */
+int orc_euler_update(int64_t n, double dt, const double* UW, double* pos, double* quat, double* dir) {
+  if (n < 0 || !(dt > 0)) return -1;
+  for (int64_t i = 0; i < n; ++i) {
+    const double* U = UW + 6 * i;
+    const double* W = U + 3;
+    for (int k = 0; k < 3; ++k) pos[3 * i + k] = pos[3 * i + k] + dt * U[k];
+    if (quat) {
+      double* th = quat + 4 * i;
+      double s = th[0], px = th[1], py = th[2], pz = th[3];
+      /* Psi Omega = 1/2 [ -p.W ; s W - p x W ] */
+      double ds = -0.5 * (px * W[0] + py * W[1] + pz * W[2]);
+      double cx = py * W[2] - pz * W[1];
+      double cy = pz * W[0] - px * W[2];
+      double cz = px * W[1] - py * W[0];
+      double dx = 0.5 * (s * W[0] - cx);
+      double dy = 0.5 * (s * W[1] - cy);
+      double dz = 0.5 * (s * W[2] - cz);
+      s += dt * ds; px += dt * dx; py += dt * dy; pz += dt * dz;
+      double nn = sqrt(s * s + px * px + py * py + pz * pz);
+      th[0] = s / nn; th[1] = px / nn; th[2] = py / nn; th[3] = pz / nn;
+    }
+    if (dir) {
+      double* t = dir + 3 * i;
+      double wx = W[1] * t[2] - W[2] * t[1];
+      double wy = W[2] * t[0] - W[0] * t[2];
+      double wz = W[0] * t[1] - W[1] * t[0];
+      double ax = t[0] + dt * wx, ay = t[1] + dt * wy, az = t[2] + dt * wz;
+      double nn = sqrt(ax * ax + ay * ay + az * az);
+      t[0] = ax / nn; t[1] = ay / nn; t[2] = az / nn;
+    }
+  }
+  return 0;
+}

@@ -103,6 +103,13 @@ int orc_bbpgd_dense(int64_t n, const double* M, const double* q, double tol, int
 /* phi = || min(gamma, g) ||_2. */
 double orc_minmap_residual(int64_t n, const double* gamma, const double* g);
 
+/* Explicit Euler update of the configuration, step 4 of the
+ * four-step procedure: c' = c + dt U, theta' = normalize(theta + dt Psi(theta) Omega)
+ * with Psi = 1/2 [-p^T ; s I - [p]x] for theta = (s, p); rod axes t' = normalize(t + dt Omega x t).
+ * UW: n x 6 total velocity (U_nc + U_c).  quat (n x 4, (s, px, py, pz)) and dir (n x 3) may be
+ * NULL; updated in place. */
+int orc_euler_update(int64_t n, double dt, const double* UW, double* pos, double* quat, double* dir);
+
 #ifdef __cplusplus
 }
 #endif

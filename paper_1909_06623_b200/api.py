@@ -199,6 +199,26 @@ class Context:
         self.n, self.nc, self.kind = n, nc.value, kind
         return {"status": rc, "nc": nc.value, **st.as_dict()}
 
+    def time_step(self, kind, pos, F_ext, radius=None, direction=None, length=None, b=0.5, gap_abs=0.0,
+                  gap_rel=0.1, mu=1.0, dt=0.01, tol=1e-8, max_iter=5000, bb_mode=0, quat=None, want_U=True):
+        """One whole time step: returns the next centres (and rod axes),
+        updates `quat` (n x 4) in place, and the total velocity U_nc + U_c."""
+        n = int(pos.shape[0])
+        prob = _lib.Problem(0 if kind == "spheres" else 1, 0, n, _ptr(pos), _ptr(radius), _ptr(direction),
+                            _ptr(length), float(b), float(gap_abs), float(gap_rel), float(mu), float(dt),
+                            _ptr(F_ext))
+        opts = _lib.BbpgdOpts(float(mu), float(tol), int(max_iter), int(bb_mode), 0, 0)
+        pos_out = self._dev((n, 3))
+        dir_out = self._dev((n, 3)) if kind == "rods" else None
+        U = self._dev((n, 6)) if want_U else None
+        nc = C.c_int64()
+        st = _lib.BbpgdStats()
+        rc = self._rc(self.lib.sc_time_step(self._h, C.byref(prob), C.byref(opts), _ptr(pos_out), _ptr(dir_out),
+                                            _ptr(_check_dtype(quat, "f64")), _ptr(U), C.byref(nc), C.byref(st)),
+                      allow=(0, 1))
+        self.n, self.nc, self.kind = n, nc.value, kind
+        return {"pos": pos_out, "dir": dir_out, "U": U, "status": rc, "nc": nc.value, **st.as_dict()}
+
     # ------------------------------------------------------------- measurement
     def set_timing(self, enable=True):
         self._rc(self.lib.sc_set_timing(self._h, int(bool(enable))))

@@ -466,7 +466,7 @@ void sc_destroy(sc_ctx* ctx) {
   release(ctx->ci); release(ctx->cj); release(ctx->nrm4); release(ctx->lev4); release(ctx->rxn4);
   release(ctx->row_ptr); release(ctx->inc); release(ctx->icol4); release(ctx->first_ptr); release(ctx->near_ptr); release(ctx->near_idx);
   release(ctx->q); release(ctx->gam[0]); release(ctx->gam[1]); release(ctx->g[0]); release(ctx->g[1]);
-  release(ctx->w); release(ctx->gam_user); release(ctx->chunk_part); release(ctx->chunk_red);
+  release(ctx->w); release(ctx->gam_user); release(ctx->uc); release(ctx->chunk_part); release(ctx->chunk_red);
   release(ctx->sym_pairs); release(ctx->upart); release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);
   release(ctx->bbox_part); release(ctx->cell_of); release(ctx->cell_cnt); release(ctx->cell_start);
   release(ctx->sorted_idx); release(ctx->pair_cnt); release(ctx->pair_off); release(ctx->scan_tmp);
@@ -955,6 +955,82 @@ int sc_collision_step(sc_ctx* ctx, const sc_problem* prob, const sc_bbpgd_opts* 
   o.warm_start = 0;
   rc = sc_bbpgd_solve(ctx, &o, ctx->gam_user.p, nullptr, Fc_out, Uc_out, stats);
   if (n_c) *n_c = nc;
+  return rc;
+}
+
+// Step 4: C^{k+1} = C^k + G U dt, quaternion kinematics theta' = Psi Omega
+// with renormalisation; rod axes t' = normalize(t + dt Omega x t).
+// Same association as the plain definition (explicit round-to-nearest).
+__global__ static void euler_update_kernel(const double4* __restrict__ pos4, const double4* __restrict__ dir4,
+                                          const double* __restrict__ Unc, const double* __restrict__ Uc,
+                                          int64_t n, double dt, double* __restrict__ pos_out,
+                                          double* __restrict__ dir_out, double* __restrict__ quat,
+                                          double* __restrict__ U_out) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  double U[6];
+  for (int k = 0; k < 6; ++k) U[k] = __dadd_rn(Unc[6 * b + k], Uc[6 * b + k]);
+  if (U_out)
+    for (int k = 0; k < 6; ++k) U_out[6 * b + k] = U[k];
+  const double4 c = pos4[b];
+  pos_out[3 * b + 0] = __dadd_rn(c.x, __dmul_rn(dt, U[0]));
+  pos_out[3 * b + 1] = __dadd_rn(c.y, __dmul_rn(dt, U[1]));
+  pos_out[3 * b + 2] = __dadd_rn(c.z, __dmul_rn(dt, U[2]));
+  const double* W = U + 3;
+  if (quat) {
+    double* th = quat + 4 * b;
+    double s = th[0], px = th[1], py = th[2], pz = th[3];
+    // Psi(theta) Omega = 1/2 [ -p.Omega ; s Omega - p x Omega ]
+    const double ds = -0.5 * (px * W[0] + py * W[1] + pz * W[2]);
+    const double cx = py * W[2] - pz * W[1], cy = pz * W[0] - px * W[2], cz = px * W[1] - py * W[0];
+    const double dx = 0.5 * (s * W[0] - cx), dy = 0.5 * (s * W[1] - cy), dz = 0.5 * (s * W[2] - cz);
+    s += dt * ds;
+    px += dt * dx;
+    py += dt * dy;
+    pz += dt * dz;
+    const double nn = sqrt(s * s + px * px + py * py + pz * pz);
+    th[0] = s / nn;
+    th[1] = px / nn;
+    th[2] = py / nn;
+    th[3] = pz / nn;
+  }
+  if (dir_out) {
+    const double4 t = dir4[b];
+    const double wx = W[1] * t.z - W[2] * t.y, wy = W[2] * t.x - W[0] * t.z, wz = W[0] * t.y - W[1] * t.x;
+    const double ax = t.x + dt * wx, ay = t.y + dt * wy, az = t.z + dt * wz;
+    const double nn = sqrt(ax * ax + ay * ay + az * az);
+    dir_out[3 * b + 0] = ax / nn;
+    dir_out[3 * b + 1] = ay / nn;
+    dir_out[3 * b + 2] = az / nn;
+  }
+}
+
+int sc_time_step(sc_ctx* ctx, const sc_problem* prob, const sc_bbpgd_opts* opts, double* pos_out, double* dir_out,
+                 double* quat, double* U_out, int64_t* n_c, sc_bbpgd_stats* stats) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (prob == nullptr || (prob->n > 0 && pos_out == nullptr) || (prob->kind == 1 && prob->n > 0 && !dir_out))
+    return fail(ctx, SC_EINVAL, "time_step: bad arguments");
+  const int64_t n = prob->n;
+  if (int rc = ensure(ctx, ctx->uc, 6 * std::max<int64_t>(n, 1))) return rc;
+  int rc = sc_collision_step(ctx, prob, opts, nullptr, ctx->uc.p, n_c, stats);  // steps 1-3
+  if (rc < 0) return rc;
+  if (n == 0) return rc;
+  cudaSetDevice(ctx->device);
+  Stager st(ctx);
+  double *dpos = nullptr, *ddir = nullptr, *dq = nullptr, *dU = nullptr;
+  if (int e = st.out(pos_out, 3 * n, &dpos)) return e;
+  if (prob->kind == 1) {
+    if (int e = st.out(dir_out, 3 * n, &ddir)) return e;
+  }
+  if (int e = st.inout(quat, 4 * n, &dq)) return e;
+  if (int e = st.out(U_out, 6 * n, &dU)) return e;
+  timer_begin(ctx, SC_K_MISC);
+  euler_update_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(
+      ctx->pos4.p, ctx->dir4.p, ctx->w.p, ctx->uc.p, n, prob->dt, dpos, ddir, dq, dU);
+  timer_end(ctx, SC_K_MISC);
+  if (int e = check_launch(ctx, "euler_update")) return e;
+  if (int e = st.finish()) return e;
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
   return rc;
 }
 

@@ -100,7 +100,7 @@ struct sc_ctx {
   // LCP state
   bool have_q = false;
   sc::DBuf<double> q;
-  sc::DBuf<double> gam[2], g[2], w, gam_user;
+  sc::DBuf<double> gam[2], g[2], w, gam_user, uc;  // w: U_ext (n x 6); uc: U_c for time stepping
   sc::DBuf<double> chunk_part;  // nchunks * 4
   sc::DBuf<double> chunk_red;   // reduced (allreduce output)
   sc::DBuf<double4> f4;         // sources: (Fx,Fy,Fz,0) [npad]

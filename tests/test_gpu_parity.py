@@ -334,3 +334,37 @@ def test_c3_full_size_converged_certificate(ctx):
         go = float(np.dot(ct.normal[l], ui[:3] - uj[:3])) + ct.gap[l] / p.dt
         assert abs(g[l] - go) <= 1e-8 * (1 + abs(go)), (l, g[l], go)
         assert min(gam[l], go) > -1e-8 and (gam[l] == 0 or abs(go) < 1e-7 * (1 + gam[l]))
+
+
+# ---------------------------------------------------------------- NEXT row f1: time stepping
+@pytest.mark.parametrize("name,n,steps", [("C1", None, 3), ("C2", 1500, 2), ("C4", 8000, 2)])
+def test_time_steps_vs_oracle(ctx, name, n, steps):
+    """Several whole time steps (U_nc, contacts, LCP, Euler update) on the GPU vs the oracle:
+    the configurations stay within the LCP tolerance of each other."""
+    p = make_problem(name, n=n, fixed_iters=0)
+    po = make_problem(name, n=n, fixed_iters=0)
+    quat = np.tile([1.0, 0.0, 0.0, 0.0], (p.n, 1))
+    qg = _cuda(quat)
+    qo = quat.copy()
+    pos_g = _cuda(p.pos)
+    dir_g = _cuda(p.direction) if p.kind == "rods" else None
+    for _ in range(steps):
+        r = ctx.time_step(p.kind, pos_g, _cuda(p.force), radius=_cuda(p.radius) if p.radius is not None else None,
+                          direction=dir_g, length=_cuda(p.length) if p.length is not None else None,
+                          b=p.rod_radius, gap_abs=p.gap_abs, gap_rel=p.gap_rel, mu=p.mu, dt=p.dt, tol=p.tol,
+                          max_iter=p.max_iter, quat=qg)
+        assert r["status"] == 0 and r["residual"] < 1e-8
+        pos_g = r["pos"]
+        dir_g = r["dir"] if p.kind == "rods" else None
+        o = oracle.time_step(po, quat=qo)
+        po.pos = o["pos"]
+        qo = o["quat"]
+        if p.kind == "rods":
+            po.direction = o["direction"]
+    scale = np.abs(o["U"]).max() * p.dt
+    np.testing.assert_allclose(_np(pos_g), po.pos, rtol=0, atol=1e-7 * scale + 1e-13)
+    np.testing.assert_allclose(_np(qg), qo, rtol=0, atol=1e-9)
+    if p.kind == "rods":
+        np.testing.assert_allclose(_np(dir_g), po.direction, rtol=0, atol=1e-9)
+        np.testing.assert_allclose(np.linalg.norm(_np(dir_g), axis=1), 1.0, atol=1e-14)
+    np.testing.assert_allclose(np.linalg.norm(_np(qg), axis=1), 1.0, atol=1e-14)
