@@ -21,12 +21,18 @@ namespace sc {
 namespace {
 
 constexpr int kT = 256;
+constexpr int kR = 256;  // threads of the reduction kernels (D^T per chunk, finalize); 512 measured slower
 inline unsigned nblk(int64_t n) { return static_cast<unsigned>((n + kT - 1) / kT); }
 
 enum GatherMode { kProj = 0, kRaw = 1 };
+constexpr int kLpbS = 2;  // lanes per body in the D-gather: spheres (~2.7 incidences per body)
+constexpr int kLpbR = 4;  // rods (~4.5 incidences per body)
 enum GatherOut { kOutF4 = 0, kOutRodU = 1, kOutFT = 2 };
 
-template <int KIND, int MODE, int OUT>
+// LPB lanes cooperate on one body (incidences e0+k, e0+k+LPB, ...), then an xor-butterfly
+// combines them (every lane ends with the same bits: a+b == b+a) -- more loads in flight
+// than one serial chain per body.
+template <int KIND, int MODE, int OUT, int LPB>
 __global__ void __launch_bounds__(kT) gather_kernel(
     const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ inc, const double4* __restrict__ icol4,
     const double4* __restrict__ nrm4, const double4* __restrict__ rxn4, const double* __restrict__ a,
@@ -35,21 +41,15 @@ __global__ void __launch_bounds__(kT) gather_kernel(
     const double4* __restrict__ dir4, const double4* __restrict__ mob4, double4* __restrict__ out4,
     double* __restrict__ outFT, const int32_t* __restrict__ done) {
   if (done != nullptr && *done) return;
-  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (b >= nout) return;
-  if (b >= n) {  // padded source rows: zero force
-    if (OUT == kOutF4) out4[b] = make_double4(0, 0, 0, 0);
-    if (OUT == kOutRodU) {
-      out4[2 * b] = make_double4(0, 0, 0, 0);
-      out4[2 * b + 1] = make_double4(0, 0, 0, 0);
-    }
-    return;
-  }
+  const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t b = gt / LPB;
+  const int k = static_cast<int>(gt % LPB);
+  const bool real = b < n;
   const double alpha = MODE == kProj ? dsc->alpha : 0.0;
   double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
-  const int32_t e0 = row_ptr[b], e1 = row_ptr[b + 1];
-#pragma unroll 4
-  for (int32_t e = e0; e < e1; ++e) {
+  const int32_t e0 = real ? row_ptr[b] : 0, e1 = real ? row_ptr[b + 1] : 0;
+#pragma unroll 2
+  for (int32_t e = e0 + k; e < e1; e += LPB) {
     const int32_t v = inc[e];
     const int32_t l = v >> 1;
     const int side = v & 1;
@@ -80,6 +80,26 @@ __global__ void __launch_bounds__(kT) gather_kernel(
       tz = fma(sgm, rx.z, tz);
     }
   }
+#pragma unroll
+  for (int o = LPB / 2; o >= 1; o >>= 1) {
+    fx += __shfl_xor_sync(0xffffffffu, fx, o);
+    fy += __shfl_xor_sync(0xffffffffu, fy, o);
+    fz += __shfl_xor_sync(0xffffffffu, fz, o);
+    if (KIND == kRods) {
+      tx += __shfl_xor_sync(0xffffffffu, tx, o);
+      ty += __shfl_xor_sync(0xffffffffu, ty, o);
+      tz += __shfl_xor_sync(0xffffffffu, tz, o);
+    }
+  }
+  if (k != 0 || b >= nout) return;
+  if (!real) {  // padded source rows: zero force
+    if (OUT == kOutF4) out4[b] = make_double4(0, 0, 0, 0);
+    if (OUT == kOutRodU) {
+      out4[2 * b] = make_double4(0, 0, 0, 0);
+      out4[2 * b + 1] = make_double4(0, 0, 0, 0);
+    }
+    return;
+  }
   if (OUT == kOutF4) {
     out4[b] = make_double4(fx, fy, fz, 0.0);
   } else if (OUT == kOutFT) {
@@ -96,28 +116,28 @@ __global__ void __launch_bounds__(kT) gather_kernel(
   }
 }
 
-__device__ __forceinline__ void block_reduce4(double v[4], double* red /* [4][kT] smem */) {
+__device__ __forceinline__ void block_reduce4(double v[4], double* red /* [4][kR] smem */) {
   const int t = threadIdx.x;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) red[k * kT + t] = v[k];
+  for (int k = 0; k < 4; ++k) red[k * kR + t] = v[k];
   __syncthreads();
-  for (int w = kT / 2; w > 0; w >>= 1) {
+  for (int w = kR / 2; w > 0; w >>= 1) {
     if (t < w) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) red[k * kT + t] += red[k * kT + t + w];
+      for (int k = 0; k < 4; ++k) red[k * kR + t] += red[k * kR + t + w];
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int k = 0; k < 4; ++k) v[k] = red[k * kT];
+  for (int k = 0; k < 4; ++k) v[k] = red[k * kR];
 }
 
 // Sums chunk partials in fixed order (thread t: chunks t, t+256, ...; then a fixed tree)
 // and advances the BBPGD scalars.  mode 0: after Step 10 of iteration j; mode 1: alpha_0
-// (Step 6); mode 2: phi_0 (Step 3).  Called by one whole CTA of kT threads.
+// (Step 6); mode 2: phi_0 (Step 3).  Called by one whole CTA of kR threads.
 __device__ void finalize_block(const double* part, int64_t nchunks, int mode, DevScalars* s, double* red) {
   double p[4] = {0, 0, 0, 0};
-  for (int64_t c = threadIdx.x; c < nchunks; c += kT) {
+  for (int64_t c = threadIdx.x; c < nchunks; c += kR) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) p[k] += __ldcg(part + c * 4 + k);
   }
@@ -166,10 +186,10 @@ __device__ void finalize_block(const double* part, int64_t nchunks, int mode, De
   }
 }
 
-__global__ void __launch_bounds__(kT) finalize_kernel(const double* __restrict__ part, int64_t nchunks, int mode,
+__global__ void __launch_bounds__(kR) finalize_kernel(const double* __restrict__ part, int64_t nchunks, int mode,
                                                       DevScalars* __restrict__ s) {
   if (s->done) return;
-  __shared__ double red[4 * kT];
+  __shared__ double red[4 * kR];
   finalize_block(part, nchunks, mode, s, red);
 }
 
@@ -179,7 +199,7 @@ enum DtMode { kDtIter = 0, kDtAlpha0 = 1, kDtG0 = 2, kDtInitQ = 3 };
 // (threadfence + counter) also runs K-FINALIZE, saving a launch per iteration; the sums are
 // the same fixed-order sums as the separate finalize kernel.
 template <int KIND, int MODE, bool FUSE>
-__global__ void __launch_bounds__(kT) dt_kernel(
+__global__ void __launch_bounds__(kR) dt_kernel(
     const int32_t* __restrict__ first_ptr, int64_t n, int64_t c0, const int32_t* __restrict__ ci,
     const int32_t* __restrict__ cj, const double4* __restrict__ nrm4, const double4* __restrict__ rxn4,
     const double4* __restrict__ u4, const double* __restrict__ q, const double* __restrict__ gam_new,
@@ -187,14 +207,14 @@ __global__ void __launch_bounds__(kT) dt_kernel(
     double* __restrict__ part, const int32_t* __restrict__ done, int64_t nchunks, DevScalars* __restrict__ sc,
     unsigned int* __restrict__ counter) {
   if (done != nullptr && *done) return;
-  __shared__ double red[4 * kT];
+  __shared__ double red[4 * kR];
   const int64_t c = c0 + blockIdx.x;
   int64_t blo = c * kChunkBodies, bhi = blo + kChunkBodies;
   if (blo > n) blo = n;
   if (bhi > n) bhi = n;
   const int32_t l0 = first_ptr[blo], l1 = first_ptr[bhi];
   double p[4] = {0, 0, 0, 0};
-  for (int32_t l = l0 + threadIdx.x; l < l1; l += kT) {
+  for (int32_t l = l0 + threadIdx.x; l < l1; l += kR) {
     double v = 0.0;
     if (MODE != kDtInitQ) {
       const int32_t i = ci[l], j = cj[l];
@@ -355,11 +375,11 @@ int launch_gather_proj(sc_ctx* ctx, const double* gam_old, const double* g_old, 
   const int32_t* done = &ctx->dsc->done;
   timer_begin(ctx, SC_K_GATHER);
   if (ctx->kind == kSpheres)
-    gather_kernel<kSpheres, kProj, kOutF4><<<nblk(ctx->npad), kT, 0, ctx->stream>>>(
+    gather_kernel<kSpheres, kProj, kOutF4, kLpbS><<<nblk(ctx->npad * kLpbS), kT, 0, ctx->stream>>>(
         ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, gam_old, g_old, gam_new, ctx->dsc, ctx->n, ctx->npad,
         nullptr, nullptr, ctx->f4.p, nullptr, done);
   else
-    gather_kernel<kRods, kProj, kOutRodU><<<nblk(ctx->npad), kT, 0, ctx->stream>>>(
+    gather_kernel<kRods, kProj, kOutRodU, kLpbR><<<nblk(ctx->npad * kLpbR), kT, 0, ctx->stream>>>(
         ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, gam_old, g_old, gam_new, ctx->dsc, ctx->n,
         ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done);
   timer_end(ctx, SC_K_GATHER);
@@ -371,21 +391,21 @@ int launch_gather_raw(sc_ctx* ctx, const double* v, double mu, double* FT_user) 
   timer_begin(ctx, SC_K_GATHER);
   if (FT_user != nullptr) {
     if (ctx->kind == kSpheres)
-      gather_kernel<kSpheres, kRaw, kOutFT><<<nblk(ctx->n), kT, 0, ctx->stream>>>(
+      gather_kernel<kSpheres, kRaw, kOutFT, kLpbS><<<nblk(ctx->n * kLpbS), kT, 0, ctx->stream>>>(
           ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n, ctx->n,
           nullptr, nullptr, nullptr, FT_user, nullptr);
     else
-      gather_kernel<kRods, kRaw, kOutFT><<<nblk(ctx->n), kT, 0, ctx->stream>>>(
+      gather_kernel<kRods, kRaw, kOutFT, kLpbR><<<nblk(ctx->n * kLpbR), kT, 0, ctx->stream>>>(
           ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n, ctx->n,
           nullptr, nullptr, nullptr, FT_user, nullptr);
   } else {
     const int32_t* done = &ctx->dsc->done;
     if (ctx->kind == kSpheres)
-      gather_kernel<kSpheres, kRaw, kOutF4><<<nblk(ctx->npad), kT, 0, ctx->stream>>>(
+      gather_kernel<kSpheres, kRaw, kOutF4, kLpbS><<<nblk(ctx->npad * kLpbS), kT, 0, ctx->stream>>>(
           ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n, ctx->npad,
           nullptr, nullptr, ctx->f4.p, nullptr, done);
     else
-      gather_kernel<kRods, kRaw, kOutRodU><<<nblk(ctx->npad), kT, 0, ctx->stream>>>(
+      gather_kernel<kRods, kRaw, kOutRodU, kLpbR><<<nblk(ctx->npad * kLpbR), kT, 0, ctx->stream>>>(
           ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n,
           ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done);
   }
@@ -414,11 +434,11 @@ int launch_dt(sc_ctx* ctx, int mode, const double* gam_new, const double* gam_ol
 #define SC_DT(KIND, MODE)                                                                                       \
   do {                                                                                                          \
     if (fuse)                                                                                                   \
-      dt_kernel<KIND, MODE, true><<<grid, kT, 0, ctx->stream>>>(                                                \
+      dt_kernel<KIND, MODE, true><<<grid, kR, 0, ctx->stream>>>(                                                \
           ctx->first_ptr.p, ctx->n, c0, ctx->ci.p, ctx->cj.p, ctx->nrm4.p, ctx->rxn4.p, u4, q, gam_new, gam_old, \
           g_old, g_out, part, done, ctx->nchunks, ctx->dsc, ctx->dcount);                                       \
     else                                                                                                        \
-      dt_kernel<KIND, MODE, false><<<grid, kT, 0, ctx->stream>>>(                                               \
+      dt_kernel<KIND, MODE, false><<<grid, kR, 0, ctx->stream>>>(                                               \
           ctx->first_ptr.p, ctx->n, c0, ctx->ci.p, ctx->cj.p, ctx->nrm4.p, ctx->rxn4.p, u4, q, gam_new, gam_old, \
           g_old, g_out, part, done, ctx->nchunks, ctx->dsc, ctx->dcount);                                       \
   } while (0)
@@ -445,7 +465,7 @@ int launch_dt(sc_ctx* ctx, int mode, const double* gam_new, const double* gam_ol
 
 int launch_finalize(sc_ctx* ctx, int mode, const double* part) {
   timer_begin(ctx, SC_K_FINALIZE);
-  finalize_kernel<<<1, kT, 0, ctx->stream>>>(part, ctx->nchunks, mode, ctx->dsc);
+  finalize_kernel<<<1, kR, 0, ctx->stream>>>(part, ctx->nchunks, mode, ctx->dsc);
   timer_end(ctx, SC_K_FINALIZE);
   return check_launch(ctx, "finalize");
 }
