@@ -121,7 +121,10 @@ typedef struct {
   int32_t max_iter;     /* j_max */
   int32_t bb_mode;      /* 0 = BB1 (paper default), 1 = BB2, 2 = alternate */
   int32_t fixed_iters;  /* 1: run exactly max_iter iterations, no early exit (reading A22) */
-  int32_t warm_start;   /* 1: gamma holds gamma_0 on entry; 0: gamma_0 = 0 (reading A3) */
+  int32_t warm_start;   /* 0: gamma_0 = 0 (reading A3); 1: gamma holds gamma_0 on entry;
+                           2: gamma_0 = the previous solve's gamma of the same body pair (i, j),
+                              0 for new pairs -- the warm start of a time-stepping run (Step 1,
+                              P:L586); needs the same body count, else falls back to 0 */
 } sc_bbpgd_opts;
 
 typedef struct {

@@ -273,9 +273,18 @@ def euler_update(dt, UW, pos, quat=None, direction=None):
     return pos, quat, direction
 
 
-def time_step(problem, quat=None, max_iter=None):
-    """The four steps of P:L480-L489 on the CPU: U_nc, contacts + D, LCP, Euler update."""
-    res = solve_problem(problem, max_iter=max_iter, fixed_iters=0)
+def warm_gamma(prev_ct, prev_gamma, ct):
+    """gamma_0 for a new constraint list: the previous gamma of the same pair (i, j), else 0."""
+    if prev_ct is None:
+        return None
+    prev = {(int(i), int(j)): g for i, j, g in zip(prev_ct.i, prev_ct.j, prev_gamma)}
+    return np.array([prev.get((int(i), int(j)), 0.0) for i, j in zip(ct.i, ct.j)])
+
+
+def time_step(problem, quat=None, max_iter=None, warm=None):
+    """The four steps of P:L480-L489 on the CPU: U_nc, contacts + D, LCP, Euler update.
+    warm = (prev contacts, prev gamma): Step 1's gamma_0 from the previous step's gamma."""
+    res = solve_problem(problem, max_iter=max_iter, fixed_iters=0, warm=warm)
     U = res["U_ext"] + res["Uc"]
     pos, quat, direction = euler_update(problem.dt, U, problem.pos, quat,
                                         problem.direction if problem.kind == "rods" else None)
@@ -294,13 +303,14 @@ def system_for(problem, method="grid"):
                   length=problem.length, b=problem.rod_radius)
 
 
-def solve_problem(problem, max_iter=None, fixed_iters=None, bb_mode=0):
+def solve_problem(problem, max_iter=None, fixed_iters=None, bb_mode=0, warm=None):
     """The whole per-step path on the CPU: contacts, D, U_ext, q, BBPGD."""
     sysm = system_for(problem)
     U_ext = sysm.mobility(problem.force)
     q = sysm.lcp_q(problem.dt, U_ext)
     fixed = problem.fixed_iters if fixed_iters is None else fixed_iters
     jmax = (fixed if fixed else problem.max_iter) if max_iter is None else max_iter
-    res = sysm.bbpgd(q, tol=problem.tol, max_iter=jmax, bb_mode=bb_mode, fixed_iters=int(bool(fixed)))
+    g0 = warm_gamma(warm[0], warm[1], sysm.ct) if warm is not None else None
+    res = sysm.bbpgd(q, tol=problem.tol, max_iter=jmax, bb_mode=bb_mode, fixed_iters=int(bool(fixed)), gamma0=g0)
     res.update(system=sysm, q=q, U_ext=U_ext)
     return res

@@ -166,9 +166,9 @@ class Context:
         return out
 
     def bbpgd_solve(self, mu=1.0, tol=1e-8, max_iter=5000, bb_mode=0, fixed_iters=False, gamma0=None,
-                    want_g=True, want_Fc=True, want_Uc=True, out=None):
-        opts = _lib.BbpgdOpts(float(mu), float(tol), int(max_iter), int(bb_mode), int(bool(fixed_iters)),
-                              int(gamma0 is not None))
+                    want_g=True, want_Fc=True, want_Uc=True, out=None, warm_from_previous=False):
+        warm = 1 if gamma0 is not None else (2 if warm_from_previous else 0)
+        opts = _lib.BbpgdOpts(float(mu), float(tol), int(max_iter), int(bb_mode), int(bool(fixed_iters)), warm)
         out = out or {}
         gamma = out.get("gamma")
         if gamma is None:
@@ -200,14 +200,15 @@ class Context:
         return {"status": rc, "nc": nc.value, **st.as_dict()}
 
     def time_step(self, kind, pos, F_ext, radius=None, direction=None, length=None, b=0.5, gap_abs=0.0,
-                  gap_rel=0.1, mu=1.0, dt=0.01, tol=1e-8, max_iter=5000, bb_mode=0, quat=None, want_U=True):
+                  gap_rel=0.1, mu=1.0, dt=0.01, tol=1e-8, max_iter=5000, bb_mode=0, quat=None, want_U=True,
+                  warm_start=False):
         """One whole time step: returns the next centres (and rod axes),
         updates `quat` (n x 4) in place, and the total velocity U_nc + U_c."""
         n = int(pos.shape[0])
         prob = _lib.Problem(0 if kind == "spheres" else 1, 0, n, _ptr(pos), _ptr(radius), _ptr(direction),
                             _ptr(length), float(b), float(gap_abs), float(gap_rel), float(mu), float(dt),
                             _ptr(F_ext))
-        opts = _lib.BbpgdOpts(float(mu), float(tol), int(max_iter), int(bb_mode), 0, 0)
+        opts = _lib.BbpgdOpts(float(mu), float(tol), int(max_iter), int(bb_mode), 0, 2 if warm_start else 0)
         pos_out = self._dev((n, 3))
         dir_out = self._dev((n, 3)) if kind == "rods" else None
         U = self._dev((n, 6)) if want_U else None

@@ -378,6 +378,54 @@ static int ensure_rod_mob(sc_ctx* ctx, double mu) {
   return 0;
 }
 
+// ---------------------------------------------------------- warm start across solves
+__global__ static void pair_keys_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, int64_t nc,
+                                        int64_t n, const double* __restrict__ gam, int64_t* __restrict__ key,
+                                        double* __restrict__ gcopy) {
+  const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (l >= nc) return;
+  key[l] = static_cast<int64_t>(ci[l]) * n + cj[l];  // ascending: constraints are sorted by (i, j)
+  gcopy[l] = gam[l];
+}
+
+__global__ static void warm_match_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj,
+                                         int64_t nc, int64_t n, const int64_t* __restrict__ pkey,
+                                         const double* __restrict__ pgam, int64_t pnc, double* __restrict__ gam0) {
+  const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (l >= nc) return;
+  const int64_t k = static_cast<int64_t>(ci[l]) * n + cj[l];
+  int64_t lo = 0, hi = pnc;  // binary search in the previous (sorted) key list
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (pkey[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  gam0[l] = (lo < pnc && pkey[lo] == k) ? pgam[lo] : 0.0;
+}
+
+int save_for_warm_start(sc_ctx* ctx, const double* gam) {
+  const int64_t nc = ctx->nc;
+  if (int rc = ensure(ctx, ctx->prev_key, std::max<int64_t>(nc, 1))) return rc;
+  if (int rc = ensure(ctx, ctx->prev_gam, std::max<int64_t>(nc, 1))) return rc;
+  if (nc > 0) {
+    timer_begin(ctx, SC_K_MISC);
+    pair_keys_kernel<<<static_cast<unsigned>((nc + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->ci.p, ctx->cj.p, nc, ctx->n, gam, ctx->prev_key.p, ctx->prev_gam.p);
+    timer_end(ctx, SC_K_MISC);
+    if (int rc = check_launch(ctx, "pair_keys")) return rc;
+  }
+  ctx->prev_nc = nc;
+  ctx->prev_n = ctx->n;
+  return 0;
+}
+
+int launch_warm_match(sc_ctx* ctx, double* gam0) {
+  timer_begin(ctx, SC_K_MISC);
+  warm_match_kernel<<<static_cast<unsigned>((ctx->nc + 255) / 256), 256, 0, ctx->stream>>>(
+      ctx->ci.p, ctx->cj.p, ctx->nc, ctx->n, ctx->prev_key.p, ctx->prev_gam.p, ctx->prev_nc, gam0);
+  timer_end(ctx, SC_K_MISC);
+  return check_launch(ctx, "warm_match");
+}
+
 }  // namespace sc
 
 using namespace sc;
@@ -466,7 +514,7 @@ void sc_destroy(sc_ctx* ctx) {
   release(ctx->ci); release(ctx->cj); release(ctx->nrm4); release(ctx->lev4); release(ctx->rxn4);
   release(ctx->row_ptr); release(ctx->inc); release(ctx->icol4); release(ctx->first_ptr); release(ctx->near_ptr); release(ctx->near_idx);
   release(ctx->q); release(ctx->gam[0]); release(ctx->gam[1]); release(ctx->g[0]); release(ctx->g[1]);
-  release(ctx->w); release(ctx->gam_user); release(ctx->uc); release(ctx->chunk_part); release(ctx->chunk_red);
+  release(ctx->w); release(ctx->gam_user); release(ctx->uc); release(ctx->prev_key); release(ctx->prev_gam); release(ctx->chunk_part); release(ctx->chunk_red);
   release(ctx->sym_pairs); release(ctx->upart); release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);
   release(ctx->bbox_part); release(ctx->cell_of); release(ctx->cell_cnt); release(ctx->cell_start);
   release(ctx->sorted_idx); release(ctx->pair_cnt); release(ctx->pair_off); release(ctx->scan_tmp);
@@ -743,7 +791,7 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
   if (int rc = ensure_rod_mob(ctx, mu)) return rc;
   Stager st(ctx);
   double *dgam = nullptr, *dg = nullptr, *dF = nullptr, *dU = nullptr;
-  if (opts->warm_start) {
+  if (opts->warm_start == 1) {
     if (int rc = st.inout(gamma, nc, &dgam)) return rc;
   } else {
     if (int rc = st.out(gamma, nc, &dgam)) return rc;
@@ -791,8 +839,13 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
 
   // Steps 1-5: gamma_0, g_0 = M gamma_0 + q, phi_0
   double* gam0 = ctx->gam[0].p;
-  if (opts->warm_start) {
-    SC_CUDA(cudaMemcpyAsync(gam0, dgam, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  const bool from_prev = opts->warm_start == 2 && ctx->prev_nc > 0 && ctx->prev_n == n;
+  if (opts->warm_start == 1 || from_prev) {
+    if (from_prev) {  // gamma_0 of each (i, j) = the previous solve's gamma of the same pair, else 0
+      if (int rc = launch_warm_match(ctx, gam0)) return rc;
+    } else {
+      SC_CUDA(cudaMemcpyAsync(gam0, dgam, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
     // projection onto gamma >= 0 via the proj kernel with alpha = 0 (Step 1)
     if (int rc = launch_proj_own(ctx, gam0, gam0, gam0, 0, nc)) return rc;
     if (int rc = mvop_raw(gam0)) return rc;
@@ -918,6 +971,7 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
       if (int rc = launch_rod_unpack(ctx, ctx->u4.p, dU)) return rc;
     }
   }
+  if (int rc = save_for_warm_start(ctx, gfin)) return rc;
   int32_t* dact = ctx->derr;  // reuse the flag word as a counter
   SC_CUDA(cudaMemsetAsync(dact, 0, sizeof(int32_t), ctx->stream));
   if (int rc = launch_count_active(ctx, gfin, dact)) return rc;
@@ -952,7 +1006,7 @@ int sc_collision_step(sc_ctx* ctx, const sc_problem* prob, const sc_bbpgd_opts* 
   if ((rc = ensure(ctx, ctx->gam_user, std::max<int64_t>(nc, 1)))) return rc;
   sc_bbpgd_opts o = *opts;
   o.mu = prob->mu;
-  o.warm_start = 0;
+  if (o.warm_start != 2) o.warm_start = 0;  // (1 would need a caller gamma; 2 = previous solve)
   rc = sc_bbpgd_solve(ctx, &o, ctx->gam_user.p, nullptr, Fc_out, Uc_out, stats);
   if (n_c) *n_c = nc;
   return rc;

@@ -101,6 +101,9 @@ struct sc_ctx {
   bool have_q = false;
   sc::DBuf<double> q;
   sc::DBuf<double> gam[2], g[2], w, gam_user, uc;  // w: U_ext (n x 6); uc: U_c for time stepping
+  sc::DBuf<int64_t> prev_key;   // warm start: (i*n + j) keys of the previous solve (sorted)
+  sc::DBuf<double> prev_gam;    // ... and its gamma
+  int64_t prev_nc = 0, prev_n = -1;
   sc::DBuf<double> chunk_part;  // nchunks * 4
   sc::DBuf<double> chunk_red;   // reduced (allreduce output)
   sc::DBuf<double4> f4;         // sources: (Fx,Fy,Fz,0) [npad]
