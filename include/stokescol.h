@@ -167,6 +167,15 @@ typedef struct {
 int sc_collision_step(sc_ctx* ctx, const sc_problem* prob, const sc_bbpgd_opts* opts,
                       double* Fc_out, double* Uc_out, int64_t* n_c, sc_bbpgd_stats* stats);
 
+/* ------------------------------------- NEXT row f3: APGD comparison solver */
+/* Accelerated projected gradient descent (Mazhar et al. 2015) on
+ * the same CQP and MVOP as sc_bbpgd_solve, for the paper's BBPGD-vs-APGD MVOP
+ * comparison.  Uses opts->mu, tol, max_iter (gamma_0 = 0);
+ * stats->mvops counts every mobility solve (back-tracking trials included),
+ * stats->bb_breakdowns counts gradient restarts.  One GPU (SC_EINVAL on a
+ * multi-GPU or emulated context). */
+int sc_apgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double* g_out, sc_bbpgd_stats* stats);
+
 /* --------------------------------------------- NEXT row f1: one time step */
 /* The four steps of P:L480-L489: U_nc = Mobility(F_ext), contacts + D, the LCP
  * (BBPGD) -> U_c, and the explicit Euler update of the configuration

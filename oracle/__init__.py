@@ -92,6 +92,8 @@ def _declare(L):
     L.orc_minmap_residual.restype = d
     L.orc_minmap_residual.argtypes = [i64, vp, vp]
     L.orc_euler_update.argtypes = [i64, d, vp, vp, vp, vp]
+    L.orc_apgd.argtypes = [C.POINTER(_Sys), vp, d, i32, vp, vp, C.POINTER(Stats)]
+    L.orc_apgd_dense.argtypes = [i64, vp, vp, d, i32, vp, vp, C.POINTER(Stats)]
 
 
 def _p(a):
@@ -238,6 +240,13 @@ class System:
         _check(lib().orc_mvop(C.byref(self.s), _p(x), _p(w)), "mvop")
         return w
 
+    def apgd(self, q, tol=1e-8, max_iter=20000):
+        q = _f64(q)
+        nc = self.ct.nc
+        gamma = np.zeros(nc); g = np.empty(nc); st = Stats()
+        rc = _check(lib().orc_apgd(C.byref(self.s), _p(q), tol, max_iter, _p(gamma), _p(g), C.byref(st)), "apgd")
+        return {"gamma": gamma, "g": g, "status": rc, **st.as_dict()}
+
     def bbpgd(self, q, tol=1e-8, max_iter=5000, bb_mode=0, fixed_iters=0, gamma0=None):
         q = _f64(q)
         nc = self.ct.nc
@@ -247,6 +256,14 @@ class System:
         rc = _check(lib().orc_bbpgd(C.byref(self.s), _p(q), tol, max_iter, bb_mode, int(fixed_iters),
                                     _p(gamma), _p(g), _p(Fc), _p(Uc), C.byref(st)), "bbpgd")
         return {"gamma": gamma, "g": g, "Fc": Fc, "Uc": Uc, "status": rc, **st.as_dict()}
+
+
+def apgd_dense(M, q, tol=1e-8, max_iter=20000):
+    M, q = _f64(M), _f64(q)
+    n = q.shape[0]
+    gamma = np.zeros(n); g = np.empty(n); st = Stats()
+    rc = _check(lib().orc_apgd_dense(n, _p(M), _p(q), tol, max_iter, _p(gamma), _p(g), C.byref(st)), "apgd_dense")
+    return {"gamma": gamma, "g": g, "status": rc, **st.as_dict()}
 
 
 def bbpgd_dense(M, q, tol=1e-8, max_iter=5000, bb_mode=0):

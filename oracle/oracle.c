@@ -709,3 +709,113 @@ int orc_euler_update(int64_t n, double dt, const double* UW, double* pos, double
   }
   return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* APGD (NEXT row f3): accelerated projected gradient descent of Mazhar et   */
+/* al. 2015, the comparison solver the paper cites.  Readings  */
+/* (A24): gamma_0 = 0, L_0 = g0.M g0 / g0.g0, back-tracking L <- 2L */
+/* until f(x') <= f(y) + g.(x' - y) + L/2 |x' - y|^2, Nesterov theta / beta, */
+/* gradient restart when g.(x' - x) > 0, L <- 0.9 L after each step, stop on */
+/* phi(x', M x' + q) < tol.  stats->bb_breakdowns = restarts.                 */
+/* ------------------------------------------------------------------------ */
+static int apgd_core(int64_t n, mvop_fn mv, const void* ctx, const double* q, double tol, int32_t max_iter,
+                     double* gamma, double* g_out, orc_stats* st) {
+  memset(st, 0, sizeof(*st));
+  size_t bytes = sizeof(double) * (size_t)(n > 0 ? n : 1);
+  double* x = (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+  double* xn = (double*)malloc(bytes);
+  double* y = (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+  double* gy = (double*)malloc(bytes);
+  double* gn = (double*)malloc(bytes);
+  double* w = (double*)malloc(bytes);
+  int status = 0;
+  /* gamma_0 = 0, g_0 = M 0 + q = q (one counted MVOP, as Step 2 of Alg. 1) */
+  for (int64_t l = 0; l < n; ++l) gy[l] = q[l];
+  st->mvops = 1;
+  st->residual = orc_minmap_residual(n, x, gy);
+  if (st->residual < tol) { st->converged = 1; memcpy(gn, gy, bytes); goto done; }
+  if (mv(ctx, gy, w)) { status = -1; goto done; }
+  st->mvops = 2;
+  double L = dot(n, gy, w) / dot(n, gy, gy);
+  if (!(isfinite(L) && L > 0.0)) { status = -3; goto done; }
+  double t = 1.0 / L, theta = 1.0, fy = 0.0;
+  int restarts = 0;
+  for (int32_t k = 1; k <= max_iter; ++k) {
+    double fxn = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int bt = 0;; ++bt) {
+      long double a0 = 0.0L, a1 = 0.0L, a2 = 0.0L;
+      for (int64_t l = 0; l < n; ++l) {
+        double v = y[l] - t * gy[l];
+        xn[l] = v > 0.0 ? v : 0.0;
+        double d = xn[l] - y[l];
+        a0 += (long double)gy[l] * d;
+        a1 += (long double)d * d;
+        a2 += (long double)gy[l] * (xn[l] - x[l]);
+      }
+      s0 = (double)a0; s1 = (double)a1; s2 = (double)a2;
+      if (mv(ctx, xn, w)) { status = -1; goto done; }
+      st->mvops += 1;
+      for (int64_t l = 0; l < n; ++l) gn[l] = w[l] + q[l];
+      fxn = 0.5 * dot(n, xn, w) + dot(n, q, xn);
+      double rhs = fy + s0 + 0.5 * L * s1;
+      if (fxn <= rhs + 1e-12 * (fabs(fxn) + fabs(rhs)) || bt >= 60) break;
+      L *= 2.0;
+      t = 1.0 / L;
+    }
+    st->iters = k;
+    st->residual = orc_minmap_residual(n, xn, gn);
+    if (!isfinite(st->residual)) { status = -3; goto done; }
+    double theta_n = 0.5 * (-theta * theta + theta * sqrt(theta * theta + 4.0));
+    double beta = theta * (1.0 - theta) / (theta * theta + theta_n);
+    int restart = s2 > 0.0;
+    for (int64_t l = 0; l < n; ++l) {
+      double xo = x[l];
+      x[l] = xn[l];
+      xn[l] = xo; /* xn now holds gamma_k */
+    }
+    if (st->residual < tol) { st->converged = 1; break; }
+    if (restart) {
+      ++restarts;
+      memcpy(y, x, bytes);
+      memcpy(gy, gn, bytes);
+      fy = fxn;
+      theta = 1.0;
+    } else {
+      for (int64_t l = 0; l < n; ++l) y[l] = x[l] + beta * (x[l] - xn[l]);
+      if (mv(ctx, y, w)) { status = -1; goto done; }
+      st->mvops += 1;
+      for (int64_t l = 0; l < n; ++l) gy[l] = w[l] + q[l];
+      fy = 0.5 * dot(n, y, w) + dot(n, q, y);
+      theta = theta_n;
+    }
+    L *= 0.9;
+    t = 1.0 / L;
+  }
+  st->bb_breakdowns = restarts;
+  if (!st->converged) status = 1;
+done:
+  memcpy(gamma, x, bytes);
+  if (g_out && status >= 0) {
+    /* gradient at the returned iterate */
+    if (mv(ctx, x, w) == 0)
+      for (int64_t l = 0; l < n; ++l) g_out[l] = w[l] + q[l];
+  }
+  {
+    int32_t act = 0;
+    for (int64_t l = 0; l < n; ++l) if (gamma[l] > 0.0) ++act;
+    st->active = act;
+  }
+  free(x); free(xn); free(y); free(gy); free(gn); free(w);
+  return status;
+}
+
+int orc_apgd(const orc_system* s, const double* q, double tol, int32_t max_iter, double* gamma, double* g_out,
+             orc_stats* st) {
+  return apgd_core(s->nc, sys_mv, s, q, tol, max_iter, gamma, g_out, st);
+}
+
+int orc_apgd_dense(int64_t n, const double* M, const double* q, double tol, int32_t max_iter, double* gamma,
+                   double* g_out, orc_stats* st) {
+  dense_ctx d = {n, M};
+  return apgd_core(n, dense_mv, &d, q, tol, max_iter, gamma, g_out, st);
+}

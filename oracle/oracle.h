@@ -103,6 +103,13 @@ int orc_bbpgd_dense(int64_t n, const double* M, const double* q, double tol, int
 /* phi = || min(gamma, g) ||_2. */
 double orc_minmap_residual(int64_t n, const double* gamma, const double* g);
 
+/* APGD comparison solver (Mazhar et al. 2015, cited at P:L546-L558; readings A24):
+ * gamma_0 = 0; stats->mvops counts every MVOP incl. back-tracking; bb_breakdowns = restarts. */
+int orc_apgd(const orc_system* s, const double* q, double tol, int32_t max_iter, double* gamma, double* g_out,
+             orc_stats* st);
+int orc_apgd_dense(int64_t n, const double* M, const double* q, double tol, int32_t max_iter, double* gamma,
+                   double* g_out, orc_stats* st);
+
 /* Explicit Euler update of the configuration, step 4 of the
  * four-step procedure: c' = c + dt U, theta' = normalize(theta + dt Psi(theta) Omega)
  * with Psi = 1/2 [-p^T ; s I - [p]x] for theta = (s, p); rod axes t' = normalize(t + dt Omega x t).

@@ -199,6 +199,16 @@ class Context:
         self.n, self.nc, self.kind = n, nc.value, kind
         return {"status": rc, "nc": nc.value, **st.as_dict()}
 
+    def apgd_solve(self, mu=1.0, tol=1e-8, max_iter=20000):
+        """APGD comparison solver on the same CQP (NEXT row f3); stats['bb_breakdowns'] = restarts."""
+        opts = _lib.BbpgdOpts(float(mu), float(tol), int(max_iter), 0, 0, 0)
+        gamma = self._dev((self.nc,))
+        g = self._dev((self.nc,))
+        st = _lib.BbpgdStats()
+        rc = self._rc(self.lib.sc_apgd_solve(self._h, C.byref(opts), _ptr(gamma), _ptr(g), C.byref(st)),
+                      allow=(0, 1))
+        return {"gamma": gamma, "g": g, "status": rc, **st.as_dict()}
+
     def time_step(self, kind, pos, F_ext, radius=None, direction=None, length=None, b=0.5, gap_abs=0.0,
                   gap_rel=0.1, mu=1.0, dt=0.01, tol=1e-8, max_iter=5000, bb_mode=0, quat=None, want_U=True,
                   warm_start=False):

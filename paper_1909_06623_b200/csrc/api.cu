@@ -1012,6 +1012,139 @@ int sc_collision_step(sc_ctx* ctx, const sc_problem* prob, const sc_bbpgd_opts* 
   return rc;
 }
 
+// ------------------------------------------------------------ NEXT row f3: APGD
+// Accelerated projected gradient descent (Mazhar et al. 2015, cited at P:L546-L558), the
+// comparison solver of the paper's Fig. pairshearBBPGD; readings in DESIGN.md
+// (A24): gamma_0 = 0, L_0 = g0.M g0 / g0.g0 (the Cauchy-step Lipschitz estimate, one MVOP like
+// BBPGD's Step 6), back-tracking L <- 2L until f(gamma') <= f(y) + g.(gamma'-y) + L/2|gamma'-y|^2,
+// Nesterov theta/beta, gradient restart when g.(gamma' - gamma) > 0, L <- 0.9 L after a step,
+// stop on the same residual phi = ||min(gamma, g)|| < tol.  One GPU.
+int sc_apgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double* g_out, sc_bbpgd_stats* stats) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (opts == nullptr || !(opts->mu > 0.0) || !(opts->tol >= 0.0) || opts->max_iter < 0)
+    return fail(ctx, SC_EINVAL, "apgd_solve: bad options");
+  if (!ctx->assembled || !ctx->have_q) return fail(ctx, SC_EINVAL, "apgd_solve needs assemble_D and lcp_q first");
+  if (ctx->world > 1 || ctx->emul_world > 1) return fail(ctx, SC_EINVAL, "apgd_solve is a 1-GPU comparison solver");
+  const int64_t nc = ctx->nc;
+  if (nc > 0 && gamma == nullptr) return fail(ctx, SC_EINVAL, "apgd_solve: gamma is NULL");
+  cudaSetDevice(ctx->device);
+  sc_bbpgd_stats stt;
+  std::memset(&stt, 0, sizeof(stt));
+  const double mu = opts->mu;
+  if (int rc = ensure_rod_mob(ctx, mu)) return rc;
+  Stager st(ctx);
+  double *dgam = nullptr, *dg = nullptr;
+  if (int rc = st.out(gamma, nc, &dgam)) return rc;
+  if (int rc = st.out(g_out, nc, &dg)) return rc;
+  if (nc == 0) {
+    stt.converged = 1;
+    if (stats) *stats = stt;
+    return st.finish();
+  }
+  if (int rc = ensure(ctx, ctx->apgd_y, nc)) return rc;
+  if (int rc = ensure(ctx, ctx->apgd_sums, 4)) return rc;
+  double* x = ctx->gam[0].p;   // gamma_k
+  double* xn = ctx->gam[1].p;  // gamma_{k+1}
+  double* y = ctx->apgd_y.p;   // extrapolated point
+  double* gy = ctx->g[0].p;    // g at y
+  double* gn = ctx->g[1].p;    // g at gamma_{k+1}
+  const bool spheres = ctx->kind == kSpheres;
+  Dist D(ctx);
+  double hs[4];
+  auto sums = [&](double* out) -> int {
+    if (int rc = launch_sum_chunks(ctx, ctx->apgd_sums.p)) return rc;
+    SC_CUDA(cudaMemcpyAsync(out, ctx->apgd_sums.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    SC_CUDA(cudaStreamSynchronize(ctx->stream));
+    return 0;
+  };
+  // gout = M v + q; returns (v.Mv, q.v, phi(v)^2)
+  auto mvop_grad = [&](const double* v, double* gout, double* out) -> int {
+    if (int rc = launch_gather_raw(ctx, v, mu, nullptr)) return rc;
+    if (spheres) {
+      if (int rc = D.rpy(mu, nullptr)) return rc;
+    }
+    if (int rc = launch_dt(ctx, 4, v, nullptr, nullptr, gout, 0, ctx->nchunks, false)) return rc;
+    return sums(out);
+  };
+  SC_CUDA(cudaMemsetAsync(ctx->dsc, 0, sizeof(DevScalars), ctx->stream));  // done = 0 for the kernels
+  // gamma_0 = 0: g_0 = q (the zero-vector MVOP, counted as in BBPGD), phi_0
+  SC_CUDA(cudaMemsetAsync(x, 0, nc * sizeof(double), ctx->stream));
+  SC_CUDA(cudaMemsetAsync(y, 0, nc * sizeof(double), ctx->stream));
+  if (int rc = launch_dt(ctx, 3, x, nullptr, nullptr, gy, 0, ctx->nchunks, false)) return rc;
+  if (int rc = sums(hs)) return rc;
+  stt.mvops = 1;
+  double phi = std::sqrt(hs[3]);
+  int rc_final = SC_OK;
+  if (!(phi < opts->tol)) {
+    // L_0 = g0.M g0 / g0.g0: kDtGrad on v = g0 = q gives v.Mv and q.v = |q|^2
+    if (int rc = mvop_grad(gy, gn, hs)) return rc;
+    stt.mvops = 2;
+    double L = hs[0] / hs[1];
+    if (!(std::isfinite(L) && L > 0.0)) return fail(ctx, SC_ENONFINITE, "apgd: bad Lipschitz estimate");
+    double t = 1.0 / L, theta = 1.0, fy = 0.0;  // f(y_0) = f(0) = 0
+    int restarts = 0;
+    bool conv = false;
+    for (int k = 1; k <= opts->max_iter; ++k) {
+      double s[4], fxn = 0.0;
+      for (int bt = 0;; ++bt) {  // back-tracking on the local Lipschitz estimate
+        if (int rc = apgd_launch_step(ctx, y, gy, x, t, xn)) return rc;
+        if (int rc = sums(s)) return rc;
+        if (int rc = mvop_grad(xn, gn, hs)) return rc;
+        stt.mvops += 1;
+        fxn = 0.5 * hs[0] + hs[1];
+        const double rhs = fy + s[0] + 0.5 * L * s[1];
+        if (fxn <= rhs + 1e-12 * (std::fabs(fxn) + std::fabs(rhs)) || bt >= 60) break;
+        L *= 2.0;
+        t = 1.0 / L;
+      }
+      stt.iters = k;
+      phi = std::sqrt(hs[2]);
+      if (!std::isfinite(phi)) return fail(ctx, SC_ENONFINITE, "apgd: non-finite residual");
+      std::swap(x, xn);  // gamma_{k+1} accepted (xn now holds gamma_k)
+      std::swap(gy, gn);  // gy <- g(gamma_{k+1}) (kept if the next y is gamma_{k+1})
+      if (phi < opts->tol) {
+        conv = true;
+        break;
+      }
+      const double theta_n = 0.5 * (-theta * theta + theta * std::sqrt(theta * theta + 4.0));
+      const double beta = theta * (1.0 - theta) / (theta * theta + theta_n);
+      if (s[2] > 0.0) {  // gradient restart: y = gamma_{k+1}, theta = 1 (g at y already known)
+        ++restarts;
+        SC_CUDA(cudaMemcpyAsync(y, x, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        fy = fxn;
+        theta = 1.0;
+      } else {
+        if (int rc = apgd_launch_momentum(ctx, x, xn, beta, y)) return rc;
+        if (int rc = mvop_grad(y, gy, hs)) return rc;
+        stt.mvops += 1;
+        fy = 0.5 * hs[0] + hs[1];
+        theta = theta_n;
+      }
+      L *= 0.9;
+      t = 1.0 / L;
+    }
+    stt.bb_breakdowns = restarts;
+    stt.alpha = t;
+    if (!conv) rc_final = SC_NOT_CONVERGED;
+    stt.converged = conv ? 1 : 0;
+    // the accepted iterate is x; its gradient: gy if the loop ended on convergence or restart
+    // bookkeeping differs -- recompute once for the output (not counted as an MVOP of the method)
+    if (int rc = mvop_grad(x, gn, hs)) return rc;
+    phi = std::sqrt(hs[2]);
+    if (dg) SC_CUDA(cudaMemcpyAsync(dg, gn, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  } else {
+    stt.converged = 1;
+    if (dg) SC_CUDA(cudaMemcpyAsync(dg, gy, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  stt.residual = phi;
+  SC_CUDA(cudaMemcpyAsync(dgam, x, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (int rc = st.finish()) return rc;
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (int rc = check_flag(ctx, SC_EDEGENERATE, "coincident centres in the RPY sum")) return rc;
+  if (stats) *stats = stt;
+  return rc_final;
+}
+
 // Step 4: C^{k+1} = C^k + G U dt, quaternion kinematics theta' = Psi Omega
 // with renormalisation; rod axes t' = normalize(t + dt Omega x t).
 // Same association as the plain definition (explicit round-to-nearest).

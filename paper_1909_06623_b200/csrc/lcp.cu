@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kR) finalize_kernel(const double* __restrict__
   finalize_block(part, nchunks, mode, s, red);
 }
 
-enum DtMode { kDtIter = 0, kDtAlpha0 = 1, kDtG0 = 2, kDtInitQ = 3 };
+enum DtMode { kDtIter = 0, kDtAlpha0 = 1, kDtG0 = 2, kDtInitQ = 3, kDtGrad = 4 };
 
 // One CTA per chunk c in [c0, c0 + gridDim.x).  FUSE (1 GPU): the last CTA to finish
 // (threadfence + counter) also runs K-FINALIZE, saving a launch per iteration; the sums are
@@ -244,6 +244,14 @@ __global__ void __launch_bounds__(kR) dt_kernel(
       const double g0 = g_old[l];
       p[0] = fma(g0, g0, p[0]);
       p[1] = fma(g0, v, p[1]);
+    } else if (MODE == kDtGrad) {  // g = M x + q for x = gam_new; x.Mx, q.x, phi(x)^2 (APGD)
+      const double x = gam_new[l];
+      const double g = v + q[l];
+      g_out[l] = g;
+      const double m = x < g ? x : g;
+      p[0] = fma(x, v, p[0]);
+      p[1] = fma(q[l], x, p[1]);
+      p[2] = fma(m, m, p[2]);
     } else {  // kDtG0 (warm start: g0 = D^T U + q) / kDtInitQ (gamma0 = 0: g0 = q)
       const double g = (MODE == kDtG0 ? v : 0.0) + q[l];
       g_out[l] = g;
@@ -448,6 +456,7 @@ int launch_dt(sc_ctx* ctx, int mode, const double* gam_new, const double* gam_ol
       case kDtIter: SC_DT(kSpheres, kDtIter); break;
       case kDtAlpha0: SC_DT(kSpheres, kDtAlpha0); break;
       case kDtG0: SC_DT(kSpheres, kDtG0); break;
+      case kDtGrad: SC_DT(kSpheres, kDtGrad); break;
       default: SC_DT(kSpheres, kDtInitQ); break;
     }
   } else {
@@ -455,6 +464,7 @@ int launch_dt(sc_ctx* ctx, int mode, const double* gam_new, const double* gam_ol
       case kDtIter: SC_DT(kRods, kDtIter); break;
       case kDtAlpha0: SC_DT(kRods, kDtAlpha0); break;
       case kDtG0: SC_DT(kRods, kDtG0); break;
+      case kDtGrad: SC_DT(kRods, kDtGrad); break;
       default: SC_DT(kRods, kDtInitQ); break;
     }
   }

@@ -101,6 +101,7 @@ struct sc_ctx {
   bool have_q = false;
   sc::DBuf<double> q;
   sc::DBuf<double> gam[2], g[2], w, gam_user, uc;  // w: U_ext (n x 6); uc: U_c for time stepping
+  sc::DBuf<double> apgd_y, apgd_sums;  // APGD: extrapolated point, reduced sums
   sc::DBuf<int64_t> prev_key;   // warm start: (i*n + j) keys of the previous solve (sorted)
   sc::DBuf<double> prev_gam;    // ... and its gamma
   int64_t prev_nc = 0, prev_n = -1;
@@ -213,5 +214,10 @@ int launch_rod_drag_user(sc_ctx* ctx, const double* FT, double mu, double* UW);
 int launch_rod_unpack(sc_ctx* ctx, const double4* u4, double* UW);
 int launch_count_active(sc_ctx* ctx, const double* gam, int32_t* out);
 int launch_q(sc_ctx* ctx, double dt, const double* dtu, double* q);
+
+// ---- APGD comparison solver (apgd.cu) --------------------------------------
+int apgd_launch_step(sc_ctx* ctx, const double* y, const double* g, const double* gam, double t, double* gam_new);
+int apgd_launch_momentum(sc_ctx* ctx, const double* gam_new, const double* gam, double beta, double* y);
+int launch_sum_chunks(sc_ctx* ctx, double* out4);
 
 }  // namespace sc

@@ -395,3 +395,23 @@ def test_time_steps_warm_start_matches_oracle(ctx):
     scale = np.abs(o["U"]).max() * p.dt
     np.testing.assert_allclose(_np(pos_g), po.pos, rtol=0, atol=1e-7 * scale + 1e-13)
     assert it_warm[0] == it_cold[0]  # the first step has no previous gamma
+
+
+# ---------------------------------------------------------------- NEXT row f3: APGD
+@pytest.mark.parametrize("name,n", [("C1", None), ("C4", 5000)])
+def test_apgd_vs_oracle_and_bbpgd(ctx, name, n):
+    """APGD on the GPU reaches the same gamma as the oracle's APGD and as BBPGD, with more
+    MVOPs than BBPGD."""
+    p = make_problem(name, n=n, fixed_iters=0)
+    b = _gpu_solve(ctx, p)
+    a = ctx.apgd_solve(mu=p.mu, tol=p.tol, max_iter=20000)
+    sysm = oracle.system_for(p)
+    q = sysm.lcp_q(p.dt, sysm.mobility(p.force))
+    ao = sysm.apgd(q, tol=p.tol, max_iter=20000)
+    assert a["status"] == 0 and a["residual"] < 1e-8 and ao["status"] == 0
+    ga = _np(a["gamma"])
+    assert _relL2(ga, ao["gamma"]) <= 1e-6
+    assert _relL2(ga, _np(b["gamma"])) <= 1e-6
+    assert a["mvops"] > b["mvops"]
+    g_cert = sysm.mvop(ga) + q
+    np.testing.assert_allclose(_np(a["g"]), g_cert, rtol=0, atol=1e-10 * np.abs(q).max())
