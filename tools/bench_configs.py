@@ -116,11 +116,40 @@ def main():
     ap.add_argument("--configs", default="C1,C2,C3,C4,C5")
     ap.add_argument("--no-oracle", action="store_true")
     ap.add_argument("--c5-converged", action="store_true", help="also run C5 to convergence (long)")
+    ap.add_argument("--apgd", default="", help="configs to also solve with APGD (BBPGD vs APGD MVOPs)")
     a = ap.parse_args()
     for name in a.configs.split(","):
         print(json.dumps(run(name, None, not a.no_oracle)), flush=True)
         if name == "C5" and a.c5_converged:
             print(json.dumps(run(name, 0, False)), flush=True)
+    for name in [c for c in a.apgd.split(",") if c]:
+        print(json.dumps(apgd_compare(name)), flush=True)
+
+
+def apgd_compare(name):
+    """The paper's BBPGD-vs-APGD comparison on one config: MVOPs and time."""
+    p = make_problem(name, fixed_iters=0)
+    dev = torch.device("cuda:0")
+    t = lambda a: None if a is None else torch.as_tensor(a, device=dev)
+    ctx = Context(0)
+    if p.kind == "spheres":
+        ctx.build_contacts_spheres(t(p.pos), t(p.radius), p.gap_abs, p.gap_rel)
+    else:
+        ctx.build_contacts_rods(t(p.pos), t(p.direction), t(p.length), p.rod_radius, p.gap_abs)
+    ctx.assemble_D()
+    ctx.lcp_q(p.dt, ctx.mobility_apply(t(p.force), mu=p.mu))
+    out = {"config": name, "compare": "bbpgd_vs_apgd"}
+    for label, fn in (("bbpgd", lambda: ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=p.max_iter)),
+                      ("apgd", lambda: ctx.apgd_solve(mu=p.mu, tol=p.tol, max_iter=20 * p.max_iter))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = fn()
+        torch.cuda.synchronize()
+        out[label] = {"iters": r["iters"], "mvops": r["mvops"], "residual": r["residual"],
+                      "converged": r["converged"], "seconds": time.perf_counter() - t0}
+        out[label + "_gamma_norm"] = float(r["gamma"].norm())
+    ctx.close()
+    return out
 
 
 if __name__ == "__main__":
