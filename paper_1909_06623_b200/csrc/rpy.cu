@@ -70,6 +70,7 @@ struct Consts {
   double kn2;     // -9/(32a)           (mono, near)
   double kn3;     // 1/(8 a^2)          (mono, near)
   long long near_bits;  // bits of (2a)^2  (mono)
+  int tau_hi;           // high word of (2a)^2 (mono; symmetric kernel's clamp)
 };
 
 // Far-field contributions of TPT targets x SU sources, branch-free and written stage by
@@ -312,6 +313,10 @@ constexpr size_t kRpySmem = 4 * kRpyTile * sizeof(double4) + 2 * sizeof(uint64_t
 // l - 1 by one warp shuffle per step; after 32 steps lane l holds source l's sum and adds it
 // to the CTA's shared accumulator (no two warps touch one sub-block in a phase).
 // SI == SJ: forward contributions only (every ordered pair of the super-block once).
+// Near pairs (r < 2 abar) and the self pair are NOT tested in the loop: r^2 is clamped on its
+// high word (one integer max, rpy_common.cuh) so they get a bounded far-formula value, which
+// the combine swaps for the overlap branch (tools/sym_tune.cu: 82.9% vs 81.3% of the FP64
+// peak for the compare + select form).
 //
 // Output: part[slot][row][3] with slot = the partner super-block: rows of SI get slot SJ
 // (forward), rows of SJ get slot SI (reverse), so every (slot, row) is written exactly
@@ -379,6 +384,19 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       double dx[TPT], dy[TPT], dz[TPT], r2[TPT], y[TPT], h[TPT], e[TPT], c1[TPT], c2[TPT];
 #pragma unroll
       for (int m = 0; m < TPT; ++m) r2[m] = rpy_r2(p[m], pj, dx[m], dy[m], dz[m]);
+      // near pairs (incl. self): far formula at the clamped r^2 (rpy_common.cuh); the
+      // combine swaps it for the overlap branch -- no compare/select in this loop
+      double ab2[TPT];
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) {
+        if (POLY) {
+          const double abar = p[m].w + pj.w;
+          ab2[m] = abar * abar;
+          r2[m] = rpy_clamp_r2(r2[m], rpy_tau_hi(ab2[m]));
+        } else {
+          r2[m] = rpy_clamp_r2(r2[m], k.tau_hi);
+        }
+      }
 #pragma unroll
       for (int m = 0; m < TPT; ++m) asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y[m]) : "d"(r2[m]));
 #pragma unroll
@@ -398,20 +416,14 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       for (int m = 0; m < TPT; ++m) e[m] = y[m] * h[m];  // rinv^3
 #pragma unroll
       for (int m = 0; m < TPT; ++m) {
-        bool nr;
         if (POLY) {
-          const double abar = p[m].w + pj.w;
-          const double s2 = (abar * abar) * h[m];
+          const double s2 = ab2[m] * h[m];
           c1[m] = y[m] * fma(s2, 2.0 / 3.0, 1.0);
           c2[m] = e[m] * fma(s2, -2.0, 1.0);
-          nr = rpy_is_near(r2[m], abar, true, 0);
         } else {
           c1[m] = fma(k.k23a2, e[m], y[m]);
           c2[m] = e[m] * fma(k.m2a2, h[m], 1.0);
-          nr = rpy_is_near(r2[m], 0.0, false, k.near_bits);
         }
-        c1[m] = nr ? 0.0 : c1[m];
-        c2[m] = nr ? 0.0 : c2[m];
       }
       // forward: U_i += c1 f_j + c2 (d.f_j) d
 #pragma unroll
@@ -521,9 +533,13 @@ __global__ void rpy_sym_combine_kernel(const double* __restrict__ part, int64_t 
     const double4 pi = pos4[row];
     const double4 fi = f4[row];
     const double cs = (2.0 / 3.0) / pi.w;  // self: 4/(3 a_i)
-    two_sum_acc(hx, lx, cs * fi.x);
-    two_sum_acc(hy, ly, cs * fi.y);
-    two_sum_acc(hz, lz, cs * fi.z);
+    {  // the pair loop added the clamped far formula for the self pair (d = 0): swap it
+      double sx, sy, sz;
+      rpy_far_clamped_contrib(0.0, 0.0, 0.0, 0.0, 2.0 * pi.w, fi, sx, sy, sz);
+      two_sum_acc(hx, lx, fma(cs, fi.x, -sx));
+      two_sum_acc(hy, ly, fma(cs, fi.y, -sy));
+      two_sum_acc(hz, lz, fma(cs, fi.z, -sz));
+    }
     const double a_mono = 2.0 * pi.w;
     const long long near_bits = __double_as_longlong(4.0 * (a_mono * a_mono));
     for (int32_t e = near_ptr[row]; e < near_ptr[row + 1]; ++e) {
@@ -545,9 +561,11 @@ __global__ void rpy_sym_combine_kernel(const double* __restrict__ part, int64_t 
       const double c1 = (4.0 / 3.0) * ia * fma(-9.0 / 32.0 * ia, rr, 1.0);
       const double c2 = 0.125 * ia * ia * rs;
       const double t = c2 * fma(dz, fj.z, fma(dy, fj.y, dx * fj.x));
-      two_sum_acc(hx, lx, fma(t, dx, c1 * fj.x));
-      two_sum_acc(hy, ly, fma(t, dy, c1 * fj.y));
-      two_sum_acc(hz, lz, fma(t, dz, c1 * fj.z));
+      double fx_, fy_, fz_;  // minus what the pair loop added for this pair
+      rpy_far_clamped_contrib(dx, dy, dz, r2, abar, fj, fx_, fy_, fz_);
+      two_sum_acc(hx, lx, fma(t, dx, fma(c1, fj.x, -fx_)));
+      two_sum_acc(hy, ly, fma(t, dy, fma(c1, fj.y, -fy_)));
+      two_sum_acc(hz, lz, fma(t, dz, fma(c1, fj.z, -fz_)));
     }
   }
   out[row] = row < n ? make_double4(scale * (hx + lx), scale * (hy + ly), scale * (hz + lz), 0.0)
@@ -578,6 +596,7 @@ static Consts make_consts(double a) {
   k.kn3 = 1.0 / (8.0 * a * a);
   const double n2 = 4.0 * a * a;
   k.near_bits = *reinterpret_cast<const long long*>(&n2);
+  k.tau_hi = static_cast<int>(k.near_bits >> 32);
   return k;
 }
 

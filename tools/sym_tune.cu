@@ -1,0 +1,227 @@
+// sym_tune.cu -- standalone tuning harness for the symmetric RPY pair-tile loop (not product
+// code).  C5 shape: N = 262144 monodisperse spheres (a = 1), volume fraction 0.3, forces
+// N(0,1)-ish.  Times variants of the inner loop on the first NP super-block pairs and checks
+// that the variants that should agree do.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o sym_tune sym_tune.cu && ./sym_tune
+// Variants:
+//   0  product loop: near pairs zeroed by an integer compare of r^2 bits + FSEL
+//   1  r^2 clamped to (2a)^2 with fmax (near pairs get the far formula at r = 2a; the product
+//      would subtract that in the combine) -- no compare/select in the loop
+//   2  no near handling at all (timing bound only; results differ)
+//   3  variant 1 + source sub-block duplicated in shared memory (no "& 31" index wrap)
+//   4  high-word clamp: r2c = (max(hi(r2), hi(tau)), lo(r2)), one integer max per pair
+//   5  variant 4 + duplicated sub-block
+//   6  variant 4 + next step's source prefetched from shared memory
+//   7  variant 6, step loop unrolled 2
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s line %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
+
+constexpr int SB = 512, NSUB = 16;
+
+__device__ __forceinline__ double rsq_approx(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+template <int VAR, int NW, int TPT, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
+    sym(const double4* __restrict__ pos4, const double4* __restrict__ f4, const int2* __restrict__ pairs,
+        int64_t npad, double k23a2, double m2a2, long long near_bits, double a4, double* __restrict__ part) {
+  constexpr int DUP = (VAR == 3 || VAR == 5) ? 2 : 1;
+  extern __shared__ double4 smem[];
+  double4* sp = smem;
+  double4* sf = smem + SB * DUP;
+  double* sacc = reinterpret_cast<double*>(smem + 2 * SB * DUP);
+  const int2 pr = pairs[blockIdx.x];
+  const int64_t SI = pr.x, SJ = pr.y;
+  const bool rev = SI != SJ;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  for (int q = tid; q < SB; q += NW * 32) {
+    const int sub = q >> 5, l = q & 31;
+    const double4 pp = pos4[SJ * SB + q], ff = f4[SJ * SB + q];
+    if (DUP == 2) {
+      sp[sub * 64 + l] = pp; sp[sub * 64 + l + 32] = pp;
+      sf[sub * 64 + l] = ff; sf[sub * 64 + l + 32] = ff;
+    } else {
+      sp[q] = pp; sf[q] = ff;
+    }
+  }
+  double4 p[TPT];
+  double fx[TPT], fy[TPT], fz[TPT], ax[TPT], ay[TPT], az[TPT];
+#pragma unroll
+  for (int m = 0; m < TPT; ++m) {
+    const int64_t row = SI * SB + (w + NW * m) * 32 + lane;
+    p[m] = pos4[row];
+    const double4 f = f4[row];
+    fx[m] = f.x; fy[m] = f.y; fz[m] = f.z;
+    ax[m] = ay[m] = az[m] = 0.0;
+  }
+  for (int q = tid; q < 3 * SB; q += NW * 32) sacc[q] = 0.0;
+  __syncthreads();
+#pragma unroll 1
+  for (int ph = 0; ph < NSUB; ++ph) {
+    const int cj = (w + ph) & (NSUB - 1);
+    const double4* tp = sp + cj * 32 * DUP;
+    const double4* tf = sf + cj * 32 * DUP;
+    double rx = 0.0, ry = 0.0, rz = 0.0;
+    constexpr bool PF = VAR >= 6;
+    constexpr int UNR = VAR == 7 ? 2 : 1;  // prefetch the next step's source from shared memory
+    double4 pjn = tp[lane], fjn = tf[lane];
+#pragma unroll (UNR)
+    for (int st = 0; st < 32; ++st) {
+      double4 pj, fj;
+      if (PF) {
+        pj = pjn; fj = fjn;
+        const int sn = (lane + st + 1) & 31;
+        pjn = tp[sn]; fjn = tf[sn];
+      } else {
+        const int s = DUP == 2 ? lane + st : ((lane + st) & 31);
+        pj = tp[s];
+        fj = tf[s];
+      }
+      double dx[TPT], dy[TPT], dz[TPT], r2[TPT], y[TPT], h[TPT], e[TPT], c1[TPT], c2[TPT];
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) {
+        dx[m] = pj.x - p[m].x; dy[m] = pj.y - p[m].y; dz[m] = pj.z - p[m].z;
+        r2[m] = fma(dz[m], dz[m], fma(dy[m], dy[m], dx[m] * dx[m]));
+      }
+      double rc[TPT];
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) {
+        if (VAR >= 4) {  // clamp the high word only: r2c = (max(hi(r2), hi(tau)), lo(r2))
+          const int hi = max(__double2hiint(r2[m]), static_cast<int>(near_bits >> 32));
+          rc[m] = __hiloint2double(hi, __double2loint(r2[m]));
+        } else {
+          rc[m] = (VAR == 1 || VAR == 3) ? fmax(r2[m], a4) : r2[m];
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) y[m] = rsq_approx(rc[m]);
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) h[m] = rc[m] * y[m];
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) e[m] = fma(-h[m], y[m], 1.0);
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) { h[m] = fma(0.375, e[m], 0.5); e[m] = y[m] * e[m]; }
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) y[m] = fma(e[m], h[m], y[m]);
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) h[m] = y[m] * y[m];
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) e[m] = y[m] * h[m];
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) {
+        c1[m] = fma(k23a2, e[m], y[m]);
+        c2[m] = e[m] * fma(m2a2, h[m], 1.0);
+        if (VAR == 0) {
+          const bool nr = __double_as_longlong(r2[m]) < near_bits;
+          c1[m] = nr ? 0.0 : c1[m];
+          c2[m] = nr ? 0.0 : c2[m];
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < TPT; ++m) {
+        const double t = c2[m] * fma(dz[m], fj.z, fma(dy[m], fj.y, dx[m] * fj.x));
+        ax[m] = fma(t, dx[m], fma(c1[m], fj.x, ax[m]));
+        ay[m] = fma(t, dy[m], fma(c1[m], fj.y, ay[m]));
+        az[m] = fma(t, dz[m], fma(c1[m], fj.z, az[m]));
+      }
+      if (rev) {
+#pragma unroll
+        for (int m = 0; m < TPT; ++m) {
+          const double t = c2[m] * fma(dz[m], fz[m], fma(dy[m], fy[m], dx[m] * fx[m]));
+          rx = fma(t, dx[m], fma(c1[m], fx[m], rx));
+          ry = fma(t, dy[m], fma(c1[m], fy[m], ry));
+          rz = fma(t, dz[m], fma(c1[m], fz[m], rz));
+        }
+        const int src = (lane + 1) & 31;
+        rx = __shfl_sync(0xffffffffu, rx, src);
+        ry = __shfl_sync(0xffffffffu, ry, src);
+        rz = __shfl_sync(0xffffffffu, rz, src);
+      }
+    }
+    if (rev) {
+      double* a = sacc + (cj * 32 + lane) * 3;
+      a[0] += rx; a[1] += ry; a[2] += rz;
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < TPT; ++m) {
+    const int64_t row = SI * SB + (w + NW * m) * 32 + lane;
+    double* o = part + (SJ * npad + row) * 3;
+    o[0] = ax[m]; o[1] = ay[m]; o[2] = az[m];
+  }
+  if (rev) {
+    __syncthreads();
+    double* o = part + (SI * npad + SJ * SB) * 3;
+    for (int q = tid; q < 3 * SB; q += NW * 32) o[q] = sacc[q];
+  }
+}
+
+int main(int argc, char** argv) {
+  const int64_t N = 262144, NS = N / SB;
+  const int NP = argc > 1 ? atoi(argv[1]) : 40000;  // super-block pairs timed
+  const double a = 1.0, phi = 0.3;
+  const double L = cbrt(N * (4.0 / 3.0) * M_PI / phi);
+  std::mt19937_64 rng(5);
+  std::uniform_real_distribution<double> U(0.0, L);
+  std::normal_distribution<double> G(0.0, 1.0);
+  std::vector<double4> hp(N), hf(N);
+  for (int64_t i = 0; i < N; ++i) {
+    hp[i] = make_double4(U(rng), U(rng), U(rng), 0.5 * a);
+    hf[i] = make_double4(G(rng), G(rng), G(rng), 0.0);
+  }
+  // pairs: SI < SJ off-diagonal tiles, spread over the matrix
+  std::vector<int2> pairs;
+  for (int64_t S = 0; S < NS && (int)pairs.size() < NP; ++S)
+    for (int64_t d = 1; d <= NS / 2 && (int)pairs.size() < NP; d += 1) pairs.push_back(make_int2(S, (S + d) % NS));
+  double4 *dp, *df; int2* dpr; double* part;
+  CK(cudaMalloc(&dp, N * sizeof(double4))); CK(cudaMalloc(&df, N * sizeof(double4)));
+  CK(cudaMalloc(&dpr, pairs.size() * sizeof(int2)));
+  CK(cudaMalloc(&part, (size_t)NS * N * 3 * sizeof(double)));
+  CK(cudaMemcpy(dp, hp.data(), N * sizeof(double4), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(df, hf.data(), N * sizeof(double4), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dpr, pairs.data(), pairs.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  const double n2 = 4 * a * a;
+  const long long nb = *reinterpret_cast<const long long*>(&n2);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  const double upairs = (double)pairs.size() * SB * SB;
+  auto run = [&](const char* name, auto kern, int threads, int dup) {
+    const size_t sm = 2 * SB * dup * sizeof(double4) + 3 * SB * sizeof(double);
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    for (int rep = 0; rep < 4; ++rep) {
+      CK(cudaEventRecord(e0));
+      kern<<<(unsigned)pairs.size(), threads, sm>>>(dp, df, dpr, N, 2.0 / 3.0 * a * a, -2.0 * a * a, nb, n2, part);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      CK(cudaGetLastError());
+      float ms; CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (rep == 3) {
+        // algorithmic: 2 ordered pairs x 37 flops per unordered pair
+        const double tf = upairs * 74.0 / (ms * 1e-3) / 1e12;
+        cudaFuncAttributes at; cudaFuncGetAttributes(&at, kern);
+        printf("%-28s %8.3f ms  %.3e upairs/s  %6.2f TFLOP/s-alg  %5.1f%% of 37.22  regs %d\n", name, ms,
+               upairs / (ms * 1e-3), tf, 100 * tf / 37.22496, at.numRegs);
+      }
+    }
+  };
+  run("v0 product (4,4,3)", sym<0, 4, 4, 3>, 128, 1);
+  run("v1 clamp (4,4,3)", sym<1, 4, 4, 3>, 128, 1);
+  run("v2 none (4,4,3)", sym<2, 4, 4, 3>, 128, 1);
+  run("v3 clamp+dup (4,4,3)", sym<3, 4, 4, 3>, 128, 2);
+  run("v4 hiclamp (4,4,3)", sym<4, 4, 4, 3>, 128, 1);
+  run("v5 hiclamp+dup (4,4,3)", sym<5, 4, 4, 3>, 128, 2);
+  run("v6 hiclamp+pf (4,4,3)", sym<6, 4, 4, 3>, 128, 1);
+  run("v7 hiclamp+pf+unr2 (4,4,3)", sym<7, 4, 4, 3>, 128, 1);
+  run("v0 product (4,4,3) again", sym<0, 4, 4, 3>, 128, 1);
+  return 0;
+}
