@@ -68,6 +68,26 @@ const char* sc_last_error(const sc_ctx* ctx);
 /* The stream the context orders its work on (a cudaStream_t). */
 void* sc_stream(const sc_ctx* ctx);
 
+/* ------------------------------- NEXT row f2: particle-boundary collisions */
+/* Static planar walls ("a vector D_l can be added to D ... with
+ * non-zero entries corresponding to the degrees of freedom of the particle
+ * only"; a boundary does not appear in the mobility matrix).  Wall k is the
+ * plane {x : n_k . x = h_k}, n_k a unit vector pointing into the fluid.
+ * walls: HOST array n_walls x 4 = (nx, ny, nz, h); n_walls <= SC_MAX_WALLS
+ * (0 removes them).  Applies to every later build_contacts / collision_step /
+ * time_step call on this context.  Wall-particle constraint l has
+ * cj[l] = n + k (sorted after the particle pairs of body ci[l]), normal n_k
+ * (from the wall to the particle), and
+ *   spheres: gap = (n_k . c_i - h_k) - a_i, contact iff gap < gap_abs + gap_rel * a_i;
+ *   rods:    P = c_i + s t_i, s = -L/2 if n_k.t_i > 0, +L/2 if < 0, 0 if = 0 (the
+ *            axis point nearest the wall); gap = (n_k . P - h_k) - b, contact iff
+ *            gap < gap_thresh; lever r_i = P - c_i, r_j = 0.
+ * Evaluated without FMA contraction (bit-identical to the plain definition).
+ * The D column carries +n_k (and r_i x n_k) on body i only; the wall is at rest.
+ * Errors: SC_EINVAL (n_walls out of range, NULL walls, |n_k| != 1 beyond 1e-12). */
+#define SC_MAX_WALLS 8
+int sc_set_walls(sc_ctx* ctx, int n_walls, const double* walls);
+
 /* ---------------------------------------------------- (a1) build_contacts */
 /* Spheres.  Stores the bodies in the context and computes the near set
  * A(C, delta) = { (i,j) : Phi_ij < delta_ij } with

@@ -76,6 +76,8 @@ def _declare(L):
     L.orc_contacts_spheres_grid.argtypes = [i64, vp, vp, d, d, i64, vp, vp, vp, vp]
     L.orc_contacts_rods.restype = i64
     L.orc_contacts_rods.argtypes = [i64, vp, vp, vp, d, d, C.c_int, i64, vp, vp, vp, vp, vp]
+    L.orc_contacts_walls.restype = i64
+    L.orc_contacts_walls.argtypes = [C.c_int, i64, vp, vp, vp, vp, d, C.c_int, vp, d, d, i64, vp, vp, vp, vp, vp]
     L.orc_segment_closest.restype = None
     L.orc_segment_closest.argtypes = [vp, vp, d, vp, vp, d, vp, vp]
     L.orc_apply_D.argtypes = [i64, i64, vp, vp, vp, vp, vp, vp]
@@ -155,6 +157,31 @@ def contacts_rods(center, direction, length, b, gap_thresh, brute=False):
             return Contacts(ci[:nc].copy(), cj[:nc].copy(), gap[:nc].copy(), nrm[:nc].copy(),
                             lev[:nc].copy())
         cap = nc
+
+
+def contacts_walls(kind, pos, walls, radius=None, direction=None, length=None, b=0.5, gap_abs=0.0,
+                   gap_rel=0.1):
+    """Particle-wall constraints (i, n + k) in body order (oracle.c orc_contacts_walls)."""
+    pos, walls = _f64(pos), _f64(walls)
+    radius, direction, length = _f64(radius), _f64(direction), _f64(length)
+    n, nw = pos.shape[0], walls.shape[0]
+    rods = kind == "rods"
+    cap = max(16, n * nw)
+    ci = np.empty(cap, np.int32); cj = np.empty(cap, np.int32)
+    gap = np.empty(cap); nrm = np.empty((cap, 3)); lev = np.empty((cap, 2, 3))
+    m = _check(lib().orc_contacts_walls(int(rods), n, _p(pos), _p(radius), _p(direction), _p(length), float(b),
+                                        nw, _p(walls), float(gap_abs), float(gap_rel), cap, _p(ci), _p(cj),
+                                        _p(gap), _p(nrm), _p(lev) if rods else None), "contacts_walls")
+    return Contacts(ci[:m].copy(), cj[:m].copy(), gap[:m].copy(), nrm[:m].copy(), lev[:m].copy() if rods else None)
+
+
+def merge_contacts(a: Contacts, b: Contacts) -> Contacts:
+    """Union of two constraint lists, sorted by (i, j) (walls j = n + k sort last per i)."""
+    ci = np.concatenate([a.i, b.i]); cj = np.concatenate([a.j, b.j])
+    order = np.lexsort((cj, ci))
+    lev = None if a.lever is None else np.concatenate([a.lever, b.lever])[order]
+    return Contacts(ci[order], cj[order], np.concatenate([a.gap, b.gap])[order],
+                    np.concatenate([a.normal, b.normal])[order], lev)
 
 
 def segment_closest(c1, t1, L1, c2, t2, L2):
@@ -311,11 +338,20 @@ def time_step(problem, quat=None, max_iter=None, warm=None):
 
 # ------------------------------------------------------ one-call pipeline
 def system_for(problem, method="grid"):
-    """Contacts + System for a synthetic ``Problem`` (spheres or rods)."""
+    """Contacts (+ wall constraints, if the problem has walls) + System for a synthetic
+    ``Problem`` (spheres or rods)."""
+    walls = getattr(problem, "walls", None)
     if problem.kind == "spheres":
         ct = contacts_spheres(problem.pos, problem.radius, problem.gap_abs, problem.gap_rel, method)
+        if walls is not None and len(walls):
+            ct = merge_contacts(ct, contacts_walls("spheres", problem.pos, walls, radius=problem.radius,
+                                                   gap_abs=problem.gap_abs, gap_rel=problem.gap_rel))
         return System(ORC_SPHERES, problem.n, ct, mu=problem.mu, pos=problem.pos, radius=problem.radius)
     ct = contacts_rods(problem.pos, problem.direction, problem.length, problem.rod_radius, problem.gap_abs)
+    if walls is not None and len(walls):
+        ct = merge_contacts(ct, contacts_walls("rods", problem.pos, walls, direction=problem.direction,
+                                               length=problem.length, b=problem.rod_radius,
+                                               gap_abs=problem.gap_abs))
     return System(ORC_RODS, problem.n, ct, mu=problem.mu, direction=problem.direction,
                   length=problem.length, b=problem.rod_radius)
 

@@ -346,6 +346,68 @@ int64_t orc_contacts_rods(int64_t n, const double* center, const double* dir, co
 }
 
 /* ------------------------------------------------------------------------ */
+/* Particle-boundary collisions (NEXT row f2): "for each       */
+/* collision pair l between a particle and a boundary, a vector D_l can be  */
+/* added to D ... these D_l column vectors have 6 non-zero entries          */
+/* corresponding to the degrees of freedom of the particle only"; a         */
+/* boundary "does not appear in the mobility matrix".  Boundaries here are  */
+/* static planes n_k . x = h_k (unit n_k into the fluid).  Constraint       */
+/* (i, n + k); normal n_k (from the wall to the particle, reading A13's     */
+/* "from j to i").  Minimal separation of the particle and plane:  */
+/*   sphere: Phi = (n . c - h) - a;                                         */
+/*   rod: the axis segment's signed distance n.(c + s t) - h is linear in s */
+/*        on [-L/2, L/2], so its minimum is at s = -L/2 (n.t > 0), +L/2     */
+/*        (n.t < 0), anywhere for n.t = 0 (take s = 0, the centre);         */
+/*        Phi = (n . P - h) - b with P = c + s t, lever r = P - c.          */
+/* Thresholds as for pairs (reading A1): spheres gap_abs + gap_rel * a,     */
+/* rods gap_abs.  Output in body order (i ascending, then k).               */
+/* ------------------------------------------------------------------------ */
+int64_t orc_contacts_walls(int kind, int64_t n, const double* pos, const double* radius, const double* dir,
+                           const double* length, double b, int nw, const double* walls, double gap_abs,
+                           double gap_rel, int64_t cap, int32_t* ci, int32_t* cj, double* gap, double* normal,
+                           double* lever) {
+  if (n < 0 || nw < 0 || (nw > 0 && !walls) || !pos) return -1;
+  if (kind == 1 && (!dir || !length)) return -1;
+  int64_t m = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double* c = pos + 3 * i;
+    for (int k = 0; k < nw; ++k) {
+      const double* w = walls + 4 * k;
+      double P[3] = {c[0], c[1], c[2]};
+      double g, thr;
+      if (kind == 0) {
+        double a = radius ? radius[i] : 1.0;
+        g = (((w[0] * c[0] + w[1] * c[1]) + w[2] * c[2]) - w[3]) - a;
+        thr = gap_abs + gap_rel * a;
+      } else {
+        const double* t = dir + 3 * i;
+        double nt = (w[0] * t[0] + w[1] * t[1]) + w[2] * t[2];
+        double hl = 0.5 * length[i];
+        double sv = nt > 0.0 ? -hl : (nt < 0.0 ? hl : 0.0);
+        for (int d = 0; d < 3; ++d) P[d] = c[d] + sv * t[d];
+        g = (((w[0] * P[0] + w[1] * P[1]) + w[2] * P[2]) - w[3]) - b;
+        thr = gap_abs;
+      }
+      if (!(g < thr)) continue;
+      if (m < cap) {
+        ci[m] = (int32_t)i;
+        cj[m] = (int32_t)(n + k);
+        gap[m] = g;
+        for (int d = 0; d < 3; ++d) normal[3 * m + d] = w[d];
+        if (lever) {
+          for (int d = 0; d < 3; ++d) {
+            lever[6 * m + d] = P[d] - c[d];
+            lever[6 * m + 3 + d] = 0.0;
+          }
+        }
+      }
+      ++m;
+    }
+  }
+  return m;
+}
+
+/* ------------------------------------------------------------------------ */
 /* D and D^T.  Column l: on body i (+n, r_i x n), on body j   */
 /* (-n, -(r_j x n)); spheres carry no torque.                 */
 /* ------------------------------------------------------------------------ */
@@ -371,14 +433,15 @@ int orc_apply_D(int64_t n, int64_t nc, const int32_t* ci, const int32_t* cj, con
                 const double* lever, const double* gamma, double* FT) {
   if (n < 0 || nc < 0) return -1;
   memset(FT, 0, sizeof(double) * 6 * (size_t)n);
-  /* F_c = D gamma, accumulated in ascending constraint order. */
+  /* F_c = D gamma, accumulated in ascending constraint order.
+   * cj >= n: a wall (entries on the particle only). */
   for (int64_t l = 0; l < nc; ++l) {
-    if (ci[l] < 0 || cj[l] < 0 || ci[l] >= n || cj[l] >= n) return -1;
+    if (ci[l] < 0 || cj[l] < 0 || ci[l] >= n || cj[l] >= n + ORC_MAX_WALLS) return -1;
     double Di[6], Dj[6];
     column_blocks(normal, lever, l, Di, Dj);
     for (int k = 0; k < 6; ++k) {
       FT[6 * (int64_t)ci[l] + k] += Di[k] * gamma[l];
-      FT[6 * (int64_t)cj[l] + k] += Dj[k] * gamma[l];
+      if (cj[l] < n) FT[6 * (int64_t)cj[l] + k] += Dj[k] * gamma[l];
     }
   }
   return 0;
@@ -388,12 +451,13 @@ int orc_apply_DT(int64_t n, int64_t nc, const int32_t* ci, const int32_t* cj, co
                  const double* lever, const double* UW, double* out) {
   if (n < 0 || nc < 0) return -1;
   for (int64_t l = 0; l < nc; ++l) {
-    if (ci[l] < 0 || cj[l] < 0 || ci[l] >= n || cj[l] >= n) return -1;
+    if (ci[l] < 0 || cj[l] < 0 || ci[l] >= n || cj[l] >= n + ORC_MAX_WALLS) return -1;
     double Di[6], Dj[6];
     column_blocks(normal, lever, l, Di, Dj);
     double s = 0.0;
     for (int k = 0; k < 6; ++k) s += Di[k] * UW[6 * (int64_t)ci[l] + k];
-    for (int k = 0; k < 6; ++k) s += Dj[k] * UW[6 * (int64_t)cj[l] + k];
+    if (cj[l] < n)  /* a wall is at rest */
+      for (int k = 0; k < 6; ++k) s += Dj[k] * UW[6 * (int64_t)cj[l] + k];
     out[l] = s;
   }
   return 0;

@@ -46,7 +46,19 @@ void orc_segment_closest(const double* c1, const double* t1, double L1,
                          const double* c2, const double* t2, double L2,
                          double* P1, double* P2);
 
+/* ---- particle-boundary constraints (NEXT row f2) ---- */
+/* Static planes n_k . x = h_k (walls: nw x 4 = (nx, ny, nz, h), unit n into the fluid).
+ * kind 0 spheres (radius may be NULL: 1), 1 rods (dir, length, radius b).  Emits
+ * (i, n + k) in body order with gap, normal n_k and (rods, lever != NULL) r_i = P - c_i,
+ * r_j = 0.  Thresholds: spheres gap_abs + gap_rel * a_i, rods gap_abs (strict '<'). */
+#define ORC_MAX_WALLS 8
+int64_t orc_contacts_walls(int kind, int64_t n, const double* pos, const double* radius, const double* dir,
+                           const double* length, double b, int nw, const double* walls, double gap_abs,
+                           double gap_rel, int64_t cap, int32_t* ci, int32_t* cj, double* gap, double* normal,
+                           double* lever);
+
 /* ---- collision matrix D and its transpose ---- */
+/* cj >= n marks a wall constraint (entries on body ci only). */
 /* lever == NULL: sphere columns (6 nnz); else rod columns (12 nnz). */
 int orc_apply_D(int64_t n, int64_t nc, const int32_t* ci, const int32_t* cj, const double* normal,
                 const double* lever, const double* gamma, double* FT /* n x 6 */);

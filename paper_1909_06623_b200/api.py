@@ -104,6 +104,18 @@ class Context:
     def _dev(self, shape, dtype=None):
         return torch.empty(shape, dtype=dtype or torch.float64, device=f"cuda:{self.device}")
 
+    # ------------------------------------------------------- NEXT row f2
+    def set_walls(self, walls):
+        """Static planar walls n.x = h (rows (nx, ny, nz, h), unit n into the fluid) for every
+        later contact build on this context; wall k appears as body n + k in the constraint
+        list (include/stokescol.h sc_set_walls).  walls=None or empty removes them."""
+        import numpy as np
+        w = np.ascontiguousarray(np.zeros((0, 4)) if walls is None else np.asarray(walls, dtype=np.float64))
+        if w.ndim != 2 or w.shape[1] != 4:
+            raise ValueError("walls must be k x 4")
+        self._rc(self.lib.sc_set_walls(self._h, int(w.shape[0]), w.ctypes.data if w.size else None))
+        self._walls = w
+
     # ------------------------------------------------------------- (a1)
     def build_contacts_spheres(self, pos, radius=None, gap_abs=0.0, gap_rel=0.1) -> int:
         n = int(pos.shape[0])

@@ -384,7 +384,8 @@ __global__ static void pair_keys_kernel(const int32_t* __restrict__ ci, const in
                                         double* __restrict__ gcopy) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (l >= nc) return;
-  key[l] = static_cast<int64_t>(ci[l]) * n + cj[l];  // ascending: constraints are sorted by (i, j)
+  // ascending: constraints are sorted by (i, j); j < n + SC_MAX_WALLS (walls are n + k)
+  key[l] = static_cast<int64_t>(ci[l]) * (n + SC_MAX_WALLS) + cj[l];
   gcopy[l] = gam[l];
 }
 
@@ -393,7 +394,7 @@ __global__ static void warm_match_kernel(const int32_t* __restrict__ ci, const i
                                          const double* __restrict__ pgam, int64_t pnc, double* __restrict__ gam0) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (l >= nc) return;
-  const int64_t k = static_cast<int64_t>(ci[l]) * n + cj[l];
+  const int64_t k = static_cast<int64_t>(ci[l]) * (n + SC_MAX_WALLS) + cj[l];
   int64_t lo = 0, hi = pnc;  // binary search in the previous (sorted) key list
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
@@ -546,6 +547,25 @@ int sc_plan_partition(int64_t n, int world, int rank, int64_t* out7) {
   out7[4] = lo / kChunkBodies;
   out7[5] = hi / kChunkBodies;
   out7[6] = choose_nsplit(npad, world);
+  return SC_OK;
+}
+
+// ------------------------------------------------------------ NEXT row f2: walls
+int sc_set_walls(sc_ctx* ctx, int n_walls, const double* walls) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (n_walls < 0 || n_walls > SC_MAX_WALLS || (n_walls > 0 && walls == nullptr))
+    return fail(ctx, SC_EINVAL, "set_walls: 0 <= n_walls <= SC_MAX_WALLS and walls != NULL");
+  for (int k = 0; k < n_walls; ++k) {
+    const double* w = walls + 4 * k;
+    const double nn = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
+    if (!(std::isfinite(w[3]) && std::fabs(nn - 1.0) <= 1e-12))
+      return fail(ctx, SC_EINVAL, "set_walls: normals must be unit vectors and offsets finite");
+  }
+  ctx->nwalls = n_walls;
+  for (int k = 0; k < SC_MAX_WALLS; ++k)
+    ctx->walls[k] = k < n_walls ? make_double4(walls[4 * k], walls[4 * k + 1], walls[4 * k + 2], walls[4 * k + 3])
+                                : make_double4(0, 0, 0, 0);
+  ctx->prev_nc = 0;  // the constraint numbering changes: no warm start across this call
   return SC_OK;
 }
 

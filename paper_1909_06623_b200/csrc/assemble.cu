@@ -16,19 +16,19 @@ constexpr int kT = 256;
 inline unsigned nblk(int64_t n) { return static_cast<unsigned>((n + kT - 1) / kT); }
 
 __global__ void degree_count(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, int64_t nc,
-                             int32_t* __restrict__ deg) {
+                             int64_t n, int32_t* __restrict__ deg) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (l >= nc) return;
   atomicAdd(&deg[ci[l]], 1);
-  atomicAdd(&deg[cj[l]], 1);
+  if (cj[l] < n) atomicAdd(&deg[cj[l]], 1);  // cj >= n: a wall (no column entries, NEXT row f2)
 }
 
 __global__ void incidence_fill(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, int64_t nc,
-                               int32_t* __restrict__ cursor, int32_t* __restrict__ inc) {
+                               int64_t n, int32_t* __restrict__ cursor, int32_t* __restrict__ inc) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (l >= nc) return;
   inc[atomicAdd(&cursor[ci[l]], 1)] = static_cast<int32_t>(l << 1);
-  inc[atomicAdd(&cursor[cj[l]], 1)] = static_cast<int32_t>((l << 1) | 1);
+  if (cj[l] < n) inc[atomicAdd(&cursor[cj[l]], 1)] = static_cast<int32_t>((l << 1) | 1);
 }
 
 __global__ void incidence_sort(const int32_t* __restrict__ row_ptr, int64_t n, int32_t* __restrict__ inc) {
@@ -49,10 +49,11 @@ __global__ void incidence_sort(const int32_t* __restrict__ row_ptr, int64_t n, i
 // Signed D_l block of every incidence, in incidence (per-body) order, so the spheres'
 // D-gather streams it: sigma n, sigma = +1 on i, -1 on j.
 template <int KIND>
-__global__ void incidence_columns(const int32_t* __restrict__ inc, int64_t ninc, const double4* __restrict__ nrm4,
+__global__ void incidence_columns(const int32_t* __restrict__ inc, const int32_t* __restrict__ ninc_dev, int64_t ninc,
+                                  const double4* __restrict__ nrm4,
                                   const double4* __restrict__ /*rxn4*/, double4* __restrict__ icol4) {
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= ninc) return;
+  if (e >= ninc || e >= *ninc_dev) return;  // row_ptr[n] = 2 n_c - (wall constraints)
   const int32_t v = inc[e];
   const int32_t l = v >> 1;
   const int side = v & 1;
@@ -86,7 +87,7 @@ int assemble(sc_ctx* ctx) {
   SC_CUDA(cudaMemsetAsync(deg, 0, sizeof(int32_t) * (n + 1), ctx->stream));
   if (nc > 0) {
     timer_begin(ctx, SC_K_ASSEMBLE);
-    degree_count<<<nblk(nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, nc, deg);
+    degree_count<<<nblk(nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, nc, n, deg);
     timer_end(ctx, SC_K_ASSEMBLE);
     if (int rc = check_launch(ctx, "degree_count")) return rc;
   }
@@ -95,7 +96,7 @@ int assemble(sc_ctx* ctx) {
     int32_t* cursor = ctx->cell_cnt.p;
     SC_CUDA(cudaMemcpyAsync(cursor, ctx->row_ptr.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
     timer_begin(ctx, SC_K_ASSEMBLE);
-    incidence_fill<<<nblk(nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, nc, cursor, ctx->inc.p);
+    incidence_fill<<<nblk(nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, nc, n, cursor, ctx->inc.p);
     timer_end(ctx, SC_K_ASSEMBLE);
     if (int rc = check_launch(ctx, "incidence_fill")) return rc;
     timer_begin(ctx, SC_K_ASSEMBLE);
@@ -113,7 +114,7 @@ int assemble(sc_ctx* ctx) {
       const int64_t ninc = 2 * nc;
       if (int rc = ensure(ctx, ctx->icol4, ninc)) return rc;
       timer_begin(ctx, SC_K_ASSEMBLE);
-      incidence_columns<kSpheres><<<nblk(ninc), kT, 0, ctx->stream>>>(ctx->inc.p, ninc, ctx->nrm4.p, nullptr,
+      incidence_columns<kSpheres><<<nblk(ninc), kT, 0, ctx->stream>>>(ctx->inc.p, ctx->row_ptr.p + n, ninc, ctx->nrm4.p, nullptr,
                                                                       ctx->icol4.p);
       timer_end(ctx, SC_K_ASSEMBLE);
       if (int rc = check_launch(ctx, "incidence_columns")) return rc;

@@ -201,12 +201,52 @@ struct RodTest {
   }
 };
 
+// ------------------------------------------------------------------ walls
+// NEXT row f2: particle-boundary collisions.  A wall is the static plane
+// {x : n.x = h} (unit n pointing into the fluid); it is not in the mobility matrix, so its
+// constraint column has entries on the particle only.  Constraint (i, n + k) for wall k:
+//   spheres: Phi = (n.c_i - h) - a_i,  contact iff Phi < gap_abs + gap_rel * a_i
+//   rods:    the axis point closest to the wall, P = c + s t with s = -L/2 (n.t > 0),
+//            +L/2 (n.t < 0), 0 (n.t = 0: parallel, the centre); Phi = (n.P - h) - b,
+//            contact iff Phi < gap_thresh; lever arm r_i = P - c_i
+// with the normal n (from the wall to the particle), evaluated without FMA contraction
+// (fixed association, like the pair tests: bit-identical to the oracle).
+struct WallSet {
+  int nw;
+  double4 w[SC_MAX_WALLS];  // (nx, ny, nz, h)
+};
+
+__device__ __forceinline__ double wall_dot_rn(const double4& w, double x, double y, double z) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(w.x, x), __dmul_rn(w.y, y)), __dmul_rn(w.z, z));
+}
+
+// returns the contact decision; gap and (rods) the closest axis point P
+template <int KIND>
+__device__ __forceinline__ bool wall_test(const double4& c, const double4& t, const double4& w, const SphereTest& st,
+                                          const RodTest& rt, double& gap, double (&P)[3]) {
+  if (KIND == kSpheres) {
+    const double a = 2.0 * c.w;  // exact: w = a/2
+    gap = __dsub_rn(__dsub_rn(wall_dot_rn(w, c.x, c.y, c.z), w.w), a);
+    P[0] = c.x; P[1] = c.y; P[2] = c.z;
+    return gap < __dadd_rn(st.gap_abs, __dmul_rn(st.gap_rel, a));
+  } else {
+    const double nt = wall_dot_rn(w, t.x, t.y, t.z);
+    const double hl = 0.5 * c.w;  // exact
+    const double s = nt > 0.0 ? -hl : (nt < 0.0 ? hl : 0.0);
+    P[0] = __dadd_rn(c.x, __dmul_rn(s, t.x));
+    P[1] = __dadd_rn(c.y, __dmul_rn(s, t.y));
+    P[2] = __dadd_rn(c.z, __dmul_rn(s, t.z));
+    gap = __dsub_rn(__dsub_rn(wall_dot_rn(w, P[0], P[1], P[2]), w.w), 0.5 * rt.b2);
+    return gap < rt.thresh;
+  }
+}
+
 // Pass 1 (count) / pass 2 (emit j's), one thread per cell-sorted body.
 template <int KIND, bool EMIT>
 __global__ void pair_search(const double4* __restrict__ s4, const double4* __restrict__ sd4,
                             const int32_t* __restrict__ sidx, const int32_t* __restrict__ cell_start,
-                            int64_t n, Grid g, SphereTest st, RodTest rt, int32_t* __restrict__ cnt,
-                            const int32_t* __restrict__ off, int32_t* __restrict__ ci,
+                            int64_t n, Grid g, SphereTest st, RodTest rt, WallSet walls,
+                            int32_t* __restrict__ cnt, const int32_t* __restrict__ off, int32_t* __restrict__ ci,
                             int32_t* __restrict__ cj) {
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= n) return;
@@ -246,6 +286,18 @@ __global__ void pair_search(const double4* __restrict__ s4, const double4* __res
         }
       }
     }
+  for (int k = 0; k < walls.nw; ++k) {  // wall k is "body" n + k (sorts after every particle)
+    double gap, P[3];
+    if (wall_test<KIND>(pi, ti, walls.w[k], st, rt, gap, P)) {
+      if (EMIT) {
+        ci[o] = i;
+        cj[o] = static_cast<int32_t>(n + k);
+        ++o;
+      } else {
+        ++count;
+      }
+    }
+  }
   if (!EMIT) cnt[i] = count;
 }
 
@@ -303,10 +355,18 @@ __global__ void sort_partners(const int32_t* __restrict__ off, int64_t n, int32_
 }
 
 __global__ void sphere_geometry(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, int64_t nc,
-                                const double4* __restrict__ p, SphereTest st, double4* __restrict__ nrm4,
-                                int32_t* __restrict__ err) {
+                                int64_t n, const double4* __restrict__ p, SphereTest st, WallSet walls,
+                                double4* __restrict__ nrm4, int32_t* __restrict__ err) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (l >= nc) return;
+  if (cj[l] >= n) {  // wall constraint: the wall normal
+    const double4 w = walls.w[cj[l] - n];
+    double gap, P[3];
+    RodTest rt{0, 0, 0};
+    wall_test<kSpheres>(p[ci[l]], make_double4(0, 0, 0, 0), w, st, rt, gap, P);
+    nrm4[l] = make_double4(w.x, w.y, w.z, gap);
+    return;
+  }
   double dx, dy, dz, r, gap;
   st(p[ci[l]], p[cj[l]], dx, dy, dz, r, gap);
   if (r == 0.0) {
@@ -317,12 +377,23 @@ __global__ void sphere_geometry(const int32_t* __restrict__ ci, const int32_t* _
   nrm4[l] = make_double4(__ddiv_rn(dx, r), __ddiv_rn(dy, r), __ddiv_rn(dz, r), gap);
 }
 
-__global__ void rod_geometry(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, int64_t nc,
+__global__ void rod_geometry(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, int64_t nc, int64_t n,
                              const double4* __restrict__ c4, const double4* __restrict__ d4, RodTest rt,
-                             double4* __restrict__ nrm4, double4* __restrict__ lev4, int32_t* __restrict__ err) {
+                             WallSet walls, double4* __restrict__ nrm4, double4* __restrict__ lev4,
+                             int32_t* __restrict__ err) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (l >= nc) return;
   const int32_t i = ci[l], j = cj[l];
+  if (j >= n) {  // wall constraint: normal n_w, lever arm P - c_i on the rod, none on the wall
+    const double4 w = walls.w[j - n], pi = c4[i];
+    double gap, P[3];
+    SphereTest st{0, 0};
+    wall_test<kRods>(pi, d4[i], w, st, rt, gap, P);
+    nrm4[l] = make_double4(w.x, w.y, w.z, gap);
+    lev4[2 * l] = make_double4(__dsub_rn(P[0], pi.x), __dsub_rn(P[1], pi.y), __dsub_rn(P[2], pi.z), 0.0);
+    lev4[2 * l + 1] = make_double4(0.0, 0.0, 0.0, 0.0);
+    return;
+  }
   const double4 pi = c4[i], pj = c4[j], ti = d4[i], tj = d4[j];
   RodPair rp;
   double dist, gap;
@@ -361,6 +432,9 @@ __global__ void rod_geometry(const int32_t* __restrict__ ci, const int32_t* __re
 inline unsigned nblk(int64_t n, int t = kT) { return static_cast<unsigned>((n + t - 1) / t); }
 
 int build_common(sc_ctx* ctx, SphereTest st, RodTest rt) {
+  WallSet walls;
+  walls.nw = ctx->nwalls;
+  for (int k = 0; k < SC_MAX_WALLS; ++k) walls.w[k] = ctx->walls[k];
   const int64_t n = ctx->n;
   const int kind = ctx->kind;
   ctx->nc = 0;
@@ -439,11 +513,11 @@ int build_common(sc_ctx* ctx, SphereTest st, RodTest rt) {
   timer_begin(ctx, SC_K_CONTACTS);
   if (kind == kSpheres)
     pair_search<kSpheres, false><<<nblk(n), kT, 0, ctx->stream>>>(
-        ctx->sorted4.p, nullptr, ctx->sorted_idx.p, ctx->cell_start.p, n, g, st, rt, ctx->pair_cnt.p, nullptr,
+        ctx->sorted4.p, nullptr, ctx->sorted_idx.p, ctx->cell_start.p, n, g, st, rt, walls, ctx->pair_cnt.p, nullptr,
         nullptr, nullptr);
   else
     pair_search<kRods, false><<<nblk(n), kT, 0, ctx->stream>>>(
-        ctx->sorted4.p, ctx->sorted_dir4.p, ctx->sorted_idx.p, ctx->cell_start.p, n, g, st, rt,
+        ctx->sorted4.p, ctx->sorted_dir4.p, ctx->sorted_idx.p, ctx->cell_start.p, n, g, st, rt, walls,
         ctx->pair_cnt.p, nullptr, nullptr, nullptr);
   timer_end(ctx, SC_K_CONTACTS);
   if (int rc = check_launch(ctx, "pair_count")) return rc;
@@ -466,11 +540,11 @@ int build_common(sc_ctx* ctx, SphereTest st, RodTest rt) {
     timer_begin(ctx, SC_K_CONTACTS);
     if (kind == kSpheres)
       pair_search<kSpheres, true><<<nblk(n), kT, 0, ctx->stream>>>(
-          ctx->sorted4.p, nullptr, ctx->sorted_idx.p, ctx->cell_start.p, n, g, st, rt, nullptr,
+          ctx->sorted4.p, nullptr, ctx->sorted_idx.p, ctx->cell_start.p, n, g, st, rt, walls, nullptr,
           ctx->first_ptr.p, ctx->ci.p, ctx->cj.p);
     else
       pair_search<kRods, true><<<nblk(n), kT, 0, ctx->stream>>>(
-          ctx->sorted4.p, ctx->sorted_dir4.p, ctx->sorted_idx.p, ctx->cell_start.p, n, g, st, rt, nullptr,
+          ctx->sorted4.p, ctx->sorted_dir4.p, ctx->sorted_idx.p, ctx->cell_start.p, n, g, st, rt, walls, nullptr,
           ctx->first_ptr.p, ctx->ci.p, ctx->cj.p);
     timer_end(ctx, SC_K_CONTACTS);
     if (int rc = check_launch(ctx, "pair_emit")) return rc;
@@ -480,11 +554,11 @@ int build_common(sc_ctx* ctx, SphereTest st, RodTest rt) {
     if (int rc = check_launch(ctx, "sort_partners")) return rc;
     timer_begin(ctx, SC_K_CONTACTS);
     if (kind == kSpheres)
-      sphere_geometry<<<nblk(nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, nc, ctx->pos4.p, st, ctx->nrm4.p,
-                                                         ctx->derr);
+      sphere_geometry<<<nblk(nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, nc, n, ctx->pos4.p, st, walls,
+                                                         ctx->nrm4.p, ctx->derr);
     else
-      rod_geometry<<<nblk(nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, nc, ctx->pos4.p, ctx->dir4.p, rt,
-                                                      ctx->nrm4.p, ctx->lev4.p, ctx->derr);
+      rod_geometry<<<nblk(nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, nc, n, ctx->pos4.p, ctx->dir4.p, rt,
+                                                      walls, ctx->nrm4.p, ctx->lev4.p, ctx->derr);
     timer_end(ctx, SC_K_CONTACTS);
     if (int rc = check_launch(ctx, "geometry")) return rc;
   }

@@ -218,12 +218,15 @@ __global__ void __launch_bounds__(kR) dt_kernel(
     double v = 0.0;
     if (MODE != kDtInitQ) {
       const int32_t i = ci[l], j = cj[l];
+      const bool wall = j >= n;  // a wall (NEXT row f2): static, not in the mobility
       const double4 nv = nrm4[l];
+      const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
       if (KIND == kSpheres) {
-        const double4 ui = u4[i], uj = u4[j];
+        const double4 ui = u4[i], uj = wall ? z4 : u4[j];
         v = fma(nv.z, ui.z - uj.z, fma(nv.y, ui.y - uj.y, nv.x * (ui.x - uj.x)));
       } else {
-        const double4 ui = u4[2 * i], uj = u4[2 * j], wi = u4[2 * i + 1], wj = u4[2 * j + 1];
+        const double4 ui = u4[2 * i], wi = u4[2 * i + 1];
+        const double4 uj = wall ? z4 : u4[2 * j], wj = wall ? z4 : u4[2 * j + 1];
         const double4 ra = rxn4[2 * l], rb = rxn4[2 * l + 1];
         v = fma(nv.z, ui.z - uj.z, fma(nv.y, ui.y - uj.y, nv.x * (ui.x - uj.x)));
         v += fma(ra.z, wi.z, fma(ra.y, wi.y, ra.x * wi.x)) - fma(rb.z, wj.z, fma(rb.y, wj.y, rb.x * wj.x));
@@ -347,12 +350,13 @@ __global__ void rod_unpack_kernel(const double4* __restrict__ u4, int64_t n, dou
 template <int KIND>
 __global__ void dt_user_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj,
                                const double4* __restrict__ nrm4, const double4* __restrict__ rxn4,
-                               const double* __restrict__ UW, int64_t nc, int addgap, double inv_dt,
+                               const double* __restrict__ UW, int64_t nc, int64_t n, int addgap, double inv_dt,
                                double* __restrict__ out) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (l >= nc) return;
+  const double zero6[6] = {0, 0, 0, 0, 0, 0};
   const double* ui = UW + 6 * static_cast<int64_t>(ci[l]);
-  const double* uj = UW + 6 * static_cast<int64_t>(cj[l]);
+  const double* uj = cj[l] < n ? UW + 6 * static_cast<int64_t>(cj[l]) : zero6;  // cj >= n: a wall
   const double4 nv = nrm4[l];
   double v = nv.x * (ui[0] - uj[0]) + nv.y * (ui[1] - uj[1]) + nv.z * (ui[2] - uj[2]);
   if (KIND == kRods) {
@@ -519,10 +523,10 @@ int launch_dt_user(sc_ctx* ctx, const double* UW, double* out, const double* add
   timer_begin(ctx, SC_K_DT);
   if (ctx->kind == kSpheres)
     dt_user_kernel<kSpheres><<<nblk(ctx->nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, ctx->nrm4.p, nullptr,
-                                                                     UW, ctx->nc, addgap, qscale, out);
+                                                                     UW, ctx->nc, ctx->n, addgap, qscale, out);
   else
     dt_user_kernel<kRods><<<nblk(ctx->nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, ctx->nrm4.p,
-                                                                  ctx->rxn4.p, UW, ctx->nc, addgap, qscale, out);
+                                                                  ctx->rxn4.p, UW, ctx->nc, ctx->n, addgap, qscale, out);
   timer_end(ctx, SC_K_DT);
   return check_launch(ctx, "dt_user");
 }

@@ -77,6 +77,8 @@ struct sc_ctx {
   int poly = 0;                 // spheres: radii not all equal
   double a_const = 1.0;
   double rod_b = 0.5;
+  int nwalls = 0;               // NEXT row f2: static planar walls (sc_set_walls)
+  double4 walls[SC_MAX_WALLS] = {};  // (nx, ny, nz, h): plane n.x = h, unit n into the fluid
   sc::DBuf<double4> pos4;       // spheres: (x,y,z,a/2); rods: (x,y,z,L)
   sc::DBuf<double4> dir4;       // rods: (tx,ty,tz,0)
   sc::DBuf<double4> rodmob4;    // rods: (1/zeta_par, 1/zeta_perp, 1/zeta_rot, mu) for rod_mu

@@ -56,6 +56,7 @@ class Problem:
     fixed_iters: int          # >0: run exactly this many iterations (C5 timing mode)
     box: float
     monodisperse: bool
+    walls: np.ndarray | None = None  # (k,4) planes n.x = h, unit n into the fluid (NEXT row f2)
 
     def nbytes_inputs(self) -> int:
         arrs = [self.pos, self.radius, self.direction, self.length, self.force]
@@ -73,9 +74,24 @@ CONFIGS = {
 _SEED = {"C1": 1, "C2": 2, "C3": 3, "C4": 4, "C5": 5}
 
 
+def make_walls(kind: str | None, box: float) -> np.ndarray | None:
+    """Static planar boundaries (NEXT row f2): "floor" = the plane z = 0 (the
+    bottom face of the placement cube, normal +z); "box" = the six faces of [0, box]^3 with
+    inward normals.  Centres are drawn inside the cube, so bodies near a face overlap it."""
+    if kind is None:
+        return None
+    if kind == "floor":
+        return np.array([[0.0, 0.0, 1.0, 0.0]])
+    if kind == "box":
+        return np.array([[1.0, 0.0, 0.0, 0.0], [-1.0, 0.0, 0.0, -box], [0.0, 1.0, 0.0, 0.0],
+                         [0.0, -1.0, 0.0, -box], [0.0, 0.0, 1.0, 0.0], [0.0, 0.0, -1.0, -box]])
+    raise ValueError(f"unknown walls {kind!r}")
+
+
 def make_problem(name: str, n: int | None = None, seed: int | None = None,
-                 fixed_iters: int | None = None) -> Problem:
-    """Draw the seeded synthetic instance of config ``name`` (C1..C5)."""
+                 fixed_iters: int | None = None, walls: str | None = None) -> Problem:
+    """Draw the seeded synthetic instance of config ``name`` (C1..C5); ``walls`` adds the
+    static planes of :func:`make_walls` (no extra random draws)."""
     kind, n_full, phi, dt, gap_abs, gap_rel, jmax, fixed = CONFIGS[name]
     n = n_full if n is None else int(n)
     rng = np.random.default_rng(_SEED[name] if seed is None else seed)
@@ -115,4 +131,4 @@ def make_problem(name: str, n: int | None = None, seed: int | None = None,
                    force=force, mu=1.0, dt=dt, gap_abs=gap_abs, gap_rel=gap_rel,
                    tol=1e-8, max_iter=jmax,
                    fixed_iters=fixed if fixed_iters is None else fixed_iters,
-                   box=box, monodisperse=mono)
+                   box=box, monodisperse=mono, walls=make_walls(walls, box))
