@@ -58,12 +58,13 @@ def load(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("SC_LIB") or LIB_PATH  # SC_LIB: tuning A/B of another build of this library
+    if not os.path.exists(path):
         if not build_if_missing:
             raise RuntimeError(f"libstokescol.so not built at {LIB_PATH}")
         from . import build as _build
         _build.build()
-    lib = C.CDLL(LIB_PATH)
+    lib = C.CDLL(path)
     vp, i64, i32, d, ci = C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_int
     pp = C.POINTER(C.c_void_p)
     sig = {
