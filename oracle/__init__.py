@@ -25,7 +25,7 @@ _HDR = os.path.join(_HERE, "oracle.h")
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
-ORC_SPHERES, ORC_RODS = 0, 1
+ORC_SPHERES, ORC_RODS, ORC_SPHERES_RPY6 = 0, 1, 2
 
 
 def build(force: bool = False) -> str:
@@ -87,6 +87,9 @@ def _declare(L):
     L.orc_rpy_block.restype = None
     L.orc_rpy_block.argtypes = [vp, d, vp, d, d, C.c_int, vp]
     L.orc_rod_drag_apply.argtypes = [i64, vp, vp, d, d, vp, vp]
+    L.orc_rpy6_block.restype = None
+    L.orc_rpy6_block.argtypes = [vp, d, vp, d, d, C.c_int, vp]
+    L.orc_rpy6_apply_rows.argtypes = [i64, vp, vp, d, vp, i64, i64, vp]
     L.orc_lcp_q.argtypes = [C.POINTER(_Sys), vp, d, vp, vp]
     L.orc_mvop.argtypes = [C.POINTER(_Sys), vp, vp]
     L.orc_bbpgd.argtypes = [C.POINTER(_Sys), vp, d, i32, i32, i32, vp, vp, vp, vp, C.POINTER(Stats)]
@@ -186,8 +189,8 @@ def merge_contacts(a: Contacts, b: Contacts) -> Contacts:
 
 def segment_closest(c1, t1, L1, c2, t2, L2):
     P1 = np.empty(3); P2 = np.empty(3)
-    lib().orc_segment_closest(_p(_f64(c1)), _p(_f64(t1)), float(L1), _p(_f64(c2)), _p(_f64(t2)),
-                              float(L2), _p(P1), _p(P2))
+    c1, t1, c2, t2 = _f64(c1), _f64(t1), _f64(c2), _f64(t2)
+    lib().orc_segment_closest(_p(c1), _p(t1), float(L1), _p(c2), _p(t2), float(L2), _p(P1), _p(P2))
     return P1, P2
 
 
@@ -226,8 +229,26 @@ def rpy_apply_rows(pos, radius, mu, FT, row0, row1):
 
 def rpy_block(xi, ai, xj, aj, mu, self_block=False):
     M = np.empty(9)
-    lib().orc_rpy_block(_p(_f64(xi)), float(ai), _p(_f64(xj)), float(aj), float(mu), int(self_block), _p(M))
+    xi, xj = _f64(xi), _f64(xj)  # (keep the converted arrays alive across the call)
+    lib().orc_rpy_block(_p(xi), float(ai), _p(xj), float(aj), float(mu), int(self_block), _p(M))
     return M.reshape(3, 3)
+
+
+def rpy6_apply(pos, radius, mu, FT, row0=0, row1=None):
+    """Full 6N RPY grand mobility (NEXT row f4(ii), oracle.c orc_rpy6_block)."""
+    pos, radius, FT = _f64(pos), _f64(radius), _f64(FT)
+    n = pos.shape[0]
+    row1 = n if row1 is None else row1
+    UW = np.empty((row1 - row0, 6))
+    _check(lib().orc_rpy6_apply_rows(n, _p(pos), _p(radius), mu, _p(FT), row0, row1, _p(UW)), "rpy6_apply")
+    return UW
+
+
+def rpy6_block(xi, ai, xj, aj, mu, self_block=False):
+    M = np.empty(36)
+    xi, xj = _f64(xi), _f64(xj)
+    lib().orc_rpy6_block(_p(xi), float(ai), _p(xj), float(aj), float(mu), int(self_block), _p(M))
+    return M.reshape(6, 6)
 
 
 def rod_drag_apply(direction, length, b, mu, FT):
@@ -253,6 +274,8 @@ class System:
     def mobility(self, FT):
         if self.kind == ORC_SPHERES:
             return rpy_apply(self.pos, self.radius, self.mu, FT)
+        if self.kind == ORC_SPHERES_RPY6:
+            return rpy6_apply(self.pos, self.radius, self.mu, FT)
         return rod_drag_apply(self.direction, self.length, self.b, self.mu, FT)
 
     def lcp_q(self, dt, U_nc):
@@ -346,7 +369,8 @@ def system_for(problem, method="grid"):
         if walls is not None and len(walls):
             ct = merge_contacts(ct, contacts_walls("spheres", problem.pos, walls, radius=problem.radius,
                                                    gap_abs=problem.gap_abs, gap_rel=problem.gap_rel))
-        return System(ORC_SPHERES, problem.n, ct, mu=problem.mu, pos=problem.pos, radius=problem.radius)
+        kind = ORC_SPHERES_RPY6 if getattr(problem, "mobility", "rpy") == "rpy6" else ORC_SPHERES
+        return System(kind, problem.n, ct, mu=problem.mu, pos=problem.pos, radius=problem.radius)
     ct = contacts_rods(problem.pos, problem.direction, problem.length, problem.rod_radius, problem.gap_abs)
     if walls is not None and len(walls):
         ct = merge_contacts(ct, contacts_walls("rods", problem.pos, walls, direction=problem.direction,

@@ -533,6 +533,87 @@ int orc_rpy_apply(int64_t n, const double* pos, const double* radius, double mu,
   return orc_rpy_apply_rows(n, pos, radius, mu, FT, 0, n, UW);
 }
 
+/* ------------------------------------------------------------------------ */
+/* NEXT row f4(ii): the full 6N RPY grand mobility (reading A27).  The      */
+/* paper cites RPY only and BASELINE specifies the              */
+/* translational blocks; the coupling blocks below restate the RPY          */
+/* literature's expressions for equal spheres (radius a -> abar, reading    */
+/* A11), with r = x_i - x_j, rhat = r / |r|, [v]x w = v x w:                */
+/*   rt (Omega_i from F_j) and tr (U_i from T_j):  -c(r) [rhat]x,           */
+/*     c = 1/(8 pi mu r^2)                             r >= 2a              */
+/*     c = (1/(16 pi mu a^2)) (r/a - 3 r^2/(8 a^2))    r <  2a              */
+/*   rr (Omega_i from T_j):                                                 */
+/*     (1/(16 pi mu r^3)) (3 rhat rhat^T - I)          r >= 2a              */
+/*     (1/(8 pi mu a^3)) [(1 - 27r/(32a) + 5r^3/(64a^3)) I                  */
+/*                        + (9r/(32a) - 3r^3/(64a^3)) rhat rhat^T]   r < 2a */
+/* Far field: rt = 1/2 curl of the translational (Stokeslet + degenerate    */
+/* quadrupole) field, rr = 1/2 curl of the rotlet; the branches join C^1 at */
+/* r = 2a and reduce to the self blocks (0 and I/(8 pi mu a^3)) at r = 0.   */
+/* Self: tt I/(6 pi mu a_i), rr I/(8 pi mu a_i^3), tr = rt = 0.             */
+/* M66 row-major: [[tt, tr], [rt, rr]] maps (F_j, T_j) to (U_i, Omega_i).   */
+/* ------------------------------------------------------------------------ */
+void orc_rpy6_block(const double* xi, double ai, const double* xj, double aj, double mu, int self,
+                    double* M66) {
+  double tt[9];
+  orc_rpy_block(xi, ai, xj, aj, mu, self, tt);
+  for (int k = 0; k < 36; ++k) M66[k] = 0.0;
+  for (int p = 0; p < 3; ++p)
+    for (int q = 0; q < 3; ++q) M66[6 * p + q] = tt[3 * p + q];
+  if (self) {
+    double s = 1.0 / (8.0 * ORC_PI * mu * ai * ai * ai);
+    for (int p = 0; p < 3; ++p) M66[6 * (3 + p) + 3 + p] = s;
+    return;
+  }
+  double rv[3] = {xi[0] - xj[0], xi[1] - xj[1], xi[2] - xj[2]};
+  double r = sqrt(rv[0] * rv[0] + rv[1] * rv[1] + rv[2] * rv[2]);
+  double e[3] = {rv[0] / r, rv[1] / r, rv[2] / r};
+  double a = 0.5 * (ai + aj);
+  double c, cI, cR;
+  if (r >= 2.0 * a) {
+    c = 1.0 / (8.0 * ORC_PI * mu * r * r);
+    cI = -1.0 / (16.0 * ORC_PI * mu * r * r * r);
+    cR = 3.0 / (16.0 * ORC_PI * mu * r * r * r);
+  } else {
+    c = (1.0 / (16.0 * ORC_PI * mu * a * a)) * (r / a - 3.0 * r * r / (8.0 * a * a));
+    cI = (1.0 / (8.0 * ORC_PI * mu * a * a * a)) * (1.0 - 27.0 * r / (32.0 * a) + 5.0 * r * r * r / (64.0 * a * a * a));
+    cR = (1.0 / (8.0 * ORC_PI * mu * a * a * a)) * (9.0 * r / (32.0 * a) - 3.0 * r * r * r / (64.0 * a * a * a));
+  }
+  /* [e]x as a matrix: [[0,-e2,e1],[e2,0,-e0],[-e1,e0,0]]; the blocks are -c [e]x */
+  double X[9] = {0.0, -e[2], e[1], e[2], 0.0, -e[0], -e[1], e[0], 0.0};
+  for (int p = 0; p < 3; ++p)
+    for (int q = 0; q < 3; ++q) {
+      M66[6 * p + 3 + q] = -c * X[3 * p + q];        /* tr */
+      M66[6 * (3 + p) + q] = -c * X[3 * p + q];      /* rt */
+      M66[6 * (3 + p) + 3 + q] = cI * (p == q ? 1.0 : 0.0) + cR * e[p] * e[q];  /* rr */
+    }
+}
+
+static int rpy6_row(int64_t n, const double* pos, const double* radius, double mu, const double* FT,
+                    int64_t i, double* out6) {
+  long double acc[6] = {0.0L, 0.0L, 0.0L, 0.0L, 0.0L, 0.0L};
+  double M[36];
+  for (int64_t j = 0; j < n; ++j) {
+    if (j != i && pos[3 * i] == pos[3 * j] && pos[3 * i + 1] == pos[3 * j + 1] && pos[3 * i + 2] == pos[3 * j + 2])
+      return -2; /* coincident centres (reading A12) */
+    orc_rpy6_block(pos + 3 * i, radius[i], pos + 3 * j, radius[j], mu, j == i, M);
+    for (int p = 0; p < 6; ++p)
+      for (int q = 0; q < 6; ++q) acc[p] += (long double)M[6 * p + q] * (long double)FT[6 * j + q];
+  }
+  for (int p = 0; p < 6; ++p) out6[p] = (double)acc[p];
+  return 0;
+}
+
+int orc_rpy6_apply_rows(int64_t n, const double* pos, const double* radius, double mu, const double* FT,
+                        int64_t row0, int64_t row1, double* UW_rows) {
+  if (n < 0 || row0 < 0 || row1 > n || row0 > row1 || !(mu > 0)) return -1;
+  int bad = 0;
+#pragma omp parallel for schedule(dynamic, 4) reduction(| : bad)
+  for (int64_t i = row0; i < row1; ++i) {
+    if (rpy6_row(n, pos, radius, mu, FT, i, UW_rows + 6 * (i - row0)) != 0) bad = 1;
+  }
+  return bad ? -2 : 0;
+}
+
 /* Spherocylinder drag, B:configs[3]:
  *   U = (1/zeta_par) t t^T F + (1/zeta_perp) (I - t t^T) F,
  *   zeta_perp = 2 zeta_par = 4 pi mu L / ln(L/(2b)),
@@ -565,6 +646,7 @@ int orc_rod_drag_apply(int64_t n, const double* dir, const double* length, doubl
 
 static int mobility(const orc_system* s, const double* FT, double* UW) {
   if (s->kind == 0) return orc_rpy_apply(s->n, s->pos, s->radius, s->mu, FT, UW);
+  if (s->kind == 2) return orc_rpy6_apply_rows(s->n, s->pos, s->radius, s->mu, FT, 0, s->n, UW);
   return orc_rod_drag_apply(s->n, s->dir, s->length, s->b, s->mu, FT, UW);
 }
 

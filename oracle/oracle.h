@@ -76,13 +76,20 @@ int orc_rpy_apply_rows(int64_t n, const double* pos, const double* radius, doubl
 /* The 3x3 translational block M_ij (i != j) or M_ii, as printed in B:configs[0]. */
 void orc_rpy_block(const double* xi, double ai, const double* xj, double aj, double mu, int self,
                    double* M33);
+/* NEXT row f4(ii): the full 6N RPY grand mobility (reading A27): translation-rotation and
+ * rotation-rotation pair blocks added to orc_rpy_block's; M66 row-major [[tt, tr], [rt, rr]]
+ * maps (F_j, T_j) to (U_i, Omega_i).  Sums in long double. */
+void orc_rpy6_block(const double* xi, double ai, const double* xj, double aj, double mu, int self,
+                    double* M66);
+int orc_rpy6_apply_rows(int64_t n, const double* pos, const double* radius, double mu, const double* FT,
+                        int64_t row0, int64_t row1, double* UW_rows);
 /* Block-diagonal spherocylinder drag (B:configs[3]). */
 int orc_rod_drag_apply(int64_t n, const double* dir, const double* length, double b, double mu,
                        const double* FT, double* UW);
 
 /* ---- LCP setup and BBPGD (Alg. 1) ---- */
 typedef struct {
-  int kind;               /* 0 spheres RPY, 1 rods drag */
+  int kind;               /* 0 spheres RPY, 1 rods drag, 2 spheres full 6N RPY (f4(ii)) */
   int64_t n;
   const double* pos;      /* spheres */
   const double* radius;   /* spheres */

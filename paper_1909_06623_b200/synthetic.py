@@ -57,6 +57,7 @@ class Problem:
     box: float
     monodisperse: bool
     walls: np.ndarray | None = None  # (k,4) planes n.x = h, unit n into the fluid (NEXT row f2)
+    mobility: str = "rpy"            # "rpy" (BASELINE) or "rpy6" (full grand mobility, NEXT row f4(ii))
 
     def nbytes_inputs(self) -> int:
         arrs = [self.pos, self.radius, self.direction, self.length, self.force]
