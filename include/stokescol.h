@@ -134,6 +134,23 @@ int sc_mobility_apply(sc_ctx* ctx, double mu, const double* FT, double* UW);
  * sc_bbpgd_solve; q_out (n_c) may be NULL. */
 int sc_lcp_q(sc_ctx* ctx, double dt, const double* U_nc, double* q_out);
 
+/* ------------------------------- NEXT row f4(ii): the full 6N RPY mobility */
+/* model 0 (default): the mobility of BASELINE.json configs[0]/[1] -- translational RPY pair
+ * blocks plus the self rotation T/(8 pi mu a^3).  model 1: the full RPY grand mobility, adding
+ * the translation-rotation and rotation-rotation pair blocks (reading A27; r = x_i - x_j,
+ * rhat = r/|r|, abar = (a_i + a_j)/2):
+ *   Omega_i from F_j and U_i from T_j: -c [rhat]x,
+ *     c = 1/(8 pi mu r^2) (r >= 2 abar), (1/(16 pi mu abar^2))(r/abar - 3 r^2/(8 abar^2)) (r < 2 abar);
+ *   Omega_i from T_j: (1/(16 pi mu r^3))(3 rhat rhat^T - I) (r >= 2 abar),
+ *     (1/(8 pi mu abar^3))[(1 - 27r/(32 abar) + 5r^3/(64 abar^3)) I
+ *                          + (9r/(32 abar) - 3r^3/(64 abar^3)) rhat rhat^T] (r < 2 abar).
+ * Spheres only (rods keep their drag).  With model 1, sc_mobility_apply (hence U_ext in
+ * sc_collision_step / sc_time_step) and the U_c output of sc_bbpgd_solve use the full
+ * mobility; the LCP iteration itself is unchanged (sphere columns of D carry no torque, so
+ * D^T M D only involves the translational blocks).  On a multi-GPU context every rank
+ * evaluates all rows of this apply.  Errors: SC_EINVAL for another model. */
+int sc_set_mobility_model(sc_ctx* ctx, int model);
+
 /* ------------------------------------------------------ (a6) bbpgd_solve */
 typedef struct {
   double mu;            /* viscosity used by every MVOP */

@@ -116,6 +116,13 @@ class Context:
         self._rc(self.lib.sc_set_walls(self._h, int(w.shape[0]), w.ctypes.data if w.size else None))
         self._walls = w
 
+    # --------------------------------------------------- NEXT row f4(ii)
+    def set_mobility_model(self, model):
+        """"rpy" (BASELINE: translational RPY + self rotation) or "rpy6" (full 6N RPY grand
+        mobility with the translation-rotation and rotation-rotation pair blocks)."""
+        m = {"rpy": 0, "rpy6": 1}[model] if isinstance(model, str) else int(model)
+        self._rc(self.lib.sc_set_mobility_model(self._h, m))
+
     # ------------------------------------------------------------- (a1)
     def build_contacts_spheres(self, pos, radius=None, gap_abs=0.0, gap_rel=0.1) -> int:
         n = int(pos.shape[0])

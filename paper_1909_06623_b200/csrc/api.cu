@@ -513,7 +513,7 @@ void sc_destroy(sc_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   release(ctx->pos4); release(ctx->dir4); release(ctx->rodmob4);
   release(ctx->ci); release(ctx->cj); release(ctx->nrm4); release(ctx->lev4); release(ctx->rxn4);
-  release(ctx->row_ptr); release(ctx->inc); release(ctx->icol4); release(ctx->first_ptr); release(ctx->near_ptr); release(ctx->near_idx);
+  release(ctx->rpy6_part); release(ctx->ft_tmp); release(ctx->row_ptr); release(ctx->inc); release(ctx->icol4); release(ctx->first_ptr); release(ctx->near_ptr); release(ctx->near_idx);
   release(ctx->q); release(ctx->gam[0]); release(ctx->gam[1]); release(ctx->g[0]); release(ctx->g[1]);
   release(ctx->w); release(ctx->gam_user); release(ctx->uc); release(ctx->prev_key); release(ctx->prev_gam); release(ctx->chunk_part); release(ctx->chunk_red);
   release(ctx->sym_pairs); release(ctx->upart); release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);
@@ -547,6 +547,14 @@ int sc_plan_partition(int64_t n, int world, int rank, int64_t* out7) {
   out7[4] = lo / kChunkBodies;
   out7[5] = hi / kChunkBodies;
   out7[6] = choose_nsplit(npad, world);
+  return SC_OK;
+}
+
+// ------------------------------------------------------------ NEXT row f4(ii)
+int sc_set_mobility_model(sc_ctx* ctx, int model) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (model != 0 && model != 1) return fail(ctx, SC_EINVAL, "set_mobility_model: 0 (RPY) or 1 (full 6N RPY)");
+  ctx->mobility_model = model;
   return SC_OK;
 }
 
@@ -754,7 +762,11 @@ int sc_mobility_apply(sc_ctx* ctx, double mu, const double* FT, double* UW) {
   double* dU = nullptr;
   if (int rc = st.in(FT, 6 * ctx->n, &dF)) return rc;
   if (int rc = st.out(UW, 6 * ctx->n, &dU)) return rc;
-  if (ctx->kind == kSpheres) {
+  if (ctx->kind == kSpheres && ctx->mobility_model == 1) {  // full grand mobility (every rank: all rows)
+    if (int rc = launch_pack_ft(ctx, dF, ctx->f4.p, ctx->t4.p)) return rc;
+    if (int rc = rpy6_apply(ctx, ctx->f4.p, ctx->t4.p, mu, dU)) return rc;
+    if (int rc = check_flag(ctx, SC_EDEGENERATE, "coincident centres in the RPY sum")) return rc;
+  } else if (ctx->kind == kSpheres) {
     if (int rc = launch_pack_ft(ctx, dF, ctx->f4.p, ctx->t4.p)) return rc;
     Dist D(ctx);
     if (int rc = D.rpy(mu, nullptr)) return rc;
@@ -985,7 +997,12 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     if (stt.iters == 0 && stt.mvops >= 2) {  // j_max = 0: u4 holds the alpha_0 product, recompute
       if (int rc = mvop_raw(gfin)) return rc;
     }
-    if (spheres) {
+    if (spheres && ctx->mobility_model == 1) {  // U_c = M D gamma with the coupling blocks (Omega_c)
+      if (int rc = ensure(ctx, ctx->ft_tmp, 6 * n)) return rc;
+      if (int rc = launch_gather_raw(ctx, gfin, mu, ctx->ft_tmp.p)) return rc;
+      if (int rc = launch_pack_ft(ctx, ctx->ft_tmp.p, ctx->f4.p, ctx->t4.p)) return rc;
+      if (int rc = rpy6_apply(ctx, ctx->f4.p, ctx->t4.p, mu, dU)) return rc;
+    } else if (spheres) {
       if (int rc = launch_unpack_uw_spheres(ctx, ctx->u4.p, nullptr, mu, dU)) return rc;
     } else {
       if (int rc = launch_rod_unpack(ctx, ctx->u4.p, dU)) return rc;

@@ -113,6 +113,9 @@ struct sc_ctx {
   sc::DBuf<double4> t4;         // torques for the public mobility apply [npad]
   sc::DBuf<double4> u4;         // velocities (Ux,Uy,Uz,0) [npad] (spheres) or [2*npad] (rods: U, W)
   sc::DBuf<double> rpy_part;    // nsplit * rows * 3
+  int mobility_model = 0;       // 0: BASELINE RPY (tt + self rotation); 1: full 6N RPY (NEXT row f4(ii))
+  sc::DBuf<double> rpy6_part;   // full RPY: nsplit * npad * 6 partials
+  sc::DBuf<double> ft_tmp;      // n x 6 scratch (F_c for the full-RPY U_c)
   int nsplit = 1;
   int rpy_mode = 0;             // 0 auto, 1 target-row kernel, 2 symmetric pair-tile kernel
   bool use_graphs = true;       // CUDA-graph replay of small-problem iteration batches (env SC_NO_GRAPHS=1: off)
@@ -190,6 +193,8 @@ int assemble(sc_ctx* ctx);
 int rpy_apply_rows(sc_ctx* ctx, const double4* f4, int64_t row0, int64_t nrows, double mu,
                    double4* u4, const int32_t* done);
 int choose_nsplit(int64_t npad, int world);
+// NEXT row f4(ii): UW (n x 6, device) = full 6N RPY grand mobility of the packed (f4, t4).
+int rpy6_apply(sc_ctx* ctx, const double4* f4, const double4* t4, double mu, double* UW);
 bool rpy_use_sym(const sc_ctx* ctx);
 int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done, int W,
                   const std::vector<int>& ranks, int mode);
