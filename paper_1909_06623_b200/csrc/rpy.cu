@@ -329,7 +329,7 @@ constexpr size_t kSymSmem = 2 * kSymSB * sizeof(double4) + 3 * kSymSB * sizeof(d
 template <bool POLY, int NW, int TPT, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB)
     rpy_sym_kernel(const double4* __restrict__ pos4, const double4* __restrict__ f4, const int2* __restrict__ pairs,
-                   int64_t npad, Consts k, double* __restrict__ part, const int32_t* __restrict__ done) {
+                   int64_t npad, Consts k, double* __restrict__ part, const int32_t* __restrict__ done, int hs) {
   static_assert(NW * TPT * 32 == kSymSB, "super-block size");
   constexpr int kSymThreads = NW * 32;
   if (done != nullptr && *done) return;
@@ -339,11 +339,15 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   double* sacc = reinterpret_cast<double*>(sf + kSymSB);  // SJ reverse accumulators [kSymSB][3]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sacc + 3 * kSymSB);
 
-  const int2 pr = pairs[blockIdx.x];
+  // hs > 1 (small N, one GPU): the CTA takes the source part h of SJ only (16/hs sub-blocks)
+  const int2 pr = pairs[blockIdx.x / hs];
+  const int h = static_cast<int>(blockIdx.x % hs);
+  const int nph = kSymNsub / hs;
   const int64_t SI = pr.x, SJ = pr.y;
   const bool rev = SI != SJ;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  constexpr uint32_t kBytes = kSymSB * sizeof(double4);
+  const uint32_t kBytes = kSymSB / hs * sizeof(double4);
+  const int src0 = h * (kSymSB / hs);  // first source of this part within SJ
   if (tid == 0) {
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -351,8 +355,8 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   __syncthreads();
   if (tid == 0) {
     mbar_expect_tx(bar, 2 * kBytes);
-    tma_load_1d(sp, pos4 + SJ * kSymSB, kBytes, bar);
-    tma_load_1d(sf, f4 + SJ * kSymSB, kBytes, bar);
+    tma_load_1d(sp + src0, pos4 + SJ * kSymSB + src0, kBytes, bar);
+    tma_load_1d(sf + src0, f4 + SJ * kSymSB + src0, kBytes, bar);
   }
   double4 p[TPT];
   double fx[TPT], fy[TPT], fz[TPT], ax[TPT], ay[TPT], az[TPT];
@@ -371,8 +375,8 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   __syncthreads();
 
 #pragma unroll 1
-  for (int ph = 0; ph < kSymNsub; ++ph) {
-    const int cj = (w + ph) & (kSymNsub - 1);
+  for (int ph = 0; ph < nph; ++ph) {
+    const int cj = h * nph + (w + ph) % nph;  // distinct across the 4 warps (nph >= 4)
     const double4* tp = sp + cj * 32;
     const double4* tf = sf + cj * 32;
     double rx = 0.0, ry = 0.0, rz = 0.0;  // accumulator of the source this lane meets
@@ -455,19 +459,19 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       __syncthreads();
     }
   }
-  // forward sums: rows of SI, slot SJ
+  // forward sums: rows of SI, slot (SJ, h)
 #pragma unroll
   for (int m = 0; m < TPT; ++m) {
     const int64_t row = SI * kSymSB + (w + NW * m) * 32 + lane;
-    double* o = part + (SJ * npad + row) * 3;
+    double* o = part + ((SJ * hs + h) * npad + row) * 3;
     o[0] = ax[m];
     o[1] = ay[m];
     o[2] = az[m];
   }
-  if (rev) {  // reverse sums: rows of SJ, slot SI
+  if (rev) {  // reverse sums: rows of part h of SJ, slot (SI, h)
     __syncthreads();
-    double* o = part + (SI * npad + SJ * kSymSB) * 3;
-    for (int q = tid; q < 3 * kSymSB; q += kSymThreads) o[q] = sacc[q];
+    double* o = part + ((SI * hs + h) * npad + SJ * kSymSB + src0) * 3;
+    for (int q = tid; q < 3 * (kSymSB / hs); q += kSymThreads) o[q] = sacc[3 * src0 + q];
   }
 }
 
@@ -629,7 +633,14 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
     ctx->sym_world = W;
     ctx->sym_off = off;
   }
-  if (int rc = ensure(ctx, ctx->rpy_part, static_cast<size_t>(NS) * ctx->npad * 3)) return rc;
+  // small N on one GPU: split every super-block pair's sources in hs parts so the grid fills
+  // 148 SMs x 3 CTAs (slots (partner, part); the unwritten ones are zeroed)
+  int hs = 1;
+  if (mode == 0)
+    while (hs < 4 && (ctx->sym_off[1] - ctx->sym_off[0]) * hs < 3 * 148) hs *= 2;
+  if (int rc = ensure(ctx, ctx->rpy_part, static_cast<size_t>(NS) * hs * ctx->npad * 3)) return rc;
+  if (hs > 1)
+    SC_CUDA(cudaMemsetAsync(ctx->rpy_part.p, 0, sizeof(double) * NS * hs * ctx->npad * 3, ctx->stream));
   const Consts k = make_consts(ctx->a_const);
   static bool attr_set = false;
   if (!attr_set) {
@@ -643,12 +654,12 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
   for (int r : ranks) {
     const int64_t p0 = ctx->sym_off[r], np = ctx->sym_off[r + 1] - p0;
     if (np == 0) continue;
-    const unsigned g = static_cast<unsigned>(np);
+    const unsigned g = static_cast<unsigned>(np * hs);
     const int2* pt = ctx->sym_pairs.p + p0;
     timer_begin(ctx, SC_K_RPY);
 #define SC_SYM(P, NW, TPT, MINB)                                                                   \
   rpy_sym_kernel<P, NW, TPT, MINB><<<g, NW * 32, kSymSmem, ctx->stream>>>(ctx->pos4.p, f4, pt, ctx->npad, k, \
-                                                                         ctx->rpy_part.p, done)
+                                                                         ctx->rpy_part.p, done, hs)
     switch (ctx->sym_variant) {
       case 1: if (ctx->poly) SC_SYM(true, 8, 2, 2); else SC_SYM(false, 8, 2, 2); break;
       case 3: if (ctx->poly) SC_SYM(true, 16, 1, 1); else SC_SYM(false, 16, 1, 1); break;
@@ -661,30 +672,30 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
   const double scale = 1.0 / (8.0 * 3.14159265358979323846 * mu);
   const int64_t npad = ctx->npad;
   const unsigned nb = static_cast<unsigned>((npad + 255) / 256);
-  auto combine = [&](int64_t s0, int64_t s1, double4* out) -> int {
+  auto combine = [&](int64_t s0, int64_t s1, double4* out, int64_t nse) -> int {
     timer_begin(ctx, SC_K_COMBINE);
     if (ctx->poly)
-      rpy_sym_combine_kernel<true><<<nb, 256, 0, ctx->stream>>>(ctx->rpy_part.p, NS, s0, s1, npad, ctx->n, scale,
+      rpy_sym_combine_kernel<true><<<nb, 256, 0, ctx->stream>>>(ctx->rpy_part.p, nse, s0, s1, npad, ctx->n, scale,
                                                                ctx->pos4.p, f4, ctx->near_ptr.p, ctx->near_idx.p,
                                                                out, done, ctx->derr);
     else
-      rpy_sym_combine_kernel<false><<<nb, 256, 0, ctx->stream>>>(ctx->rpy_part.p, NS, s0, s1, npad, ctx->n, scale,
+      rpy_sym_combine_kernel<false><<<nb, 256, 0, ctx->stream>>>(ctx->rpy_part.p, nse, s0, s1, npad, ctx->n, scale,
                                                                 ctx->pos4.p, f4, ctx->near_ptr.p, ctx->near_idx.p,
                                                                 out, done, ctx->derr);
     timer_end(ctx, SC_K_COMBINE);
     return check_launch(ctx, "rpy_sym_combine");
   };
-  if (mode == 0) return combine(0, NS, u4);
+  if (mode == 0) return combine(0, NS * hs, u4, NS * hs);  // (all slots, in order)
   if (mode == 2) {
     int64_t a0, a1;
     sym_rank_range(NS, W, ranks.front(), &a0, &a1);
-    return combine(a0, a1, u4);
+    return combine(a0, a1, u4, NS);
   }
   if (int rc = ensure(ctx, ctx->upart, static_cast<size_t>(W) * npad)) return rc;
   for (int r = 0; r < W; ++r) {
     int64_t a0, a1;
     sym_rank_range(NS, W, r, &a0, &a1);
-    if (int rc = combine(a0, a1, ctx->upart.p + r * npad)) return rc;
+    if (int rc = combine(a0, a1, ctx->upart.p + r * npad, NS)) return rc;
   }
   timer_begin(ctx, SC_K_COMBINE);
   sum_ranks_kernel<<<nb, 256, 0, ctx->stream>>>(ctx->upart.p, W, npad, u4, done);
