@@ -157,7 +157,7 @@ def run_reference(args, rank, world):
 def _config(args, world):
     return {"workload": f"{WORKLOAD}: 262,144 monodisperse spheres a=1, volume fraction 0.3, RPY all-pairs, "
                         f"F_ext ~ N(0,1)^3, dt=0.005, contacts gap<0.1a, BBPGD BB1 fixed {FIXED_ITERS} iterations",
-            "n_bodies": 262144, "bbpgd_iters": FIXED_ITERS, "parallelism": f"rpy-rows{world}",
+            "n_bodies": 262144, "bbpgd_iters": FIXED_ITERS, "parallelism": f"rpy-sym-pair-tiles-x{world}",
             "l2": "flushed between steps (256 MiB write on the library stream)",
             "step": "build_contacts+assemble_D+U_ext+q+bbpgd_solve (one sc_collision_step call)"}
 
