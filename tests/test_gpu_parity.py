@@ -336,6 +336,30 @@ def test_c3_full_size_converged_certificate(ctx):
         assert min(gam[l], go) > -1e-8 and (gam[l] == 0 or abs(go) < 1e-7 * (1 + gam[l]))
 
 
+def test_c5_full_size_converged_certificate(ctx):
+    """C5 at full size (262,144 spheres) solved to convergence (~500 iterations, ~45 s): a
+    converged oracle run is hours, so the GPU's gamma is certified by the oracle's RPY rows on
+    sampled constraints (half of them active): g_l = n.(U_i - U_j) + gap_l/dt with
+    U = RPY(F_ext + D gamma) matches the GPU's g, and min(gamma_l, g_l) ~ 0."""
+    p = make_problem("C5", fixed_iters=0)
+    r = _gpu_solve(ctx, p)
+    assert r["status"] == 0 and r["converged"] == 1 and r["residual"] < 1e-8
+    gam = _np(r["gamma"])
+    assert gam.min() >= 0.0
+    ct = oracle.contacts_spheres(p.pos, p.radius, p.gap_abs, p.gap_rel)
+    F = oracle.apply_D(p.n, ct, gam) + p.force
+    rng = np.random.default_rng(11)
+    ls = np.concatenate([rng.choice(np.flatnonzero(gam > 0), 12, replace=False), rng.choice(ct.nc, 12, replace=False)])
+    g = _np(r["g"])
+    for l in ls:
+        i, j = ct.i[l], ct.j[l]
+        ui = oracle.rpy_apply_rows(p.pos, p.radius, p.mu, F, i, i + 1)[0]
+        uj = oracle.rpy_apply_rows(p.pos, p.radius, p.mu, F, j, j + 1)[0]
+        go = float(np.dot(ct.normal[l], ui[:3] - uj[:3])) + ct.gap[l] / p.dt
+        assert abs(g[l] - go) <= 1e-8 * (1 + abs(go)), (l, g[l], go)
+        assert abs(min(gam[l], go)) < 1e-9, (l, gam[l], go)
+
+
 # ---------------------------------------------------------------- NEXT row f1: time stepping
 @pytest.mark.parametrize("name,n,steps", [("C1", None, 3), ("C2", 1500, 2), ("C4", 8000, 2)])
 def test_time_steps_vs_oracle(ctx, name, n, steps):
