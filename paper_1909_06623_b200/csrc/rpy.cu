@@ -480,8 +480,16 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 bool rpy_use_sym(const sc_ctx* ctx) {
   if (ctx->rpy_mode == 1) return false;
   if (ctx->rpy_mode == 2) return true;
-  // auto: enough super-blocks to fill the machine
-  return ctx->npad >= 8 * kSymSB;
+  // auto: enough super-blocks to fill the machine, and the per-(partner, row) slots
+  // (NS x npad x 24 B: 3.2 GB at N = 262,144, growing as N^2) within a quarter of the HBM
+  if (ctx->npad < 8 * kSymSB) return false;
+  static size_t total_b = 0;  // device memory, queried once (cudaMemGetInfo is not free)
+  if (total_b == 0) {
+    size_t free_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) total_b = size_t(1) << 40;
+  }
+  const double slot_bytes = static_cast<double>(ctx->npad / kSymSB) * ctx->npad * 3 * sizeof(double);
+  return slot_bytes <= 0.25 * static_cast<double>(total_b);
 }
 
 // Cyclic-half assignment of super-block pairs: super-block S evaluates (S, S) and
