@@ -285,8 +285,10 @@ __global__ void set_spheres_kernel(const double* __restrict__ pos, const double*
   if (b >= npad) return;
   if (b < n) {
     const double a = radius ? radius[b] : a_const;
-    if (!(a > 0.0) || !isfinite(a)) atomicExch(bad, 1);
-    pos4[b] = make_double4(pos[3 * b], pos[3 * b + 1], pos[3 * b + 2], 0.5 * a);
+    if (!(a > 0.0) || !isfinite(a)) atomicOr(bad, 1);
+    const double x = pos[3 * b], y = pos[3 * b + 1], z = pos[3 * b + 2];
+    if (!(isfinite(x) && isfinite(y) && isfinite(z))) atomicOr(bad, 2);  // NaN/Inf centre
+    pos4[b] = make_double4(x, y, z, 0.5 * a);
   } else {
     // padded rows: far away, distinct, zero force (never coincide with anything)
     pos4[b] = make_double4(1e30 + static_cast<double>(b - n) * 1e20, 1e30, 1e30, 0.5 * a_const);
@@ -306,9 +308,15 @@ __global__ void set_rods_kernel(const double* __restrict__ c, const double* __re
   if (k >= npad) return;
   if (k < n) {
     const double l = L[k];
-    if (!(l > 2.0 * b) || !isfinite(l)) atomicExch(bad, 1);  // drag needs ln(L/2b) > 0
-    pos4[k] = make_double4(c[3 * k], c[3 * k + 1], c[3 * k + 2], l);
-    dir4[k] = make_double4(d[3 * k], d[3 * k + 1], d[3 * k + 2], 0.0);
+    if (!(l > 2.0 * b) || !isfinite(l)) atomicOr(bad, 1);  // drag needs ln(L/2b) > 0
+    const double x = c[3 * k], y = c[3 * k + 1], z = c[3 * k + 2];
+    const double tx = d[3 * k], ty = d[3 * k + 1], tz = d[3 * k + 2];
+    if (!(isfinite(x) && isfinite(y) && isfinite(z) && isfinite(tx) && isfinite(ty) && isfinite(tz)))
+      atomicOr(bad, 2);
+    else if (!(fabs(tx * tx + ty * ty + tz * tz - 1.0) <= 1e-8))
+      atomicOr(bad, 1);  // axes must be unit vectors
+    pos4[k] = make_double4(x, y, z, l);
+    dir4[k] = make_double4(tx, ty, tz, 0.0);
   } else {
     pos4[k] = make_double4(1e30 + static_cast<double>(k - n) * 1e20, 1e30, 1e30, 1.0);
     dir4[k] = make_double4(1, 0, 0, 0);
@@ -350,6 +358,21 @@ static int prepare_bodies(sc_ctx* ctx, int kind, int64_t n) {
   if (kind == kRods) {
     if (int rc = ensure(ctx, ctx->dir4, ctx->npad)) return rc;
     if (int rc = ensure(ctx, ctx->rodmob4, ctx->npad)) return rc;
+  }
+  return 0;
+}
+
+// Body-input flags of set_spheres/set_rods: bit 1 -> non-finite coordinates (SC_ENONFINITE),
+// bit 0 -> invalid radius / length / axis (SC_EINVAL, msg).
+static int check_body_flags(sc_ctx* ctx, const char* msg) {
+  SC_CUDA(cudaMemcpyAsync(ctx->herr, ctx->derr, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int32_t f = *ctx->herr;
+  if (f) {
+    SC_CUDA(cudaMemsetAsync(ctx->derr, 0, sizeof(int32_t), ctx->stream));
+    *ctx->herr = 0;
+    if (f & 2) return fail(ctx, SC_ENONFINITE, "non-finite body coordinates or axes");
+    return fail(ctx, SC_EINVAL, msg);
   }
   return 0;
 }
@@ -596,7 +619,7 @@ int sc_build_contacts_spheres(sc_ctx* ctx, int64_t n, const double* pos, const d
       dpos, drad, n, ctx->npad, 1.0, ctx->pos4.p, ctx->derr);
   timer_end(ctx, SC_K_MISC);
   if (int rc = check_launch(ctx, "set_spheres")) return rc;
-  if (int rc = check_flag(ctx, SC_EINVAL, "radii must be positive and finite")) return rc;
+  if (int rc = check_body_flags(ctx, "radii must be positive and finite")) return rc;
   // monodisperse fast path when all radii are equal
   ctx->poly = 0;
   ctx->a_const = 1.0;
@@ -644,7 +667,7 @@ int sc_build_contacts_rods(sc_ctx* ctx, int64_t n, const double* center, const d
       dc, dd, dl, n, ctx->npad, b, ctx->pos4.p, ctx->dir4.p, ctx->derr);
   timer_end(ctx, SC_K_MISC);
   if (int rc = check_launch(ctx, "set_rods")) return rc;
-  if (int rc = check_flag(ctx, SC_EINVAL, "rod lengths must exceed 2b (ln(L/2b) > 0)")) return rc;
+  if (int rc = check_body_flags(ctx, "rod lengths must exceed 2b (ln(L/2b) > 0) and axes be unit vectors")) return rc;
   if (int rc = build_contacts_rods(ctx, gap_thresh)) return rc;
   if (n_c) *n_c = ctx->nc;
   return SC_OK;
