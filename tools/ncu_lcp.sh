@@ -1,10 +1,15 @@
-# true (non-event-inflated) durations of the LCP kernels, warm L2, for head vs new builds
-for lib in head new; do
-  for c in C4 C5; do
-    if [ $lib = head ]; then export SC_LIB=$PWD/tools/ab/lib_head.so; else unset SC_LIB; fi
-    ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --cache-control none --clock-control none -k regex:"gather|dt_kernel" -s 6 -c 6 --csv python tools/lcp_profile.py $c 10 2>/dev/null | grep -E '"(gpu__time|dram)' | python3 -c "
-import sys,csv
+# true (non-event-inflated) durations of the LCP kernels, warm L2: head build vs D^T CTA shapes
+prof() {  # label, config, env...
+  env "${@:3}" ncu --metrics gpu__time_duration.sum --cache-control none --clock-control none \
+      -k regex:"gather|dt_kernel" -s 6 -c 6 --csv python tools/lcp_profile.py $2 10 2>/dev/null \
+    | grep -E '"gpu__time' | python3 -c "
+import sys,csv,collections
+d=collections.defaultdict(list)
 for r in csv.reader(sys.stdin):
-    print('$lib $c', r[4][:45], r[-3], r[-1])"
-  done
+    d[r[4].split('(')[0].split('::')[-1][:40]].append(float(r[-1]))
+print('$1 $2', {k: round(sum(v)/len(v)/1000,2) for k,v in d.items()})"
+}
+for c in C4 C5; do
+  prof head $c SC_LIB=$PWD/tools/ab/lib_head.so
+  for cfg in 0 1 2 3; do prof cfg$cfg $c SC_DT_CFG=$cfg; done
 done
