@@ -151,6 +151,12 @@ int sc_lcp_q(sc_ctx* ctx, double dt, const double* U_nc, double* q_out);
  * evaluates all rows of this apply.  Errors: SC_EINVAL for another model. */
 int sc_set_mobility_model(sc_ctx* ctx, int model);
 
+/* ------------------------------------------------------- residual (SPEC) */
+/* phi = || min(gamma, g) ||_2, the min-map complementarity residual of the LCP (
+ * BBPGD's convergence measure).  gamma, g: n_c values (host or device); phi: one double
+ * (host or device).  Fixed-order reduction (deterministic).  Errors: SC_EINVAL (NULL, n_c < 0). */
+int sc_minmap_residual(sc_ctx* ctx, int64_t n_c, const double* gamma, const double* g, double* phi);
+
 /* ------------------------------------------------------ (a6) bbpgd_solve */
 typedef struct {
   double mu;            /* viscosity used by every MVOP */

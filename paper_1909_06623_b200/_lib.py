@@ -25,7 +25,7 @@ EXPORTS = [
     "sc_assemble_D", "sc_apply_D", "sc_apply_DT", "sc_mobility_apply", "sc_lcp_q", "sc_bbpgd_solve",
     "sc_collision_step", "sc_set_timing", "sc_get_timing", "sc_reset_timing", "sc_launch_count",
     "sc_plan_partition", "sc_set_emulated_world", "sc_set_rpy_kernel", "sc_time_step", "sc_apgd_solve",
-    "sc_set_walls", "sc_set_mobility_model",
+    "sc_set_walls", "sc_set_mobility_model", "sc_minmap_residual",
 ]
 
 
@@ -95,6 +95,7 @@ def load(build_if_missing: bool = True):
         "sc_set_rpy_kernel": (ci, [vp, ci]),
         "sc_set_walls": (ci, [vp, ci, vp]),
         "sc_set_mobility_model": (ci, [vp, ci]),
+        "sc_minmap_residual": (ci, [vp, i64, vp, vp, vp]),
         "sc_apgd_solve": (ci, [vp, C.POINTER(BbpgdOpts), vp, vp, C.POINTER(BbpgdStats)]),
         "sc_time_step": (ci, [vp, C.POINTER(Problem), C.POINTER(BbpgdOpts), vp, vp, vp, vp, C.POINTER(i64),
                               C.POINTER(BbpgdStats)]),

@@ -55,6 +55,18 @@ def _check_dtype(a, dt):
     return a
 
 
+def _f64(a, shape, what):
+    """dtype float64 and the expected shape (None entries: any); None passes through.  The C ABI
+    takes plain pointers, so a mis-sized buffer must be caught here."""
+    if a is None:
+        return None
+    _check_dtype(a, "f64")
+    got = tuple(a.shape)
+    if len(got) != len(shape) or any(w is not None and g != w for g, w in zip(got, shape)):
+        raise ValueError(f"{what}: expected shape {shape}, got {got}")
+    return a
+
+
 class Context:
     """One sc_ctx (one GPU).  ``world > 1``: NCCL communicator over ranks."""
 
@@ -127,6 +139,7 @@ class Context:
     def build_contacts_spheres(self, pos, radius=None, gap_abs=0.0, gap_rel=0.1) -> int:
         n = int(pos.shape[0])
         nc = C.c_int64()
+        _f64(pos, (n, 3), "pos"); _f64(radius, (n,), "radius")
         self._rc(self.lib.sc_build_contacts_spheres(self._h, n, _ptr(_check_dtype(pos, "f64")),
                                                     _ptr(_check_dtype(radius, "f64")), float(gap_abs),
                                                     float(gap_rel), C.byref(nc)))
@@ -136,6 +149,7 @@ class Context:
     def build_contacts_rods(self, center, direction, length, b, gap_thresh) -> int:
         n = int(center.shape[0])
         nc = C.c_int64()
+        _f64(center, (n, 3), "center"); _f64(direction, (n, 3), "direction"); _f64(length, (n,), "length")
         self._rc(self.lib.sc_build_contacts_rods(self._h, n, _ptr(_check_dtype(center, "f64")),
                                                  _ptr(_check_dtype(direction, "f64")),
                                                  _ptr(_check_dtype(length, "f64")), float(b),
@@ -162,17 +176,20 @@ class Context:
 
     def apply_D(self, gamma, out=None):
         out = self._dev((self.n, 6)) if out is None else out
+        _f64(gamma, (self.nc,), "gamma"); _f64(out, (self.n, 6), "out")
         self._rc(self.lib.sc_apply_D(self._h, _ptr(_check_dtype(gamma, "f64")), _ptr(_check_dtype(out, "f64"))))
         return out
 
     def apply_DT(self, UW, out=None):
         out = self._dev((self.nc,)) if out is None else out
+        _f64(UW, (self.n, 6), "UW"); _f64(out, (self.nc,), "out")
         self._rc(self.lib.sc_apply_DT(self._h, _ptr(_check_dtype(UW, "f64")), _ptr(_check_dtype(out, "f64"))))
         return out
 
     # ------------------------------------------------------------- (a4)
     def mobility_apply(self, FT, mu=1.0, out=None):
         out = self._dev((self.n, 6)) if out is None else out
+        _f64(FT, (self.n, 6), "FT"); _f64(out, (self.n, 6), "out")
         self._rc(self.lib.sc_mobility_apply(self._h, float(mu), _ptr(_check_dtype(FT, "f64")),
                                             _ptr(_check_dtype(out, "f64"))))
         return out
@@ -180,6 +197,7 @@ class Context:
     # ------------------------------------------------------------- q, (a6)
     def lcp_q(self, dt, U_nc, out=None):
         out = self._dev((self.nc,)) if out is None else out
+        _f64(U_nc, (self.n, 6), "U_nc"); _f64(out, (self.nc,), "out")
         self._rc(self.lib.sc_lcp_q(self._h, float(dt), _ptr(_check_dtype(U_nc, "f64")),
                                    _ptr(_check_dtype(out, "f64"))))
         return out
@@ -207,12 +225,15 @@ class Context:
                        fixed_iters=False, Fc_out=None, Uc_out=None):
         """The whole per-step path in one C call (any pointer may be host or device)."""
         n = int(pos.shape[0])
+        _f64(pos, (n, 3), "pos"); _f64(F_ext, (n, 6), "F_ext"); _f64(radius, (n,), "radius")
+        _f64(direction, (n, 3), "direction"); _f64(length, (n,), "length")
         prob = _lib.Problem(0 if kind == "spheres" else 1, 0, n, _ptr(pos), _ptr(radius), _ptr(direction),
                             _ptr(length), float(b), float(gap_abs), float(gap_rel), float(mu), float(dt),
                             _ptr(F_ext))
         opts = _lib.BbpgdOpts(float(mu), float(tol), int(max_iter), int(bb_mode), int(bool(fixed_iters)), 0)
         nc = C.c_int64()
         st = _lib.BbpgdStats()
+        _f64(Fc_out, (n, 6), "Fc_out"); _f64(Uc_out, (n, 6), "Uc_out")
         rc = self._rc(self.lib.sc_collision_step(self._h, C.byref(prob), C.byref(opts), _ptr(Fc_out),
                                                  _ptr(Uc_out), C.byref(nc), C.byref(st)), allow=(0, 1))
         self.n, self.nc, self.kind = n, nc.value, kind
@@ -234,10 +255,13 @@ class Context:
         """One whole time step: returns the next centres (and rod axes),
         updates `quat` (n x 4) in place, and the total velocity U_nc + U_c."""
         n = int(pos.shape[0])
+        _f64(pos, (n, 3), "pos"); _f64(F_ext, (n, 6), "F_ext"); _f64(radius, (n,), "radius")
+        _f64(direction, (n, 3), "direction"); _f64(length, (n,), "length")
         prob = _lib.Problem(0 if kind == "spheres" else 1, 0, n, _ptr(pos), _ptr(radius), _ptr(direction),
                             _ptr(length), float(b), float(gap_abs), float(gap_rel), float(mu), float(dt),
                             _ptr(F_ext))
         opts = _lib.BbpgdOpts(float(mu), float(tol), int(max_iter), int(bb_mode), 0, 2 if warm_start else 0)
+        _f64(quat, (n, 4), "quat")
         pos_out = self._dev((n, 3))
         dir_out = self._dev((n, 3)) if kind == "rods" else None
         U = self._dev((n, 6)) if want_U else None
@@ -248,6 +272,14 @@ class Context:
                       allow=(0, 1))
         self.n, self.nc, self.kind = n, nc.value, kind
         return {"pos": pos_out, "dir": dir_out, "U": U, "status": rc, "nc": nc.value, **st.as_dict()}
+
+    def minmap_residual(self, gamma, g) -> float:
+        """phi = || min(gamma, g) ||_2 on the GPU."""
+        nc = int(gamma.shape[0])
+        _f64(gamma, (nc,), "gamma"); _f64(g, (nc,), "g")
+        out = np.zeros(1)
+        self._rc(self.lib.sc_minmap_residual(self._h, nc, _ptr(gamma), _ptr(g), _ptr(out)))
+        return float(out[0])
 
     # ------------------------------------------------------------- measurement
     def set_timing(self, enable=True):

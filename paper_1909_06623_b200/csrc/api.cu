@@ -573,6 +573,29 @@ int sc_plan_partition(int64_t n, int world, int rank, int64_t* out7) {
   return SC_OK;
 }
 
+// ------------------------------------------------------------ residual
+int sc_minmap_residual(sc_ctx* ctx, int64_t n_c, const double* gamma, const double* g, double* phi) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (n_c < 0 || phi == nullptr || (n_c > 0 && (gamma == nullptr || g == nullptr)))
+    return fail(ctx, SC_EINVAL, "minmap_residual: bad arguments");
+  cudaSetDevice(ctx->device);
+  if (n_c == 0) {
+    *phi = 0.0;
+    return SC_OK;
+  }
+  Stager st(ctx);
+  const double *dg = nullptr, *dgr = nullptr;
+  if (int rc = st.in(gamma, n_c, &dg)) return rc;
+  if (int rc = st.in(g, n_c, &dgr)) return rc;
+  double* dphi = nullptr;
+  if (int rc = st.out(phi, 1, &dphi)) return rc;
+  if (int rc = launch_minmap(ctx, dg, dgr, n_c, dphi)) return rc;
+  if (int rc = st.finish()) return rc;
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (dphi != phi && !std::isfinite(*phi)) return fail(ctx, SC_ENONFINITE, "non-finite residual");  // (host phi)
+  return SC_OK;
+}
+
 // ------------------------------------------------------------ NEXT row f4(ii)
 int sc_set_mobility_model(sc_ctx* ctx, int model) {
   if (ctx == nullptr) return SC_EINVAL;

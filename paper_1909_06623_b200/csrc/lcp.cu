@@ -379,6 +379,25 @@ __global__ void count_active_kernel(const double* __restrict__ gam, int64_t nc, 
   if (threadIdx.x == 0) atomicAdd(out, s);
 }
 
+// phi = || min(gamma, g) ||_2, one CTA, fixed order: thread t sums l = t, t + 1024,
+// ..., then a fixed tree.
+__global__ void __launch_bounds__(1024) minmap_kernel(const double* __restrict__ gam, const double* __restrict__ g,
+                                                      int64_t nc, double* __restrict__ out) {
+  __shared__ double red[1024];
+  double acc = 0.0;
+  for (int64_t l = threadIdx.x; l < nc; l += 1024) {
+    const double m = gam[l] < g[l] ? gam[l] : g[l];
+    acc = fma(m, m, acc);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sqrt(red[0]);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -529,6 +548,13 @@ int launch_dt_user(sc_ctx* ctx, const double* UW, double* out, const double* add
                                                                   ctx->rxn4.p, UW, ctx->nc, ctx->n, addgap, qscale, out);
   timer_end(ctx, SC_K_DT);
   return check_launch(ctx, "dt_user");
+}
+
+int launch_minmap(sc_ctx* ctx, const double* gam, const double* g, int64_t nc, double* out) {
+  timer_begin(ctx, SC_K_MISC);
+  minmap_kernel<<<1, 1024, 0, ctx->stream>>>(gam, g, nc, out);
+  timer_end(ctx, SC_K_MISC);
+  return check_launch(ctx, "minmap");
 }
 
 int launch_count_active(sc_ctx* ctx, const double* gam, int32_t* out) {

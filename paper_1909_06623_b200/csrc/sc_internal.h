@@ -220,6 +220,7 @@ int launch_unpack_uw_spheres(sc_ctx* ctx, const double4* u4, const double4* t4, 
 int launch_rod_drag_user(sc_ctx* ctx, const double* FT, double mu, double* UW);
 int launch_rod_unpack(sc_ctx* ctx, const double4* u4, double* UW);
 int launch_count_active(sc_ctx* ctx, const double* gam, int32_t* out);
+int launch_minmap(sc_ctx* ctx, const double* gam, const double* g, int64_t nc, double* out);
 int launch_q(sc_ctx* ctx, double dt, const double* dtu, double* q);
 
 // ---- APGD comparison solver (apgd.cu) --------------------------------------

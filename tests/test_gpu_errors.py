@@ -34,7 +34,7 @@ def _code(fn):
 
 def test_calls_out_of_order(ctx):
     assert _code(lambda: ctx.assemble_D()) == EINVAL
-    assert _code(lambda: ctx.mobility_apply(_cuda(np.zeros((2, 6))))) == EINVAL
+    assert _code(lambda: ctx.mobility_apply(_cuda(np.zeros((0, 6))))) == EINVAL  # before build_contacts
     pos = np.array([[0.0, 0, 0], [2.05, 0, 0]])
     ctx.build_contacts_spheres(_cuda(pos), None, 0.0, 0.1)
     assert _code(lambda: ctx.bbpgd_solve()) == EINVAL  # needs assemble_D and lcp_q first
@@ -86,3 +86,20 @@ def test_iteration_cap_is_soft(ctx):
     r = ctx.bbpgd_solve(tol=1e-8, max_iter=5)
     assert r["status"] == 1 and r["converged"] == 0 and r["iters"] == 5 and r["mvops"] == 7
     assert float(r["gamma"].min()) >= 0.0 and np.isfinite(r["residual"])
+
+
+def test_minmap_residual_entry_point(ctx):
+    """sc_minmap_residual (SPEC's min_map_residual) equals the solver's phi and numpy's."""
+    p = make_problem("C1", fixed_iters=0)
+    ctx.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+    ctx.assemble_D()
+    ctx.lcp_q(p.dt, ctx.mobility_apply(_cuda(p.force)))
+    r = ctx.bbpgd_solve(tol=p.tol, max_iter=p.max_iter)
+    phi = ctx.minmap_residual(r["gamma"], r["g"])
+    gm, g = r["gamma"].cpu().numpy(), r["g"].cpu().numpy()
+    assert phi == pytest.approx(float(np.linalg.norm(np.minimum(gm, g))), rel=1e-12)
+    assert phi == pytest.approx(r["residual"], rel=1e-10)
+    # host buffers through the same entry point
+    assert ctx.minmap_residual(gm, g) == pytest.approx(phi, rel=1e-15)
+    with pytest.raises(ValueError):
+        ctx.minmap_residual(r["gamma"], r["g"][:-1])
