@@ -269,7 +269,9 @@ int sc_set_emulated_world(sc_ctx* ctx, int world);
  * target-row kernel), 1 = target-row kernel (the multi-GPU sharding unit;
  * bitwise identical for any number of ranks), 2 = symmetric pair-tile kernel
  * (each unordered pair evaluated once).  Both compute the same sum; they differ
- * in rounding only.  Errors: SC_EINVAL for another mode. */
+ * in rounding only.  Mode 0 on one GPU also runs the BBPGD loop of small sphere problems
+ * (padded N <= 2048) as one persistent cooperative kernel; modes 1 and 2 keep
+ * the kernel-per-step path.  Errors: SC_EINVAL for another mode. */
 int sc_set_rpy_kernel(sc_ctx* ctx, int mode);
 
 #ifdef __cplusplus

@@ -493,6 +493,7 @@ static int create_common(sc_ctx** out, int device, void* stream) {
   cudaMemset(ctx->dsc, 0, sizeof(DevScalars));
   if (const char* v = std::getenv("SC_SYM_VARIANT")) ctx->sym_variant = std::atoi(v);
   if (const char* v = std::getenv("SC_NO_GRAPHS")) ctx->use_graphs = std::atoi(v) == 0;
+  if (const char* v = std::getenv("SC_NO_PERSIST")) ctx->use_persist = std::atoi(v) == 0;
   *ctx->herr = 0;
   *out = ctx;
   return SC_OK;
@@ -975,7 +976,12 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     // graph and replayed, removing per-kernel launch gaps.
     cudaGraphExec_t gexec = nullptr;
     int64_t graph_kernels = 0;
-    if (batch >= 4 && !dist && !ctx->timer.enabled && ctx->use_graphs) {
+    const bool persist = !dist && persist_eligible(ctx);
+    if (persist) {  // small problem: the whole loop in one cooperative launch (persist.cu)
+      if (int rc = bbpgd_persistent(ctx, mu)) return rc;
+      if (int rc = read_scalars(ctx)) return rc;
+    }
+    if (!persist && batch >= 4 && !dist && !ctx->timer.enabled && ctx->use_graphs) {
       cudaGraph_t graph = nullptr;
       const int64_t l0 = ctx->launch_count;
       SC_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
@@ -993,7 +999,7 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
       graph_kernels = ctx->launch_count - l0;
       ctx->launch_count = l0;
     }
-    int enq = 0;
+    int enq = persist ? opts->max_iter : 0;
     while (enq < opts->max_iter) {
       int nb = std::min(batch, opts->max_iter - enq);
       if (gexec) {

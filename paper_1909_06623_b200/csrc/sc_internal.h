@@ -21,6 +21,7 @@ constexpr int kRpyTile = 128;           // sources per shared-memory tile
 constexpr int kNpadQuantum = 512;       // npad = N rounded up to this (RPY row blocks and super-blocks)
 constexpr int kChunkBodies = 256;       // B_c: bodies per reduction chunk
 constexpr int kPartials = 4;            // doubles per chunk partial
+constexpr int kPersistMaxBodies = 2048; // persistent single-launch BBPGD loop up to this npad (persist.cu)
 
 enum BodyKind { kNone = -1, kSpheres = 0, kRods = 1 };
 
@@ -118,6 +119,7 @@ struct sc_ctx {
   sc::DBuf<double> ft_tmp;      // n x 6 scratch (F_c for the full-RPY U_c)
   int nsplit = 1;
   int rpy_mode = 0;             // 0 auto, 1 target-row kernel, 2 symmetric pair-tile kernel
+  bool use_persist = true;      // persistent BBPGD loop for small sphere problems (env SC_NO_PERSIST=1: off)
   bool use_graphs = true;       // CUDA-graph replay of small-problem iteration batches (env SC_NO_GRAPHS=1: off)
   int sym_variant = 0;          // tuning: (warps, targets/lane) of the symmetric kernel (env SC_SYM_VARIANT)
   int64_t sym_nsb = -1;         // super-blocks the pair tables were built for
@@ -222,6 +224,10 @@ int launch_rod_unpack(sc_ctx* ctx, const double4* u4, double* UW);
 int launch_count_active(sc_ctx* ctx, const double* gam, int32_t* out);
 int launch_minmap(sc_ctx* ctx, const double* gam, const double* g, int64_t nc, double* out);
 int launch_q(sc_ctx* ctx, double dt, const double* dtu, double* q);
+
+// ---- persistent small-problem BBPGD loop (persist.cu) ------------------------
+bool persist_eligible(const sc_ctx* ctx);
+int bbpgd_persistent(sc_ctx* ctx, double mu);
 
 // ---- APGD comparison solver (apgd.cu) --------------------------------------
 int apgd_launch_step(sc_ctx* ctx, const double* y, const double* g, const double* gam, double t, double* gam_new);

@@ -360,6 +360,38 @@ def test_c5_full_size_converged_certificate(ctx):
         assert abs(min(gam[l], go)) < 1e-9, (l, gam[l], go)
 
 
+@pytest.mark.parametrize("name,n,walls", [("C1", None, None), ("C2", 1500, None), ("C1", None, "box"),
+                                          ("C5", 1800, None)])
+def test_persistent_loop_matches_standard_path(name, n, walls):
+    """Small problems (npad <= 2048) run Steps 7-16 in one cooperative launch (persist.cu); the
+    launch-per-kernel path (SC_NO_PERSIST=1) and the oracle agree with it."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import os
+    p = make_problem(name, n=n, fixed_iters=0, walls=walls)
+    out = {}
+    for label, env in (("persist", "0"), ("standard", "1")):
+        os.environ["SC_NO_PERSIST"] = env
+        try:
+            c = Context(0)
+        finally:
+            os.environ.pop("SC_NO_PERSIST", None)
+        c.set_walls(p.walls)
+        launches0 = c.launch_count()
+        out[label] = (_gpu_solve(c, p), c.launch_count() - launches0)
+        c.close()
+    rp, lp = out["persist"]
+    rs, ls = out["standard"]
+    o = oracle.solve_problem(p)
+    for r in (rp, rs):
+        assert r["status"] == 0 and r["converged"] == 1 and r["residual"] < 1e-8
+        assert _relL2(_np(r["gamma"]), o["gamma"]) <= 1e-6
+        assert _relL2(_np(r["Fc"]), o["Fc"]) <= 1e-6
+        assert _relL2(_np(r["Uc"]), o["Uc"]) <= 1e-6
+    assert abs(rp["iters"] - rs["iters"]) <= max(10, rs["iters"] // 5)
+    assert lp < ls  # one launch for the whole loop
+
+
 # ---------------------------------------------------------------- NEXT row f1: time stepping
 @pytest.mark.parametrize("name,n,steps", [("C1", None, 3), ("C2", 1500, 2), ("C4", 8000, 2)])
 def test_time_steps_vs_oracle(ctx, name, n, steps):
