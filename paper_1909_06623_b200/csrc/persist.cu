@@ -199,7 +199,7 @@ int bbpgd_persistent(sc_ctx* ctx, double mu) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bbpgd_persistent_kernel, kPT, 0);
-    grid = nsm * std::min(occ, 2);
+    grid = occ >= 1 ? nsm : 0;  // one CTA per SM: cheapest grid barrier (measured vs 2 and 4 per SM)
     if (grid <= 0) return fail(ctx, SC_ECUDA, "persistent BBPGD kernel cannot be resident");
   }
   PersistArgs a;
