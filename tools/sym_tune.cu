@@ -166,6 +166,119 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   }
 }
 
+
+// variant 8: two source sub-blocks per phase (8 pair chains per lane per step, two reverse
+// accumulators), high-word clamp
+template <int NW, int TPT, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
+    sym2(const double4* __restrict__ pos4, const double4* __restrict__ f4, const int2* __restrict__ pairs,
+         int64_t npad, double k23a2, double m2a2, long long near_bits, double a4, double* __restrict__ part) {
+  extern __shared__ double4 smem[];
+  double4* sp = smem;
+  double4* sf = smem + SB;
+  double* sacc = reinterpret_cast<double*>(smem + 2 * SB);
+  const int2 pr = pairs[blockIdx.x];
+  const int64_t SI = pr.x, SJ = pr.y;
+  const bool rev = SI != SJ;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  for (int q = tid; q < SB; q += NW * 32) { sp[q] = pos4[SJ * SB + q]; sf[q] = f4[SJ * SB + q]; }
+  double4 p[TPT];
+  double fx[TPT], fy[TPT], fz[TPT], ax[TPT], ay[TPT], az[TPT];
+#pragma unroll
+  for (int m = 0; m < TPT; ++m) {
+    const int64_t row = SI * SB + (w + NW * m) * 32 + lane;
+    p[m] = pos4[row];
+    const double4 f = f4[row];
+    fx[m] = f.x; fy[m] = f.y; fz[m] = f.z;
+    ax[m] = ay[m] = az[m] = 0.0;
+  }
+  for (int q = tid; q < 3 * SB; q += NW * 32) sacc[q] = 0.0;
+  __syncthreads();
+  const int tau = static_cast<int>(near_bits >> 32);
+#pragma unroll 1
+  for (int ph = 0; ph < NSUB / 2; ++ph) {
+    const int cj[2] = {(w + ph) & (NSUB - 1), (w + ph + NSUB / 2) & (NSUB - 1)};
+    double rx[2] = {0, 0}, ry[2] = {0, 0}, rz[2] = {0, 0};
+#pragma unroll 1
+    for (int st = 0; st < 32; ++st) {
+      const int sidx = (lane + st) & 31;
+      double4 pj[2], fj[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) { pj[u] = sp[cj[u] * 32 + sidx]; fj[u] = sf[cj[u] * 32 + sidx]; }
+      constexpr int KK = 2 * TPT;
+      double dx[KK], dy[KK], dz[KK], r2[KK], y[KK], h[KK], e[KK], c1[KK], c2[KK];
+#pragma unroll
+      for (int c = 0; c < KK; ++c) {
+        const int m = c % TPT, u = c / TPT;
+        dx[c] = pj[u].x - p[m].x; dy[c] = pj[u].y - p[m].y; dz[c] = pj[u].z - p[m].z;
+        r2[c] = fma(dz[c], dz[c], fma(dy[c], dy[c], dx[c] * dx[c]));
+        const int hi = max(__double2hiint(r2[c]), tau);
+        r2[c] = __hiloint2double(hi, __double2loint(r2[c]));
+      }
+#pragma unroll
+      for (int c = 0; c < KK; ++c) y[c] = rsq_approx(r2[c]);
+#pragma unroll
+      for (int c = 0; c < KK; ++c) h[c] = r2[c] * y[c];
+#pragma unroll
+      for (int c = 0; c < KK; ++c) e[c] = fma(-h[c], y[c], 1.0);
+#pragma unroll
+      for (int c = 0; c < KK; ++c) { h[c] = fma(0.375, e[c], 0.5); e[c] = y[c] * e[c]; }
+#pragma unroll
+      for (int c = 0; c < KK; ++c) y[c] = fma(e[c], h[c], y[c]);
+#pragma unroll
+      for (int c = 0; c < KK; ++c) h[c] = y[c] * y[c];
+#pragma unroll
+      for (int c = 0; c < KK; ++c) e[c] = y[c] * h[c];
+#pragma unroll
+      for (int c = 0; c < KK; ++c) { c1[c] = fma(k23a2, e[c], y[c]); c2[c] = e[c] * fma(m2a2, h[c], 1.0); }
+#pragma unroll
+      for (int c = 0; c < KK; ++c) {
+        const int m = c % TPT, u = c / TPT;
+        const double t = c2[c] * fma(dz[c], fj[u].z, fma(dy[c], fj[u].y, dx[c] * fj[u].x));
+        ax[m] = fma(t, dx[c], fma(c1[c], fj[u].x, ax[m]));
+        ay[m] = fma(t, dy[c], fma(c1[c], fj[u].y, ay[m]));
+        az[m] = fma(t, dz[c], fma(c1[c], fj[u].z, az[m]));
+      }
+      if (rev) {
+#pragma unroll
+        for (int c = 0; c < KK; ++c) {
+          const int m = c % TPT, u = c / TPT;
+          const double t = c2[c] * fma(dz[c], fz[m], fma(dy[c], fy[m], dx[c] * fx[m]));
+          rx[u] = fma(t, dx[c], fma(c1[c], fx[m], rx[u]));
+          ry[u] = fma(t, dy[c], fma(c1[c], fy[m], ry[u]));
+          rz[u] = fma(t, dz[c], fma(c1[c], fz[m], rz[u]));
+        }
+        const int src = (lane + 1) & 31;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          rx[u] = __shfl_sync(0xffffffffu, rx[u], src);
+          ry[u] = __shfl_sync(0xffffffffu, ry[u], src);
+          rz[u] = __shfl_sync(0xffffffffu, rz[u], src);
+        }
+      }
+    }
+    if (rev) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        double* a = sacc + (cj[u] * 32 + lane) * 3;
+        a[0] += rx[u]; a[1] += ry[u]; a[2] += rz[u];
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < TPT; ++m) {
+    const int64_t row = SI * SB + (w + NW * m) * 32 + lane;
+    double* o = part + (SJ * npad + row) * 3;
+    o[0] = ax[m]; o[1] = ay[m]; o[2] = az[m];
+  }
+  if (rev) {
+    __syncthreads();
+    double* o = part + (SI * npad + SJ * SB) * 3;
+    for (int q = tid; q < 3 * SB; q += NW * 32) o[q] = sacc[q];
+  }
+}
+
 int main(int argc, char** argv) {
   const int64_t N = 262144, NS = N / SB;
   const int NP = argc > 1 ? atoi(argv[1]) : 40000;  // super-block pairs timed
@@ -222,6 +335,9 @@ int main(int argc, char** argv) {
   run("v5 hiclamp+dup (4,4,3)", sym<5, 4, 4, 3>, 128, 2);
   run("v6 hiclamp+pf (4,4,3)", sym<6, 4, 4, 3>, 128, 1);
   run("v7 hiclamp+pf+unr2 (4,4,3)", sym<7, 4, 4, 3>, 128, 1);
-  run("v0 product (4,4,3) again", sym<0, 4, 4, 3>, 128, 1);
+  run("v8 2 src/phase (4,4,2)", sym2<4, 4, 2>, 128, 1);
+  run("v8 2 src/phase (4,4,1)", sym2<4, 4, 1>, 128, 1);
+  run("v8 2 src/phase (4,2,3)", sym2<4, 2, 3>, 128, 1);
+  run("v4 hiclamp (4,4,3) again", sym<4, 4, 4, 3>, 128, 1);
   return 0;
 }
