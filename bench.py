@@ -288,6 +288,8 @@ def main():
         out["e2e"] = {"value": applies_per_step * pairs_per_apply / (e2e_ms / 1e3), "unit": UNIT,
                       "h2d_bytes_per_step": int(hpos.numel() * 8 + hrad.numel() * 8 + hF.numel() * 8),
                       "d2h_bytes_per_step": int(hFc.numel() * 8 + hUc.numel() * 8), "ms_per_step": e2e_ms}
+    if world == 1 and not args.no_e2e:
+        out["other_configs"] = other_configs()
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline()
     if rank == 0:
@@ -295,6 +297,41 @@ def main():
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def other_configs():
+    """Time to solution (device-timed, CUDA events on the library stream around one
+    sc_collision_step, inputs resident) of the converged BASELINE configs that take
+    milliseconds: C1 (512 spheres, the persistent loop) and C4 (200,000 rods).  Context for the
+    BBPGD-iterations/s half of the metric; not part of `value`."""
+    import torch
+
+    from paper_1909_06623_b200 import Context
+    from paper_1909_06623_b200.synthetic import make_problem
+    res = {}
+    for name in ("C1", "C4"):
+        p = make_problem(name, fixed_iters=0)
+        t = lambda a: None if a is None else torch.as_tensor(a, device="cuda:0")
+        ctx = Context(0)
+        args = (p.kind, t(p.pos), t(p.force))
+        kw = dict(radius=t(p.radius), direction=t(p.direction), length=t(p.length), b=p.rod_radius,
+                  gap_abs=p.gap_abs, gap_rel=p.gap_rel, mu=p.mu, dt=p.dt, tol=p.tol, max_iter=p.max_iter)
+        ctx.collision_step(*args, **kw)
+        s = ctx.torch_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(s)
+        reps = 5
+        for _ in range(reps):
+            r = ctx.collision_step(*args, **kw)
+        e1.record(s)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        res[name] = {"n": p.n, "n_c": r["nc"], "bbpgd_iters": r["iters"], "residual": r["residual"],
+                     "converged": r["converged"], "time_to_solution_ms": ms,
+                     "bbpgd_iters_per_s": r["iters"] / (ms / 1e3)}
+        ctx.close()
+    return res
 
 
 def ncu_profile_summary(kernel):

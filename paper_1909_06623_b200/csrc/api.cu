@@ -84,7 +84,7 @@ static bool is_device_ptr(const void* p) {
 
 struct Stager {
   sc_ctx* ctx;
-  std::vector<DBuf<char>> bufs;
+  std::vector<size_t> slots;  // pool buffers this call holds
   struct Pending {
     void* host;
     const void* dev;
@@ -93,7 +93,21 @@ struct Stager {
   std::vector<Pending> outs;
   explicit Stager(sc_ctx* c) : ctx(c) {}
   ~Stager() {
-    for (auto& b : bufs) release(b);
+    for (size_t k : slots) ctx->stage_busy[k] = false;
+  }
+  // a free pool buffer of at least `bytes` (grown in place if needed; never freed per call)
+  int acquire(size_t bytes, char** p) {
+    size_t k = 0;
+    while (k < ctx->stage_pool.size() && ctx->stage_busy[k]) ++k;
+    if (k == ctx->stage_pool.size()) {
+      ctx->stage_pool.emplace_back();
+      ctx->stage_busy.push_back(false);
+    }
+    if (int rc = ensure(ctx, ctx->stage_pool[k], bytes)) return rc;
+    ctx->stage_busy[k] = true;
+    slots.push_back(k);
+    *p = ctx->stage_pool[k].p;
+    return 0;
   }
   // device view of an input (copied if host)
   template <typename T>
@@ -102,11 +116,11 @@ struct Stager {
       *out = p;
       return 0;
     }
-    bufs.emplace_back();
-    if (int rc = ensure(ctx, bufs.back(), count * sizeof(T))) return rc;
-    cudaError_t e = cudaMemcpyAsync(bufs.back().p, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream);
+    char* b = nullptr;
+    if (int rc = acquire(count * sizeof(T), &b)) return rc;
+    cudaError_t e = cudaMemcpyAsync(b, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "stage in");
-    *out = reinterpret_cast<const T*>(bufs.back().p);
+    *out = reinterpret_cast<const T*>(b);
     return 0;
   }
   template <typename T>
@@ -115,10 +129,10 @@ struct Stager {
       *o = p;
       return 0;
     }
-    bufs.emplace_back();
-    if (int rc = ensure(ctx, bufs.back(), count * sizeof(T))) return rc;
-    *o = reinterpret_cast<T*>(bufs.back().p);
-    outs.push_back({p, bufs.back().p, count * sizeof(T)});
+    char* b = nullptr;
+    if (int rc = acquire(count * sizeof(T), &b)) return rc;
+    *o = reinterpret_cast<T*>(b);
+    outs.push_back({p, b, count * sizeof(T)});
     return 0;
   }
   // in + out (read-modify-write)
@@ -544,6 +558,7 @@ void sc_destroy(sc_ctx* ctx) {
   release(ctx->bbox_part); release(ctx->cell_of); release(ctx->cell_cnt); release(ctx->cell_start);
   release(ctx->sorted_idx); release(ctx->pair_cnt); release(ctx->pair_off); release(ctx->scan_tmp);
   release(ctx->sorted4); release(ctx->sorted_dir4); release(ctx->stage);
+  for (auto& b : ctx->stage_pool) release(b);
   if (ctx->dsc) cudaFree(ctx->dsc);
   if (ctx->hsc) cudaFreeHost(ctx->hsc);
   if (ctx->derr) cudaFree(ctx->derr);

@@ -211,6 +211,20 @@ def test_bbpgd_converged_parity(ctx, name, n):
     assert r["active"] == int(np.sum(gam > 0))
 
 
+@pytest.mark.parametrize("bb_mode", [1, 2])
+@pytest.mark.parametrize("name,n", [("C1", None), ("C2", 2048), ("C4", 5000)])
+def test_bbpgd_bb2_and_alternating_steps(ctx, name, n, bb_mode):
+    """The BB2 and alternating BB1/BB2 step lengths (reading A4) against the
+    oracle's same rule: converged gamma, D gamma within 1e-6."""
+    p = make_problem(name, n=n, fixed_iters=0)
+    r = _gpu_solve(ctx, p, bb_mode=bb_mode)
+    o = oracle.solve_problem(p, bb_mode=bb_mode)
+    assert o["status"] == 0 and r["status"] == 0 and r["converged"] == 1 and r["residual"] < 1e-8
+    assert _relL2(_np(r["gamma"]), o["gamma"]) <= 1e-6
+    assert _relL2(_np(r["Fc"]), o["Fc"]) <= 1e-6
+    assert r["iters"] <= 2 * o["iters"] + 20 and o["iters"] <= 2 * r["iters"] + 20
+
+
 @pytest.mark.parametrize("name,n", [("C2", 2048), ("C4", 20000)])
 def test_bbpgd_lockstep_fixed_iterations(ctx, name, n):
     p = make_problem(name, n=n)
