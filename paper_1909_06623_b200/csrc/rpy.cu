@@ -326,10 +326,11 @@ constexpr int kSymSB = 512;                    // bodies per super-block
 constexpr int kSymNsub = kSymSB / 32;          // 16 sub-blocks of 32
 constexpr size_t kSymSmem = 2 * kSymSB * sizeof(double4) + 3 * kSymSB * sizeof(double) + 16;
 
-template <bool POLY, int NW, int TPT, int MINB>
+template <bool POLY, int NW, int TPT, int MINB, int HS>
 __global__ void __launch_bounds__(NW * 32, MINB)
     rpy_sym_kernel(const double4* __restrict__ pos4, const double4* __restrict__ f4, const int2* __restrict__ pairs,
-                   int64_t npad, Consts k, double* __restrict__ part, const int32_t* __restrict__ done, int hs) {
+                   int64_t npad, Consts k, double* __restrict__ part, const int32_t* __restrict__ done) {
+  constexpr int hs = HS;  // source parts per super-block pair (compile-time: no index math at HS = 1)
   static_assert(NW * TPT * 32 == kSymSB, "super-block size");
   constexpr int kSymThreads = NW * 32;
   if (done != nullptr && *done) return;
@@ -342,11 +343,11 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   // hs > 1 (small N, one GPU): the CTA takes the source part h of SJ only (16/hs sub-blocks)
   const int2 pr = pairs[blockIdx.x / hs];
   const int h = static_cast<int>(blockIdx.x % hs);
-  const int nph = kSymNsub / hs;
+  constexpr int nph = kSymNsub / hs;
   const int64_t SI = pr.x, SJ = pr.y;
   const bool rev = SI != SJ;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const uint32_t kBytes = kSymSB / hs * sizeof(double4);
+  constexpr uint32_t kBytes = kSymSB / hs * sizeof(double4);
   const int src0 = h * (kSymSB / hs);  // first source of this part within SJ
   if (tid == 0) {
     mbar_init(bar, 1);
@@ -644,7 +645,7 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
   // small N on one GPU: split every super-block pair's sources in hs parts so the grid fills
   // 148 SMs x 3 CTAs (slots (partner, part); the unwritten ones are zeroed)
   int hs = 1;
-  if (mode == 0)
+  if (mode == 0 && ctx->sym_variant == 0)  // (the 4-warp kernel: 16 / hs sub-blocks >= 4 warps)
     while (hs < 4 && (ctx->sym_off[1] - ctx->sym_off[0]) * hs < 3 * 148) hs *= 2;
   if (int rc = ensure(ctx, ctx->rpy_part, static_cast<size_t>(NS) * hs * ctx->npad * 3)) return rc;
   if (hs > 1)
@@ -652,10 +653,11 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
   const Consts k = make_consts(ctx->a_const);
   static bool attr_set = false;
   if (!attr_set) {
-#define SC_ATTR(P, NW, TPT, MINB) \
-  cudaFuncSetAttribute(rpy_sym_kernel<P, NW, TPT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem)
-    SC_ATTR(false, 4, 4, 3); SC_ATTR(true, 4, 4, 3); SC_ATTR(false, 8, 2, 2); SC_ATTR(true, 8, 2, 2);
-    SC_ATTR(false, 16, 1, 1); SC_ATTR(true, 16, 1, 1);
+#define SC_ATTR(P, NW, TPT, MINB, HS) \
+  cudaFuncSetAttribute(rpy_sym_kernel<P, NW, TPT, MINB, HS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem)
+    SC_ATTR(false, 4, 4, 3, 1); SC_ATTR(true, 4, 4, 3, 1); SC_ATTR(false, 4, 4, 3, 2); SC_ATTR(true, 4, 4, 3, 2);
+    SC_ATTR(false, 4, 4, 3, 4); SC_ATTR(true, 4, 4, 3, 4);
+    SC_ATTR(false, 8, 2, 2, 1); SC_ATTR(true, 8, 2, 2, 1); SC_ATTR(false, 16, 1, 1, 1); SC_ATTR(true, 16, 1, 1, 1);
 #undef SC_ATTR
     attr_set = true;
   }
@@ -665,13 +667,21 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
     const unsigned g = static_cast<unsigned>(np * hs);
     const int2* pt = ctx->sym_pairs.p + p0;
     timer_begin(ctx, SC_K_RPY);
-#define SC_SYM(P, NW, TPT, MINB)                                                                   \
-  rpy_sym_kernel<P, NW, TPT, MINB><<<g, NW * 32, kSymSmem, ctx->stream>>>(ctx->pos4.p, f4, pt, ctx->npad, k, \
-                                                                         ctx->rpy_part.p, done, hs)
+#define SC_SYM(P, NW, TPT, MINB, HS)                                                                     \
+  rpy_sym_kernel<P, NW, TPT, MINB, HS><<<g, NW * 32, kSymSmem, ctx->stream>>>(ctx->pos4.p, f4, pt, ctx->npad, k, \
+                                                                             ctx->rpy_part.p, done)
     switch (ctx->sym_variant) {
-      case 1: if (ctx->poly) SC_SYM(true, 8, 2, 2); else SC_SYM(false, 8, 2, 2); break;
-      case 3: if (ctx->poly) SC_SYM(true, 16, 1, 1); else SC_SYM(false, 16, 1, 1); break;
-      default: if (ctx->poly) SC_SYM(true, 4, 4, 3); else SC_SYM(false, 4, 4, 3); break;
+      case 1: if (ctx->poly) SC_SYM(true, 8, 2, 2, 1); else SC_SYM(false, 8, 2, 2, 1); break;
+      case 3: if (ctx->poly) SC_SYM(true, 16, 1, 1, 1); else SC_SYM(false, 16, 1, 1, 1); break;
+      default:
+        if (hs == 4) {
+          if (ctx->poly) SC_SYM(true, 4, 4, 3, 4); else SC_SYM(false, 4, 4, 3, 4);
+        } else if (hs == 2) {
+          if (ctx->poly) SC_SYM(true, 4, 4, 3, 2); else SC_SYM(false, 4, 4, 3, 2);
+        } else {
+          if (ctx->poly) SC_SYM(true, 4, 4, 3, 1); else SC_SYM(false, 4, 4, 3, 1);
+        }
+        break;
     }
 #undef SC_SYM
     timer_end(ctx, SC_K_RPY);
