@@ -482,7 +482,7 @@ bool rpy_use_sym(const sc_ctx* ctx) {
   if (ctx->rpy_mode == 1) return false;
   if (ctx->rpy_mode == 2) return true;
   // auto: enough super-blocks to fill the machine, and the per-(partner, row) slots
-  // (NS x npad x 24 B: 3.2 GB at N = 262,144, growing as N^2) within a quarter of the HBM
+  // (NS x npad x 24 B: 3.2 GB at N = 262,144, 51 GB at N = 2^20, growing as N^2) within 40% of HBM
   if (ctx->npad < 8 * kSymSB) return false;
   static size_t total_b = 0;  // device memory, queried once (cudaMemGetInfo is not free)
   if (total_b == 0) {
@@ -490,7 +490,7 @@ bool rpy_use_sym(const sc_ctx* ctx) {
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) total_b = size_t(1) << 40;
   }
   const double slot_bytes = static_cast<double>(ctx->npad / kSymSB) * ctx->npad * 3 * sizeof(double);
-  return slot_bytes <= 0.25 * static_cast<double>(total_b);
+  return slot_bytes <= 0.4 * static_cast<double>(total_b);
 }
 
 // Cyclic-half assignment of super-block pairs: super-block S evaluates (S, S) and

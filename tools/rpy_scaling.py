@@ -13,7 +13,8 @@ from paper_1909_06623_b200 import Context  # noqa: E402
 from paper_1909_06623_b200.synthetic import make_problem  # noqa: E402
 
 PEAK = 148 * 64 * 2 * 1.965e9
-cases = [("C5", n) for n in (2048, 4096, 8192, 16384, 32768, 65536, 131072, 262144)] + [("C2", 8192), ("C2", 65536)]
+cases = [("C5", n) for n in (2048, 4096, 8192, 16384, 32768, 65536, 131072, 262144, 524288, 1048576)] + \
+    [("C2", 8192), ("C2", 65536)]
 for name, n in cases:
     p = make_problem(name, n=n)
     ctx = Context(0)
@@ -21,7 +22,7 @@ for name, n in cases:
     pos, rad, F = (torch.as_tensor(a, device=dev) for a in (p.pos, p.radius, p.force))
     ctx.build_contacts_spheres(pos, rad, p.gap_abs, p.gap_rel)
     ctx.mobility_apply(F)
-    reps = max(3, min(200, int(2e11 / (n * n))))
+    reps = max(2, min(200, int(2e11 / (n * n))))
     s = ctx.torch_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
