@@ -1,4 +1,4 @@
-# true (non-event-inflated) durations of the LCP kernels, warm L2: head build vs D^T CTA shapes
+# true (non-event-inflated) durations of the LCP kernels, warm L2: single-list vs split D-gather
 prof() {  # label, config, env...
   env "${@:3}" ncu --metrics gpu__time_duration.sum --cache-control none --clock-control none \
       -k regex:"gather|dt_kernel" -s 6 -c 6 --csv python tools/lcp_profile.py $2 10 2>/dev/null \
@@ -10,6 +10,6 @@ for r in csv.reader(sys.stdin):
 print('$1 $2', {k: round(sum(v)/len(v)/1000,2) for k,v in d.items()})"
 }
 for c in C4 C5; do
-  prof head $c SC_LIB=$PWD/tools/ab/lib_head.so
-  for cfg in 0 1 2 3; do prof cfg$cfg $c SC_DT_CFG=$cfg; done
+  prof single $c SC_NO_GATHER_SPLIT=1
+  prof split $c
 done
