@@ -23,6 +23,7 @@
 //    GPUs).  Inside a split: plain FP64 sums over a 128-source tile, then a
 //    compensated (TwoSum) add of each tile sum.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <vector>
 
@@ -344,6 +345,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   const int2 pr = pairs[blockIdx.x / hs];
   const int h = static_cast<int>(blockIdx.x % hs);
   constexpr int nph = kSymNsub / hs;
+  // HS >= 8: fewer source sub-blocks than warps -> per-warp reverse accumulators
+  // (NW x 512/HS x 3 doubles, within the 512 x 3 of the shared allocation)
+  constexpr bool kPerWarp = nph < NW;
+  static_assert(!kPerWarp || NW * (kSymSB / HS) <= kSymSB, "per-warp accumulators fit");
   const int64_t SI = pr.x, SJ = pr.y;
   const bool rev = SI != SJ;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
@@ -377,7 +382,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 
 #pragma unroll 1
   for (int ph = 0; ph < nph; ++ph) {
-    const int cj = h * nph + (w + ph) % nph;  // distinct across the 4 warps (nph >= 4)
+    const int cj = h * nph + (w + ph) % nph;  // distinct across the 4 warps when nph >= 4
     const double4* tp = sp + cj * 32;
     const double4* tf = sf + cj * 32;
     double rx = 0.0, ry = 0.0, rz = 0.0;  // accumulator of the source this lane meets
@@ -453,11 +458,18 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       }
     }
     if (rev) {  // after 32 steps lane l holds source l's sum
-      double* a = sacc + (cj * 32 + lane) * 3;
-      a[0] += rx;
-      a[1] += ry;
-      a[2] += rz;
-      __syncthreads();
+      if (kPerWarp) {  // small parts: every warp its own accumulators (warps may share a cj)
+        double* a = sacc + ((w * nph + (cj - h * nph)) * 32 + lane) * 3;
+        a[0] += rx;
+        a[1] += ry;
+        a[2] += rz;
+      } else {
+        double* a = sacc + (cj * 32 + lane) * 3;
+        a[0] += rx;
+        a[1] += ry;
+        a[2] += rz;
+        __syncthreads();
+      }
     }
   }
   // forward sums: rows of SI, slot (SJ, h)
@@ -472,7 +484,17 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   if (rev) {  // reverse sums: rows of part h of SJ, slot (SI, h)
     __syncthreads();
     double* o = part + ((SI * hs + h) * npad + SJ * kSymSB + src0) * 3;
-    for (int q = tid; q < 3 * (kSymSB / hs); q += kSymThreads) o[q] = sacc[3 * src0 + q];
+    if (kPerWarp) {  // fixed order over the warps' accumulators
+      constexpr int kPart = kSymSB / HS;
+      for (int q = tid; q < 3 * kPart; q += kSymThreads) {
+        double v = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) v += sacc[ww * 3 * kPart + q];
+        o[q] = v;
+      }
+    } else {
+      for (int q = tid; q < 3 * (kSymSB / hs); q += kSymThreads) o[q] = sacc[3 * src0 + q];
+    }
   }
 }
 
@@ -644,9 +666,21 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
   }
   // small N on one GPU: split every super-block pair's sources in hs parts so the grid fills
   // 148 SMs x 3 CTAs (slots (partner, part); the unwritten ones are zeroed)
+  // hs minimises the makespan ceil(units / (3 x 148 resident CTAs)) / hs, with ~2% per-unit
+  // prologue cost per halving (C2: 136 pairs -> hs = 8, 1,088 units in 2.45 waves instead of
+  // 544 in 1.23); large N keeps hs = 1 (C3: 8,256 pairs)
   int hs = 1;
-  if (mode == 0 && ctx->sym_variant == 0)  // (the 4-warp kernel: 16 / hs sub-blocks >= 4 warps)
-    while (hs < 4 && (ctx->sym_off[1] - ctx->sym_off[0]) * hs < 3 * 148) hs *= 2;
+  if (mode == 0 && ctx->sym_variant == 0) {
+    const double units = static_cast<double>(ctx->sym_off[1] - ctx->sym_off[0]), slots = 3.0 * 148.0;
+    double best = 1e300;
+    for (int c = 1; c <= 8; c *= 2) {
+      const double cost = std::ceil(units * c / slots) / c * (1.0 + 0.02 * c);
+      if (cost < best) {
+        best = cost;
+        hs = c;
+      }
+    }
+  }
   if (int rc = ensure(ctx, ctx->rpy_part, static_cast<size_t>(NS) * hs * ctx->npad * 3)) return rc;
   if (hs > 1)
     SC_CUDA(cudaMemsetAsync(ctx->rpy_part.p, 0, sizeof(double) * NS * hs * ctx->npad * 3, ctx->stream));
@@ -656,7 +690,7 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
 #define SC_ATTR(P, NW, TPT, MINB, HS) \
   cudaFuncSetAttribute(rpy_sym_kernel<P, NW, TPT, MINB, HS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem)
     SC_ATTR(false, 4, 4, 3, 1); SC_ATTR(true, 4, 4, 3, 1); SC_ATTR(false, 4, 4, 3, 2); SC_ATTR(true, 4, 4, 3, 2);
-    SC_ATTR(false, 4, 4, 3, 4); SC_ATTR(true, 4, 4, 3, 4);
+    SC_ATTR(false, 4, 4, 3, 4); SC_ATTR(true, 4, 4, 3, 4); SC_ATTR(false, 4, 4, 3, 8); SC_ATTR(true, 4, 4, 3, 8);
     SC_ATTR(false, 8, 2, 2, 1); SC_ATTR(true, 8, 2, 2, 1); SC_ATTR(false, 16, 1, 1, 1); SC_ATTR(true, 16, 1, 1, 1);
 #undef SC_ATTR
     attr_set = true;
@@ -674,7 +708,9 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
       case 1: if (ctx->poly) SC_SYM(true, 8, 2, 2, 1); else SC_SYM(false, 8, 2, 2, 1); break;
       case 3: if (ctx->poly) SC_SYM(true, 16, 1, 1, 1); else SC_SYM(false, 16, 1, 1, 1); break;
       default:
-        if (hs == 4) {
+        if (hs == 8) {
+          if (ctx->poly) SC_SYM(true, 4, 4, 3, 8); else SC_SYM(false, 4, 4, 3, 8);
+        } else if (hs == 4) {
           if (ctx->poly) SC_SYM(true, 4, 4, 3, 4); else SC_SYM(false, 4, 4, 3, 4);
         } else if (hs == 2) {
           if (ctx->poly) SC_SYM(true, 4, 4, 3, 2); else SC_SYM(false, 4, 4, 3, 2);
