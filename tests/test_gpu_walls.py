@@ -146,3 +146,54 @@ def test_set_walls_errors(ctx):
     ctx.set_walls(None)
     pos = np.array([[0.0, 0, 0.5], [5.0, 0, 0.5]])
     assert ctx.build_contacts_spheres(_cuda(pos), None, 0.0, 0.1) == 0  # no walls: no constraints
+
+
+def test_time_steps_rods_in_box_vs_oracle(ctx):
+    """Rods in a closed box: two whole time steps (contacts with pairs and walls, lever arms, drag,
+    rod-axis update) against the oracle."""
+    p = make_problem("C4", n=6000, fixed_iters=0, walls="box")
+    po = make_problem("C4", n=6000, fixed_iters=0, walls="box")
+    ctx.set_walls(p.walls)
+    pos_g, dir_g = _cuda(p.pos), _cuda(p.direction)
+    for _ in range(2):
+        r = ctx.time_step("rods", pos_g, _cuda(p.force), direction=dir_g, length=_cuda(p.length), b=p.rod_radius,
+                          gap_abs=p.gap_abs, mu=p.mu, dt=p.dt, tol=p.tol, max_iter=p.max_iter)
+        assert r["status"] == 0 and r["residual"] < 1e-8
+        pos_g, dir_g = r["pos"], r["dir"]
+        o = oracle.time_step(po)
+        po.pos, po.direction = o["pos"], o["direction"]
+    scale = np.abs(o["U"]).max() * p.dt
+    np.testing.assert_allclose(_np(pos_g), po.pos, rtol=0, atol=1e-7 * scale + 1e-13)
+    np.testing.assert_allclose(_np(dir_g), po.direction, rtol=0, atol=1e-9)
+
+
+def test_apgd_with_walls_vs_oracle(ctx):
+    """The APGD comparison solver (NEXT row f3) on a problem with floor contacts."""
+    p = make_problem("C1", fixed_iters=0, walls="floor")
+    _gpu_contacts(ctx, p)
+    ctx.assemble_D()
+    ctx.lcp_q(p.dt, ctx.mobility_apply(_cuda(p.force), mu=p.mu))
+    r = ctx.apgd_solve(mu=p.mu, tol=p.tol, max_iter=20000)
+    sysm = oracle.system_for(p)
+    q = sysm.lcp_q(p.dt, sysm.mobility(p.force))
+    o = sysm.apgd(q, tol=p.tol, max_iter=20000)
+    assert r["status"] == 0 and o["status"] == 0 and r["residual"] < 1e-8
+    assert _relL2(_np(r["gamma"]), o["gamma"]) <= 1e-6
+
+
+def test_full_rpy_with_floor(ctx):
+    """Walls (f2) and the full 6N RPY (f4(ii)) together: converged solve vs the oracle."""
+    p = make_problem("C3", n=1500, fixed_iters=0, walls="floor")
+    p.mobility = "rpy6"
+    ctx.set_mobility_model("rpy6")
+    try:
+        _gpu_contacts(ctx, p)
+        ctx.assemble_D()
+        ctx.lcp_q(p.dt, ctx.mobility_apply(_cuda(p.force), mu=p.mu))
+        r = ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=p.max_iter)
+    finally:
+        ctx.set_mobility_model("rpy")
+    o = oracle.solve_problem(p)
+    assert r["status"] == 0 and o["status"] == 0 and r["residual"] < 1e-8
+    assert _relL2(_np(r["gamma"]), o["gamma"]) <= 1e-6
+    assert _relL2(_np(r["Uc"]), o["Uc"]) <= 1e-6
