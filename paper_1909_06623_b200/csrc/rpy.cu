@@ -11,17 +11,20 @@
 //      far : c1 = 1/r + (2/3) a^2 / r^3,  c2 = (1/r^3)(1 - 2 a^2/r^2)
 //      near: c1 = (4/(3 abar))(1 - 9 r/(32 abar)),  c2 = 1/(8 abar^2 r)
 //      U_i += c1 f_j + c2 (d . f_j) d
-//    The near formula at r = 0 (with 1/r -> 0) is exactly the self block
-//    I/(6 pi mu a_i), so the self term needs no special case.
+//    The near formula at r = 0 (with 1/r -> 0) is exactly the self block I/(6 pi mu a_i).
 //  * 1/sqrt(r^2): MUFU.RSQ64H seed (2^-20) + one cubic correction -> 2^-52.
-//    26 DP instructions per monodisperse pair.
-//  * Sources staged in shared memory by 1-D TMA bulk copies (cp.async.bulk,
-//    mbarrier completion), two stages; each thread owns 2 targets.
-//  * Source range split into nsplit chunks (grid.y) so the grid fills 148 SMs
-//    even with few target rows per GPU; per-split partials are combined in a
-//    fixed order by rpy_combine (deterministic, independent of the number of
-//    GPUs).  Inside a split: plain FP64 sums over a 128-source tile, then a
-//    compensated (TwoSum) add of each tile sum.
+//  * Two kernels compute the sum:
+//    - rpy_sym_kernel (default for N >= 4,096): each UNORDERED pair once, feeding both
+//      bodies (36 FP64 instructions per unordered pair); super-block pairs of 512 x 512, source
+//      super-block by one TMA bulk copy, 4 targets per lane in registers, the source's reverse
+//      accumulator carried by a warp rotation; near and self pairs by a high-word r^2 clamp
+//      swapped for the overlap branch in the combine; partials per (partner, row) slot summed in
+//      a fixed order (deterministic, the same for any number of GPUs up to the final all-reduce).
+//    - rpy_partial_kernel (small N, or forced; the bitwise P-invariant multi-GPU unit): target
+//      rows x all sources, 4 targets x 2 sources interleaved per thread, sources through two
+//      TMA-fed shared-memory stages, near pairs zeroed and added from the near list by the
+//      combine; the source range is split into nsplit chunks (grid.y) chosen from N only.
+//  * Accuracy: plain FP64 sums inside a tile, compensated (TwoSum) across tiles / splits / slots.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
