@@ -61,3 +61,27 @@ def test_partition_covers_rows_once(n, world):
     assert covered == list(range(npad))
     # nsplit depends on N only (bitwise P-invariance of the RPY sums)
     assert parts[0]["nsplit"] == plan_partition(n, 1, 0)["nsplit"]
+
+
+def _build_c_demo(out):
+    lib_dir = os.path.join(ROOT, "paper_1909_06623_b200")
+    _lib.load()  # (builds the library if missing)
+    cmd = ["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "examples", "c_api_demo.c"), "-L", lib_dir, "-lstokescol",
+           f"-Wl,-rpath,{lib_dir}", "-lm", "-o", out]
+    return subprocess.run(cmd, capture_output=True, text=True)
+
+
+def test_c_demo_compiles_against_the_header(tmp_path):
+    """The boundary is a plain C ABI: examples/c_api_demo.c builds with gcc (C, no C++) against
+    include/stokescol.h and links libstokescol.so."""
+    r = _build_c_demo(str(tmp_path / "c_api_demo"))
+    assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.gpu
+def test_c_demo_runs(tmp_path):
+    exe = str(tmp_path / "c_api_demo")
+    assert _build_c_demo(exe).returncode == 0
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "c_api_demo: ok" in r.stdout, r.stdout + r.stderr
