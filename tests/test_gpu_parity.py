@@ -175,6 +175,28 @@ def test_mobility_two_far_spheres_finite(ctx):
     assert torch.isfinite(ok).all()
 
 
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("sep", [1e-9, 1e-4, 2.0 - 1e-12, 2.0, 2.0 + 1e-12])
+def test_mobility_near_coincident_and_branch_edge(ctx, kernel, sep):
+    """Pairs at the extremes of the overlap branch (r -> 0, where the symmetric kernel's clamped
+    far value is swapped out in the combine) and straddling r = 2a to rounding, embedded in a
+    C5-recipe cloud large enough for the symmetric kernel (kernel 2) -- the oracle's block as the
+    reference."""
+    p = make_problem("C5", n=4096)
+    pos = p.pos.copy()
+    pos[1] = pos[0] + np.array([sep, 0.0, 0.0])
+    FT = np.random.default_rng(3).normal(size=(p.n, 6))
+    ctx.set_rpy_kernel(kernel)
+    try:
+        ctx.build_contacts_spheres(_cuda(pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+        U = _np(ctx.mobility_apply(_cuda(FT), mu=p.mu))
+    finally:
+        ctx.set_rpy_kernel(0)
+    Uo = oracle.rpy_apply_rows(pos, p.radius, p.mu, FT, 0, 64)
+    assert np.isfinite(U).all()
+    assert _relL2(U[:64, :3], Uo[:, :3]) <= 1e-12
+
+
 # ---------------------------------------------------------------- (a3-a6)
 def _gpu_solve(ctx, p, **kw):
     _gpu_contacts(ctx, p)
