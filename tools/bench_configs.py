@@ -21,7 +21,14 @@ sys.path.insert(0, ROOT)
 from paper_1909_06623_b200 import Context  # noqa: E402
 from paper_1909_06623_b200.synthetic import make_problem  # noqa: E402
 
-HBM_GBS = 6555.8  # MEASURED_PEAKS.json hbm_gbs
+def _hbm_gbs():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6555.8  # an earlier pod's MEASURED_PEAKS.json
+
+
+HBM_GBS = _hbm_gbs()  # MEASURED_PEAKS.json hbm_gbs (driver-written per pod)
 FP64_PEAK = 148 * 64 * 2 * 1.965e9
 BYTES = {"spheres": {"gather_c": 96, "gather_b": 28, "dt_c": 120},
          "rods": {"gather_c": 144, "gather_b": 84, "dt_c": 216}}
