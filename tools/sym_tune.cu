@@ -440,6 +440,8 @@ int main(int argc, char** argv) {
   run("v8 2 src/phase (4,4,1)", sym2<4, 4, 1>, 128, 1);
   run("v8 2 src/phase (4,2,3)", sym2<4, 2, 3>, 128, 1);
   run("v4 hiclamp (4,4,3) again", sym<4, 4, 4, 3>, 128, 1);
+  run("v4 hiclamp (4,4,2)", sym<4, 4, 4, 2>, 128, 1);
+  run("v7 hiclamp+pf+unr2 (4,4,2)", sym<7, 4, 4, 2>, 128, 1);
   {  // SB = 384: tiles of 384 x 384; time the same number of unordered pairs
     const int64_t NS3 = N / 384;
     const int NP3 = (int)((double)pairs.size() * 512.0 * 512.0 / (384.0 * 384.0));
