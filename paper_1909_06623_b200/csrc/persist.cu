@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(kPT) bbpgd_persistent_kernel(PersistArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ DevScalars s;
   __shared__ double red[4 * kR];
+  extern __shared__ double4 dyn[];  // [npad] positions, [npad] forces (phase B)
   if (threadIdx.x == 0) s = *a.sc;
   __syncthreads();
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * kPT + threadIdx.x;
@@ -102,14 +103,30 @@ __global__ void __launch_bounds__(kPT) bbpgd_persistent_kernel(PersistArgs a) {
       if (k == 0) a.f4[b] = real ? make_double4(fx, fy, fz, 0.0) : make_double4(0, 0, 0, 0);
     }
     grid.sync();
-    // ---- B: U = RPY(F), one warp per row (sums scaled by 8 pi mu, written as U)
+    // ---- B: U = RPY(F), one warp per row (sums scaled by 8 pi mu, written as U).  Every CTA
+    //      first stages all N sources (positions, forces: 64 B each, <= 64 KB) in shared memory
+    //      with coalesced loads in flight together, so the pair loop reads shared memory.
+    {
+      double4* sp = dyn;
+      double4* sf = dyn + a.npad;
+      const bool rows_here = static_cast<int64_t>(blockIdx.x) * (kPT / 32) < a.n;  // (CTA has a row)
+      if (rows_here)
+        for (int64_t j = threadIdx.x; j < a.n; j += kPT) {
+          sp[j] = a.pos4[j];
+          sf[j] = ldcg4(&a.f4[j]);
+        }
+      __syncthreads();
+    }
     for (int64_t i = warp; i < a.n; i += nwarps) {
-      const double4 pi = a.pos4[i];
+      const double4* sp = dyn;
+      const double4* sf = dyn + a.npad;
+      const double4 pi = sp[i];
       double ux = 0, uy = 0, uz = 0;
+#pragma unroll 4
       for (int64_t j = lane; j < a.n; j += 32) {
         if (j == i) continue;
-        const double4 pj = a.pos4[j];
-        const double4 fj = ldcg4(&a.f4[j]);
+        const double4 pj = sp[j];
+        const double4 fj = sf[j];
         double dx, dy, dz;
         const double r2 = rpy_r2(pi, pj, dx, dy, dz);
         if (r2 == 0.0) {
@@ -140,7 +157,7 @@ __global__ void __launch_bounds__(kPT) bbpgd_persistent_kernel(PersistArgs a) {
         uz += __shfl_xor_sync(0xffffffffu, uz, o);
       }
       if (lane == 0) {
-        const double4 fi = ldcg4(&a.f4[i]);
+        const double4 fi = dyn[a.npad + i];
         const double cs = (2.0 / 3.0) / pi.w;  // self: 4/(3 a_i)
         a.u4[i] = make_double4(a.scale * fma(cs, fi.x, ux), a.scale * fma(cs, fi.y, uy),
                                a.scale * fma(cs, fi.z, uz), 0.0);
@@ -198,7 +215,10 @@ int bbpgd_persistent(sc_ctx* ctx, double mu) {
     int dev = 0, nsm = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bbpgd_persistent_kernel, kPT, 0);
+    const size_t smem_max = 2 * sizeof(double4) * kPersistMaxBodies;
+    cudaFuncSetAttribute(bbpgd_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem_max));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bbpgd_persistent_kernel, kPT, smem_max);
     grid = occ >= 1 ? nsm : 0;  // one CTA per SM: cheapest grid barrier (measured vs 2 and 4 per SM)
     if (grid <= 0) return fail(ctx, SC_ECUDA, "persistent BBPGD kernel cannot be resident");
   }
@@ -228,8 +248,9 @@ int bbpgd_persistent(sc_ctx* ctx, double mu) {
   a.scale = 1.0 / (8.0 * 3.14159265358979323846 * mu);
   void* args[] = {&a};
   timer_begin(ctx, SC_K_MISC);
+  const size_t smem = 2 * sizeof(double4) * static_cast<size_t>(ctx->npad);
   cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bbpgd_persistent_kernel), dim3(grid),
-                                              dim3(kPT), args, 0, ctx->stream);
+                                              dim3(kPT), args, smem, ctx->stream);
   timer_end(ctx, SC_K_MISC);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaLaunchCooperativeKernel(bbpgd_persistent)");
   return check_launch(ctx, "bbpgd_persistent");

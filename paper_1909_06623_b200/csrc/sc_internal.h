@@ -21,7 +21,7 @@ constexpr int kRpyTile = 128;           // sources per shared-memory tile
 constexpr int kNpadQuantum = 512;       // npad = N rounded up to this (RPY row blocks and super-blocks)
 constexpr int kChunkBodies = 256;       // B_c: bodies per reduction chunk
 constexpr int kPartials = 4;            // doubles per chunk partial
-constexpr int kPersistMaxBodies = 1024; // persistent single-launch BBPGD loop up to this npad (persist.cu)
+constexpr int kPersistMaxBodies = 2048; // persistent single-launch BBPGD loop up to this npad (persist.cu)
 
 enum BodyKind { kNone = -1, kSpheres = 0, kRods = 1 };
 

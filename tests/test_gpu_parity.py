@@ -399,9 +399,9 @@ def test_c5_full_size_converged_certificate(ctx):
 
 
 @pytest.mark.parametrize("name,n,walls", [("C1", None, None), ("C2", 1000, None), ("C1", None, "box"),
-                                          ("C5", 1000, None)])
+                                          ("C5", 1000, None), ("C2", 2000, "floor")])
 def test_persistent_loop_matches_standard_path(name, n, walls):
-    """Small problems (npad <= 1024) run Steps 7-16 in one cooperative launch (persist.cu); the
+    """Small problems (npad <= 2048) run Steps 7-16 in one cooperative launch (persist.cu); the
     launch-per-kernel path (SC_NO_PERSIST=1) and the oracle agree with it."""
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
