@@ -25,9 +25,38 @@ __device__ __forceinline__ void block_reduce4(double v[4], double* red /* [4][kR
   for (int k = 0; k < 4; ++k) v[k] = red[k * kR];
 }
 
+// Fixed-order CTA reduction with one barrier: shuffle-down tree in each warp, then warp 0 sums
+// the warp results in order (result valid in thread 0).  red: >= 4 * (kR / 32) doubles.
+__device__ __forceinline__ void cta_reduce4_shfl(double v[4], double* red) {
+  constexpr int kW = kR / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) red[k * kW + w] = v[k];
+  }
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = lane < kW ? red[k * kW + lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+    }
+  }
+}
+
 // Sums chunk partials in fixed order (thread t: chunks t, t+256, ...; then a fixed tree)
 // and advances the BBPGD scalars.  mode 0: after Step 10 of iteration j; mode 1: alpha_0
 // (Step 6); mode 2: phi_0 (Step 3).  Called by one whole CTA of kR threads.
+// The scalar update of K-FINALIZE from the reduced sums p (one thread).
+__device__ __forceinline__ void finalize_scalars(const double p[4], int mode, DevScalars* s);
+
 __device__ __forceinline__ void finalize_block(const double* part, int64_t nchunks, int mode, DevScalars* s, double* red) {
   double p[4] = {0, 0, 0, 0};
   for (int64_t c = threadIdx.x; c < nchunks; c += kR) {
@@ -36,6 +65,10 @@ __device__ __forceinline__ void finalize_block(const double* part, int64_t nchun
   }
   block_reduce4(p, red);
   if (threadIdx.x != 0) return;
+  finalize_scalars(p, mode, s);
+}
+
+__device__ __forceinline__ void finalize_scalars(const double p[4], int mode, DevScalars* s) {
   for (int k = 0; k < 4; ++k) s->p[k] = p[k];
   if (mode == 1) {
     const double a = p[0] / p[1];  // alpha_0 = g0.g0 / g0.M g0

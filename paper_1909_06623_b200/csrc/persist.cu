@@ -188,13 +188,24 @@ __global__ void __launch_bounds__(kPT) bbpgd_persistent_kernel(PersistArgs a) {
         p[2] = fma(y, y, p[2]);
         p[3] = fma(m, m, p[3]);
       }
-      block_reduce4(p, red);
-      if (threadIdx.x < 4) a.part[c * 4 + threadIdx.x] = p[threadIdx.x];
+      cta_reduce4_shfl(p, red);
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a.part[c * 4 + k] = p[k];
+      }
       __syncthreads();
     }
     grid.sync();
-    // ---- D: K-FINALIZE on every CTA's own copy (same fixed-order sums -> same scalars)
-    finalize_block(a.part, a.nchunks, 0, &s, red);
+    // ---- D: K-FINALIZE on every CTA's own copy: thread 0 sums the few chunk partials
+    //      (npad <= 2048: <= 8 chunks) in chunk order -> the same scalars on every CTA
+    if (threadIdx.x == 0) {
+      double p[4] = {0, 0, 0, 0};
+      for (int64_t c = 0; c < a.nchunks; ++c) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p[k] += __ldcg(a.part + c * 4 + k);
+      }
+      finalize_scalars(p, 0, &s);
+    }
     __syncthreads();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.sc = s;
