@@ -312,7 +312,7 @@ __global__ void set_spheres_kernel(const double* __restrict__ pos, const double*
 __global__ void radius_minmax_kernel(const double* __restrict__ radius, int64_t n, int32_t* __restrict__ poly) {
   const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b >= n) return;
-  if (radius[b] != radius[0]) atomicExch(poly, 1);
+  if (radius[b] != radius[0]) atomicOr(poly, 4);  // bit 2: polydisperse (bits 0, 1: input errors)
 }
 
 __global__ void set_rods_kernel(const double* __restrict__ c, const double* __restrict__ d,
@@ -658,22 +658,26 @@ int sc_build_contacts_spheres(sc_ctx* ctx, int64_t n, const double* pos, const d
       dpos, drad, n, ctx->npad, 1.0, ctx->pos4.p, ctx->derr);
   timer_end(ctx, SC_K_MISC);
   if (int rc = check_launch(ctx, "set_spheres")) return rc;
-  if (int rc = check_body_flags(ctx, "radii must be positive and finite")) return rc;
-  // monodisperse fast path when all radii are equal
+  // monodisperse fast path when all radii are equal (checked with the input flags: one host read)
   ctx->poly = 0;
   ctx->a_const = 1.0;
+  double a0 = 1.0;
   if (radius != nullptr && n > 0) {
     timer_begin(ctx, SC_K_MISC);
     radius_minmax_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(drad, n, ctx->derr);
     timer_end(ctx, SC_K_MISC);
     if (int rc = check_launch(ctx, "radius_minmax")) return rc;
-    SC_CUDA(cudaMemcpyAsync(ctx->herr, ctx->derr, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
-    double a0 = 1.0;
     SC_CUDA(cudaMemcpyAsync(&a0, drad, sizeof(double), cudaMemcpyDefault, ctx->stream));
-    SC_CUDA(cudaStreamSynchronize(ctx->stream));
-    ctx->poly = *ctx->herr ? 1 : 0;
-    *ctx->herr = 0;
-    SC_CUDA(cudaMemsetAsync(ctx->derr, 0, sizeof(int32_t), ctx->stream));
+  }
+  SC_CUDA(cudaMemcpyAsync(ctx->herr, ctx->derr, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int32_t flags = *ctx->herr;
+  *ctx->herr = 0;
+  if (flags) SC_CUDA(cudaMemsetAsync(ctx->derr, 0, sizeof(int32_t), ctx->stream));
+  if (flags & 2) return fail(ctx, SC_ENONFINITE, "non-finite body coordinates or axes");
+  if (flags & 1) return fail(ctx, SC_EINVAL, "radii must be positive and finite");
+  if (radius != nullptr && n > 0) {
+    ctx->poly = (flags & 4) ? 1 : 0;
     ctx->a_const = a0;
   }
   if (ctx->npad > n) {  // padded rows carry the constant radius

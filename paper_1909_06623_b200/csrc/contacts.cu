@@ -523,8 +523,24 @@ int build_common(sc_ctx* ctx, SphereTest st, RodTest rt) {
   if (int rc = check_launch(ctx, "pair_count")) return rc;
   // 5. first_ptr = exclusive scan of counts; n_c = first_ptr[n]
   if (int rc = exclusive_scan_i32(ctx, ctx->pair_cnt.p, ctx->first_ptr.p, n, ctx->scan_tmp.p)) return rc;
-  int32_t nc32 = 0;
+  // spheres: count the RPY near list too before the one host read of both totals
+  const double a0 = ctx->a_const;
+  const double n2 = 4.0 * (a0 * a0);
+  const long long nb = *reinterpret_cast<const long long*>(&n2);
+  if (kind == kSpheres) {
+    if (int rc = ensure(ctx, ctx->near_ptr, n + 1)) return rc;
+    if (int rc = ensure(ctx, ctx->pair_off, n + 1)) return rc;
+    timer_begin(ctx, SC_K_CONTACTS);
+    near_search<false><<<nblk(n), kT, 0, ctx->stream>>>(ctx->sorted4.p, ctx->sorted_idx.p, ctx->cell_start.p, n,
+                                                        g, ctx->poly != 0, nb, ctx->pair_off.p, nullptr, nullptr);
+    timer_end(ctx, SC_K_CONTACTS);
+    if (int rc = check_launch(ctx, "near_count")) return rc;
+    if (int rc = exclusive_scan_i32(ctx, ctx->pair_off.p, ctx->near_ptr.p, n, ctx->scan_tmp.p)) return rc;
+  }
+  int32_t nc32 = 0, nn = 0;
   SC_CUDA(cudaMemcpyAsync(&nc32, ctx->first_ptr.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  if (kind == kSpheres)
+    SC_CUDA(cudaMemcpyAsync(&nn, ctx->near_ptr.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
   SC_CUDA(cudaStreamSynchronize(ctx->stream));
   if (nc32 < 0) return fail(ctx, SC_ENOMEM, "constraint count overflows int32");
   const int64_t nc = nc32;
@@ -563,20 +579,7 @@ int build_common(sc_ctx* ctx, SphereTest st, RodTest rt) {
     if (int rc = check_launch(ctx, "geometry")) return rc;
   }
   if (kind == kSpheres) {
-    // near list (pairs in the RPY overlap branch), both directions, sorted per body
-    if (int rc = ensure(ctx, ctx->near_ptr, n + 1)) return rc;
-    const double a0 = ctx->a_const;
-    const double n2 = 4.0 * (a0 * a0);
-    const long long nb = *reinterpret_cast<const long long*>(&n2);
-    timer_begin(ctx, SC_K_CONTACTS);
-    near_search<false><<<nblk(n), kT, 0, ctx->stream>>>(ctx->sorted4.p, ctx->sorted_idx.p, ctx->cell_start.p, n,
-                                                        g, ctx->poly != 0, nb, ctx->pair_cnt.p, nullptr, nullptr);
-    timer_end(ctx, SC_K_CONTACTS);
-    if (int rc = check_launch(ctx, "near_count")) return rc;
-    if (int rc = exclusive_scan_i32(ctx, ctx->pair_cnt.p, ctx->near_ptr.p, n, ctx->scan_tmp.p)) return rc;
-    int32_t nn = 0;
-    SC_CUDA(cudaMemcpyAsync(&nn, ctx->near_ptr.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
-    SC_CUDA(cudaStreamSynchronize(ctx->stream));
+    // near list (pairs in the RPY overlap branch), both directions, sorted per body (counted above)
     if (int rc = ensure(ctx, ctx->near_idx, nn)) return rc;
     if (nn > 0) {
       timer_begin(ctx, SC_K_CONTACTS);
