@@ -194,18 +194,25 @@ __global__ void __launch_bounds__(kR) dt_kernel(
     }
   }
   block_reduce4(p, red);
-  if (threadIdx.x < 4) part[c * 4 + threadIdx.x] = p[threadIdx.x];
-  if (FUSE) {
-    __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    finalize_block(part, nchunks, MODE == kDtIter ? 0 : (MODE == kDtAlpha0 ? 1 : 2), sc, red);
-    if (threadIdx.x == 0) *counter = 0u;
+  if (!FUSE) {
+    if (threadIdx.x < 4) part[c * 4 + threadIdx.x] = p[threadIdx.x];
+    return;
   }
+  // last-CTA K-FINALIZE: only thread 0's partial stores must be ordered before its counter
+  // increment (the g stores of the other threads need no fence: the next kernel sees them),
+  // so one thread writes the 4 partials and fences instead of a membar in every thread
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) part[c * 4 + k] = p[k];
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  finalize_block(part, nchunks, MODE == kDtIter ? 0 : (MODE == kDtAlpha0 ? 1 : 2), sc, red);
+  if (threadIdx.x == 0) *counter = 0u;
 }
 
 __global__ void proj_own_kernel(const double* __restrict__ gam_old, const double* __restrict__ g_old,

@@ -1,4 +1,4 @@
-# true (non-event-inflated) durations of the LCP kernels, warm L2: single-list vs split D-gather
+# true durations of the LCP kernels (warm L2): committed build (SC_LIB=tools/ab/lib_head.so) vs working tree
 prof() {  # label, config, env...
   env "${@:3}" ncu --metrics gpu__time_duration.sum --cache-control none --clock-control none \
       -k regex:"gather|dt_kernel" -s 6 -c 6 --csv python tools/lcp_profile.py $2 10 2>/dev/null \
@@ -10,6 +10,6 @@ for r in csv.reader(sys.stdin):
 print('$1 $2', {k: round(sum(v)/len(v)/1000,2) for k,v in d.items()})"
 }
 for c in C4 C5; do
-  prof single $c SC_NO_GATHER_SPLIT=1
-  prof split $c
+  prof head $c SC_LIB=$PWD/tools/ab/lib_head.so
+  prof new $c
 done
