@@ -305,14 +305,15 @@ def main():
 def other_configs():
     """Time to solution (device-timed, CUDA events on the library stream around one
     sc_collision_step, inputs resident) of the converged BASELINE configs that take
-    milliseconds: C1 (512 spheres, the persistent loop) and C4 (200,000 rods).  Context for the
+    milliseconds: C1 (512 spheres, the persistent loop), C2 (8,192 polydisperse spheres) and C4
+    (200,000 rods).  Context for the
     BBPGD-iterations/s half of the metric; not part of `value`."""
     import torch
 
     from paper_1909_06623_b200 import Context
     from paper_1909_06623_b200.synthetic import make_problem
     res = {}
-    for name in ("C1", "C4"):
+    for name in ("C1", "C2", "C4"):
         p = make_problem(name, fixed_iters=0)
         t = lambda a: None if a is None else torch.as_tensor(a, device="cuda:0")
         ctx = Context(0)
