@@ -10,7 +10,7 @@ sys.path.insert(0, ROOT)
 from paper_1909_06623_b200 import Context  # noqa: E402
 from paper_1909_06623_b200.synthetic import make_problem  # noqa: E402
 
-for name, n in (("C1", None), ("C2", 1000), ("C2", 2000), ("C5", 2048)):
+for name, n in (("C1", None), ("C5", 512), ("C2", 1000)):
     p = make_problem(name, n=n, fixed_iters=0)
     for env in ("0", "1"):
         os.environ["SC_NO_PERSIST"] = env
