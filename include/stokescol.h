@@ -83,10 +83,22 @@ void* sc_stream(const sc_ctx* ctx);
  *            axis point nearest the wall); gap = (n_k . P - h_k) - b, contact iff
  *            gap < gap_thresh; lever r_i = P - c_i, r_j = 0.
  * Evaluated without FMA contraction (bit-identical to the plain definition).
- * The D column carries +n_k (and r_i x n_k) on body i only; the wall is at rest.
+ * The D column carries +n_k (and r_i x n_k) on body i only; the wall is at rest unless
+ * sc_set_wall_velocities gives it a velocity.
  * Errors: SC_EINVAL (n_walls out of range, NULL walls, |n_k| != 1 beyond 1e-12). */
 #define SC_MAX_WALLS 8
 int sc_set_walls(sc_ctx* ctx, int n_walls, const double* walls);
+/* Moving boundaries (a boundary is "any object either static or moving with a
+ * prescribed velocity"; reading A28).  vel: HOST array n_walls x 3, the velocity V_k of
+ * wall k (n_walls must equal the count of the last sc_set_walls, which resets every V_k to 0).
+ * D is unchanged; the wall's motion enters the constant term of the LCP only:
+ *   q_l = gap_l/dt + D_l^T U_nc - n_k . V_k  for a particle-wall constraint l with wall k
+ * (sc_lcp_q, sc_collision_step, sc_time_step).  sc_time_step then advances each plane with its
+ * velocity, h_k <- h_k + dt n_k . V_k (tangential motion leaves the plane in place).
+ * Errors: SC_EINVAL (count mismatch, NULL, non-finite). */
+int sc_set_wall_velocities(sc_ctx* ctx, int n_walls, const double* vel);
+/* The current planes (HOST n_walls x 4 = (nx, ny, nz, h)), e.g. after sc_time_step moved them. */
+int sc_get_walls(const sc_ctx* ctx, double* walls);
 
 /* ---------------------------------------------------- (a1) build_contacts */
 /* Spheres.  Stores the bodies in the context and computes the near set
@@ -248,6 +260,19 @@ int sc_reset_timing(sc_ctx* ctx);
 /* Total number of kernels this context launched since creation. */
 int64_t sc_launch_count(const sc_ctx* ctx);
 
+/* Residual trace of the next solves (Alg. 1 Steps 3 and 11): with capacity > 0
+ * every sc_bbpgd_solve records phi_0 (the residual at gamma_0) and phi_j after each GD step j,
+ * up to `capacity` values, in a context-owned device buffer (one store per iteration; no host
+ * synchronisation).  capacity = 0 turns it off.  Errors: SC_EINVAL (capacity < 0). */
+int sc_set_residual_trace(sc_ctx* ctx, int32_t capacity);
+/* Copy the trace of the last solve: *count = number of values recorded (min(capacity set,
+ * iterations + 1)); the first min(capacity, *count) go to out (host or device).  Synchronises.
+ * Errors: SC_EINVAL (NULL count, capacity < 0, NULL out with capacity > 0). */
+int sc_get_residual_trace(sc_ctx* ctx, double* out, int32_t capacity, int32_t* count);
+/* Communicator of the context: out4 = {nranks, rank, CUDA device, NCCL version code}; a 1-GPU
+ * context reports {1, 0, device, version}.  Errors: SC_EINVAL (NULL), SC_ENCCL. */
+int sc_comm_info(const sc_ctx* ctx, int32_t* out4);
+
 /* Host-only helper (no GPU needed): the row/chunk partition a world-sized
  * context uses for n bodies.  out7 = {npad,
  * rows_per_rank, row_lo, row_hi, chunk_lo, chunk_hi, nsplit}: rank owns RPY
@@ -255,6 +280,15 @@ int64_t sc_launch_count(const sc_ctx* ctx);
  * (the paper's smaller-index rule); chunk c = bodies
  * [256c, 256c+256). */
 int sc_plan_partition(int64_t n, int world, int rank, int64_t* out7);
+
+/* Host-only helper (no GPU needed): the super-block pairs (SI, SJ) of the symmetric RPY kernel
+ * that rank `rank` of `world` evaluates for nsb super-blocks of 512 bodies (DESIGN.md "K-RPY":
+ * super-block S takes (S, S) and (S, S + d mod nsb) for d = 1 .. (nsb-1)/2, plus d = nsb/2 when
+ * nsb is even and S < nsb/2; rank r takes the contiguous super-block range [r s, (r+1) s),
+ * s = ceil(nsb/world)).  pairs: 2 x count int32 (may be NULL to query count).  Rows of SI receive
+ * the sources of SJ ("forward") and, for SI != SJ, rows of SJ the sources of SI ("reverse").
+ * Errors: SC_EINVAL. */
+int sc_sym_pair_table(int64_t nsb, int world, int rank, int32_t* pairs, int64_t* count);
 
 /* Testing hook: make a 1-GPU context run the multi-GPU decomposition of `world`
  * ranks (every rank's share of every step in turn, on this GPU).  The NCCL

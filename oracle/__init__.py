@@ -91,6 +91,7 @@ def _declare(L):
     L.orc_rpy6_block.argtypes = [vp, d, vp, d, d, C.c_int, vp]
     L.orc_rpy6_apply_rows.argtypes = [i64, vp, vp, d, vp, i64, i64, vp]
     L.orc_lcp_q.argtypes = [C.POINTER(_Sys), vp, d, vp, vp]
+    L.orc_lcp_q_moving_walls.argtypes = [C.POINTER(_Sys), vp, d, vp, C.c_int, vp, vp]
     L.orc_mvop.argtypes = [C.POINTER(_Sys), vp, vp]
     L.orc_bbpgd.argtypes = [C.POINTER(_Sys), vp, d, i32, i32, i32, vp, vp, vp, vp, C.POINTER(Stats)]
     L.orc_bbpgd_dense.argtypes = [i64, vp, vp, d, i32, i32, vp, vp, C.POINTER(Stats)]
@@ -282,6 +283,14 @@ class System:
         U_nc = _f64(U_nc)
         q = np.empty(self.ct.nc)
         _check(lib().orc_lcp_q(C.byref(self.s), _p(self.ct.gap), dt, _p(U_nc), _p(q)), "lcp_q")
+        return q
+
+    def lcp_q_moving_walls(self, dt, U_nc, wall_vel):
+        """q with walls moving at the prescribed velocities wall_vel (k x 3)."""
+        U_nc, wv = _f64(U_nc), _f64(np.asarray(wall_vel, dtype=np.float64).reshape(-1, 3))
+        q = np.empty(self.ct.nc)
+        _check(lib().orc_lcp_q_moving_walls(C.byref(self.s), _p(self.ct.gap), dt, _p(U_nc), wv.shape[0], _p(wv),
+                                            _p(q)), "lcp_q_moving_walls")
         return q
 
     def mvop(self, x):

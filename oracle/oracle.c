@@ -671,6 +671,27 @@ int orc_lcp_q(const orc_system* s, const double* gap, double dt, const double* U
   return 0;
 }
 
+/* Moving boundaries (NEXT row f2: "a boundary refers to any object either static
+ * or moving with a prescribed velocity"; it "does not appear in the mobility matrix").  Wall k
+ * moves with the prescribed velocity V_k, so the gap rate of a particle-wall constraint l = (i, k)
+ * is n_k . (U_i + Omega_i x r_i) - n_k . V_k: D is unchanged and the wall's motion
+ * enters only the constant part of the LCP,
+ *   q_l = gap_l/dt + D_l^T U_nc - n_l . V_k   (cj[l] = n + k; n_l = n_k for a wall constraint). */
+int orc_lcp_q_moving_walls(const orc_system* s, const double* gap, double dt, const double* U_nc, int nw,
+                           const double* wall_vel, double* q) {
+  int st = orc_lcp_q(s, gap, dt, U_nc, q);
+  if (st) return st;
+  for (int64_t l = 0; l < s->nc; ++l) {
+    int64_t k = (int64_t)s->cj[l] - s->n;
+    if (k < 0) continue;
+    if (k >= nw) return -1;
+    const double* nl = s->normal + 3 * l;
+    const double* v = wall_vel + 3 * k;
+    q[l] = q[l] - (nl[0] * v[0] + nl[1] * v[1] + nl[2] * v[2]);
+  }
+  return 0;
+}
+
 /* phi(gamma, g) = || min(gamma, g) ||_2, long double sum. */
 double orc_minmap_residual(int64_t n, const double* gamma, const double* g) {
   long double s = 0.0L;
@@ -744,7 +765,7 @@ static int bbpgd_core(int64_t n, mvop_fn mv, const void* ctx, const double* q, d
       st->converged = 1;
       if (!fixed_iters) break;
     }
-    if (fixed_iters && j == max_iter) break;
+    /* Steps 14-15 also run at j = j_max: Alg. 1 has them inside the loop body */
     /* Step 14: s = gamma_j - gamma_{j-1}, y = g_j - g_{j-1} */
     long double ss = 0.0L, sy = 0.0L, yy = 0.0L;
     for (int64_t l = 0; l < n; ++l) {

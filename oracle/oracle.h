@@ -103,6 +103,9 @@ typedef struct {
 
 /* q = gap/dt + D^T U_nc. */
 int orc_lcp_q(const orc_system* s, const double* gap, double dt, const double* U_nc, double* q);
+/* q with moving walls: q_l -= n_l . V_k for wall constraints (cj = n + k); wall_vel: nw x 3. */
+int orc_lcp_q_moving_walls(const orc_system* s, const double* gap, double dt, const double* U_nc, int nw,
+                           const double* wall_vel, double* q);
 /* One MVOP  w = M x = D^T (Mobility (D x)). */
 int orc_mvop(const orc_system* s, const double* x, double* w);
 

@@ -25,7 +25,8 @@ EXPORTS = [
     "sc_assemble_D", "sc_apply_D", "sc_apply_DT", "sc_mobility_apply", "sc_lcp_q", "sc_bbpgd_solve",
     "sc_collision_step", "sc_set_timing", "sc_get_timing", "sc_reset_timing", "sc_launch_count",
     "sc_plan_partition", "sc_set_emulated_world", "sc_set_rpy_kernel", "sc_time_step", "sc_apgd_solve",
-    "sc_set_walls", "sc_set_mobility_model", "sc_minmap_residual",
+    "sc_set_walls", "sc_set_mobility_model", "sc_minmap_residual", "sc_set_residual_trace",
+    "sc_get_residual_trace", "sc_comm_info", "sc_sym_pair_table", "sc_set_wall_velocities", "sc_get_walls",
 ]
 
 
@@ -96,6 +97,12 @@ def load(build_if_missing: bool = True):
         "sc_set_walls": (ci, [vp, ci, vp]),
         "sc_set_mobility_model": (ci, [vp, ci]),
         "sc_minmap_residual": (ci, [vp, i64, vp, vp, vp]),
+        "sc_set_residual_trace": (ci, [vp, i32]),
+        "sc_get_residual_trace": (ci, [vp, vp, i32, C.POINTER(i32)]),
+        "sc_comm_info": (ci, [vp, vp]),
+        "sc_sym_pair_table": (ci, [i64, ci, ci, vp, C.POINTER(i64)]),
+        "sc_set_wall_velocities": (ci, [vp, ci, vp]),
+        "sc_get_walls": (ci, [vp, vp]),
         "sc_apgd_solve": (ci, [vp, C.POINTER(BbpgdOpts), vp, vp, C.POINTER(BbpgdStats)]),
         "sc_time_step": (ci, [vp, C.POINTER(Problem), C.POINTER(BbpgdOpts), vp, vp, vp, vp, C.POINTER(i64),
                               C.POINTER(BbpgdStats)]),

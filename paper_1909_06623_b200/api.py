@@ -8,6 +8,7 @@ caller passes buffers.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 
 import numpy as np
@@ -88,6 +89,7 @@ class Context:
         self.n = 0
         self.nc = 0
         self.kind = None
+        self._ext = None  # torch view of the library stream (created on first use)
 
     # ------------------------------------------------------------- plumbing
     def close(self):
@@ -113,6 +115,27 @@ class Context:
     def torch_stream(self):
         return torch.cuda.ExternalStream(self.stream_ptr, device=self.device)
 
+    @contextlib.contextmanager
+    def _ordered(self):
+        """Stream ordering across the boundary: the library works on its own stream, the caller's
+        tensors are produced and consumed on torch's current stream.  Entry: the library stream
+        waits for the caller's stream; exit: the caller's stream waits for the library stream
+        (CUDA events only; no host synchronisation)."""
+        if torch is None or not torch.cuda.is_available():
+            yield
+            return
+        if self._ext is None:
+            self._ext = self.torch_stream()
+        cur = torch.cuda.current_stream(self.device)
+        same = cur.cuda_stream == self._ext.cuda_stream
+        if not same:
+            self._ext.wait_stream(cur)
+        try:
+            yield
+        finally:
+            if not same:
+                cur.wait_stream(self._ext)
+
     def _dev(self, shape, dtype=None):
         return torch.empty(shape, dtype=dtype or torch.float64, device=f"cuda:{self.device}")
 
@@ -128,6 +151,19 @@ class Context:
         self._rc(self.lib.sc_set_walls(self._h, int(w.shape[0]), w.ctypes.data if w.size else None))
         self._walls = w
 
+    def set_wall_velocities(self, vel):
+        """Prescribed velocities (k x 3) of the walls of the last set_walls call (moving
+        boundaries): they enter q as -n_k . V_k; time_step advances the planes."""
+        v = np.ascontiguousarray(np.asarray(vel, dtype=np.float64).reshape(-1, 3))
+        self._rc(self.lib.sc_set_wall_velocities(self._h, int(v.shape[0]), v.ctypes.data if v.size else None))
+
+    def get_walls(self):
+        """The current planes (k x 4), moved by time_step for walls with a velocity."""
+        k = int(getattr(self, "_walls", np.zeros((0, 4))).shape[0])
+        out = np.zeros((max(k, 1), 4))
+        self._rc(self.lib.sc_get_walls(self._h, out.ctypes.data))
+        return out[:k]
+
     # --------------------------------------------------- NEXT row f4(ii)
     def set_mobility_model(self, model):
         """"rpy" (BASELINE: translational RPY + self rotation) or "rpy6" (full 6N RPY grand
@@ -140,9 +176,10 @@ class Context:
         n = int(pos.shape[0])
         nc = C.c_int64()
         _f64(pos, (n, 3), "pos"); _f64(radius, (n,), "radius")
-        self._rc(self.lib.sc_build_contacts_spheres(self._h, n, _ptr(_check_dtype(pos, "f64")),
-                                                    _ptr(_check_dtype(radius, "f64")), float(gap_abs),
-                                                    float(gap_rel), C.byref(nc)))
+        with self._ordered():
+            self._rc(self.lib.sc_build_contacts_spheres(self._h, n, _ptr(_check_dtype(pos, "f64")),
+                                                        _ptr(_check_dtype(radius, "f64")), float(gap_abs),
+                                                        float(gap_rel), C.byref(nc)))
         self.n, self.nc, self.kind = n, nc.value, "spheres"
         return self.nc
 
@@ -150,10 +187,11 @@ class Context:
         n = int(center.shape[0])
         nc = C.c_int64()
         _f64(center, (n, 3), "center"); _f64(direction, (n, 3), "direction"); _f64(length, (n,), "length")
-        self._rc(self.lib.sc_build_contacts_rods(self._h, n, _ptr(_check_dtype(center, "f64")),
-                                                 _ptr(_check_dtype(direction, "f64")),
-                                                 _ptr(_check_dtype(length, "f64")), float(b),
-                                                 float(gap_thresh), C.byref(nc)))
+        with self._ordered():
+            self._rc(self.lib.sc_build_contacts_rods(self._h, n, _ptr(_check_dtype(center, "f64")),
+                                                     _ptr(_check_dtype(direction, "f64")),
+                                                     _ptr(_check_dtype(length, "f64")), float(b),
+                                                     float(gap_thresh), C.byref(nc)))
         self.n, self.nc, self.kind = n, nc.value, "rods"
         return self.nc
 
@@ -164,7 +202,8 @@ class Context:
         gap = self._dev((nc,))
         nrm = self._dev((nc, 3))
         lev = self._dev((nc, 2, 3)) if lever else None
-        self._rc(self.lib.sc_get_contacts(self._h, _ptr(ci), _ptr(cj), _ptr(gap), _ptr(nrm), _ptr(lev)))
+        with self._ordered():
+            self._rc(self.lib.sc_get_contacts(self._h, _ptr(ci), _ptr(cj), _ptr(gap), _ptr(nrm), _ptr(lev)))
         out = {"i": ci, "j": cj, "gap": gap, "normal": nrm}
         if lever:
             out["lever"] = lev
@@ -172,34 +211,39 @@ class Context:
 
     # ------------------------------------------------------------- (a2)
     def assemble_D(self):
-        self._rc(self.lib.sc_assemble_D(self._h))
+        with self._ordered():
+            self._rc(self.lib.sc_assemble_D(self._h))
 
     def apply_D(self, gamma, out=None):
         out = self._dev((self.n, 6)) if out is None else out
         _f64(gamma, (self.nc,), "gamma"); _f64(out, (self.n, 6), "out")
-        self._rc(self.lib.sc_apply_D(self._h, _ptr(_check_dtype(gamma, "f64")), _ptr(_check_dtype(out, "f64"))))
+        with self._ordered():
+            self._rc(self.lib.sc_apply_D(self._h, _ptr(_check_dtype(gamma, "f64")), _ptr(_check_dtype(out, "f64"))))
         return out
 
     def apply_DT(self, UW, out=None):
         out = self._dev((self.nc,)) if out is None else out
         _f64(UW, (self.n, 6), "UW"); _f64(out, (self.nc,), "out")
-        self._rc(self.lib.sc_apply_DT(self._h, _ptr(_check_dtype(UW, "f64")), _ptr(_check_dtype(out, "f64"))))
+        with self._ordered():
+            self._rc(self.lib.sc_apply_DT(self._h, _ptr(_check_dtype(UW, "f64")), _ptr(_check_dtype(out, "f64"))))
         return out
 
     # ------------------------------------------------------------- (a4)
     def mobility_apply(self, FT, mu=1.0, out=None):
         out = self._dev((self.n, 6)) if out is None else out
         _f64(FT, (self.n, 6), "FT"); _f64(out, (self.n, 6), "out")
-        self._rc(self.lib.sc_mobility_apply(self._h, float(mu), _ptr(_check_dtype(FT, "f64")),
-                                            _ptr(_check_dtype(out, "f64"))))
+        with self._ordered():
+            self._rc(self.lib.sc_mobility_apply(self._h, float(mu), _ptr(_check_dtype(FT, "f64")),
+                                                _ptr(_check_dtype(out, "f64"))))
         return out
 
     # ------------------------------------------------------------- q, (a6)
     def lcp_q(self, dt, U_nc, out=None):
         out = self._dev((self.nc,)) if out is None else out
         _f64(U_nc, (self.n, 6), "U_nc"); _f64(out, (self.nc,), "out")
-        self._rc(self.lib.sc_lcp_q(self._h, float(dt), _ptr(_check_dtype(U_nc, "f64")),
-                                   _ptr(_check_dtype(out, "f64"))))
+        with self._ordered():
+            self._rc(self.lib.sc_lcp_q(self._h, float(dt), _ptr(_check_dtype(U_nc, "f64")),
+                                       _ptr(_check_dtype(out, "f64"))))
         return out
 
     def bbpgd_solve(self, mu=1.0, tol=1e-8, max_iter=5000, bb_mode=0, fixed_iters=False, gamma0=None,
@@ -216,8 +260,9 @@ class Context:
         Fc = out.get("Fc", self._dev((self.n, 6)) if want_Fc else None)
         Uc = out.get("Uc", self._dev((self.n, 6)) if want_Uc else None)
         st = _lib.BbpgdStats()
-        rc = self._rc(self.lib.sc_bbpgd_solve(self._h, C.byref(opts), _ptr(gamma), _ptr(g), _ptr(Fc), _ptr(Uc),
-                                              C.byref(st)), allow=(0, 1))
+        with self._ordered():
+            rc = self._rc(self.lib.sc_bbpgd_solve(self._h, C.byref(opts), _ptr(gamma), _ptr(g), _ptr(Fc), _ptr(Uc),
+                                                  C.byref(st)), allow=(0, 1))
         return {"gamma": gamma, "g": g, "Fc": Fc, "Uc": Uc, "status": rc, **st.as_dict()}
 
     def collision_step(self, kind, pos, F_ext, radius=None, direction=None, length=None, b=0.5,
@@ -234,8 +279,9 @@ class Context:
         nc = C.c_int64()
         st = _lib.BbpgdStats()
         _f64(Fc_out, (n, 6), "Fc_out"); _f64(Uc_out, (n, 6), "Uc_out")
-        rc = self._rc(self.lib.sc_collision_step(self._h, C.byref(prob), C.byref(opts), _ptr(Fc_out),
-                                                 _ptr(Uc_out), C.byref(nc), C.byref(st)), allow=(0, 1))
+        with self._ordered():
+            rc = self._rc(self.lib.sc_collision_step(self._h, C.byref(prob), C.byref(opts), _ptr(Fc_out),
+                                                     _ptr(Uc_out), C.byref(nc), C.byref(st)), allow=(0, 1))
         self.n, self.nc, self.kind = n, nc.value, kind
         return {"status": rc, "nc": nc.value, **st.as_dict()}
 
@@ -245,8 +291,9 @@ class Context:
         gamma = self._dev((self.nc,))
         g = self._dev((self.nc,))
         st = _lib.BbpgdStats()
-        rc = self._rc(self.lib.sc_apgd_solve(self._h, C.byref(opts), _ptr(gamma), _ptr(g), C.byref(st)),
-                      allow=(0, 1))
+        with self._ordered():
+            rc = self._rc(self.lib.sc_apgd_solve(self._h, C.byref(opts), _ptr(gamma), _ptr(g), C.byref(st)),
+                          allow=(0, 1))
         return {"gamma": gamma, "g": g, "status": rc, **st.as_dict()}
 
     def time_step(self, kind, pos, F_ext, radius=None, direction=None, length=None, b=0.5, gap_abs=0.0,
@@ -267,9 +314,10 @@ class Context:
         U = self._dev((n, 6)) if want_U else None
         nc = C.c_int64()
         st = _lib.BbpgdStats()
-        rc = self._rc(self.lib.sc_time_step(self._h, C.byref(prob), C.byref(opts), _ptr(pos_out), _ptr(dir_out),
-                                            _ptr(_check_dtype(quat, "f64")), _ptr(U), C.byref(nc), C.byref(st)),
-                      allow=(0, 1))
+        with self._ordered():
+            rc = self._rc(self.lib.sc_time_step(self._h, C.byref(prob), C.byref(opts), _ptr(pos_out), _ptr(dir_out),
+                                                _ptr(_check_dtype(quat, "f64")), _ptr(U), C.byref(nc), C.byref(st)),
+                          allow=(0, 1))
         self.n, self.nc, self.kind = n, nc.value, kind
         return {"pos": pos_out, "dir": dir_out, "U": U, "status": rc, "nc": nc.value, **st.as_dict()}
 
@@ -278,8 +326,29 @@ class Context:
         nc = int(gamma.shape[0])
         _f64(gamma, (nc,), "gamma"); _f64(g, (nc,), "g")
         out = np.zeros(1)
-        self._rc(self.lib.sc_minmap_residual(self._h, nc, _ptr(gamma), _ptr(g), _ptr(out)))
+        with self._ordered():
+            self._rc(self.lib.sc_minmap_residual(self._h, nc, _ptr(gamma), _ptr(g), _ptr(out)))
         return float(out[0])
+
+    # ------------------------------------------------------------- residual trace
+    def set_residual_trace(self, capacity: int):
+        """Record phi_0, phi_1, ... of the next solves (up to `capacity` values; 0 = off)."""
+        self._rc(self.lib.sc_set_residual_trace(self._h, int(capacity)))
+        self._trace_cap = int(capacity)
+
+    def residual_trace(self):
+        """phi_0, phi_1, ..., phi_iters of the last solve (numpy; empty if tracing is off)."""
+        cap = getattr(self, "_trace_cap", 0)
+        out = np.zeros(max(cap, 1))
+        cnt = C.c_int32()
+        self._rc(self.lib.sc_get_residual_trace(self._h, out.ctypes.data, int(cap), C.byref(cnt)))
+        return out[:min(cap, cnt.value)].copy()
+
+    def comm_info(self) -> dict:
+        """{nranks, rank, device, nccl_version} of this context's communicator."""
+        out = (C.c_int32 * 4)()
+        self._rc(self.lib.sc_comm_info(self._h, out))
+        return dict(zip(["nranks", "rank", "device", "nccl_version"], list(out)))
 
     # ------------------------------------------------------------- measurement
     def set_timing(self, enable=True):
@@ -327,3 +396,18 @@ def plan_partition(n: int, world: int, rank: int) -> dict:
         raise ScError(rc, "plan_partition: bad arguments")
     keys = ["npad", "rows_per_rank", "row_lo", "row_hi", "chunk_lo", "chunk_hi", "nsplit"]
     return dict(zip(keys, list(out)))
+
+
+def sym_pair_table(nsb: int, world: int, rank: int) -> np.ndarray:
+    """Host-only: the (SI, SJ) super-block pairs rank `rank` of `world` evaluates in the
+    symmetric RPY kernel (include/stokescol.h sc_sym_pair_table)."""
+    lib = _lib.load()
+    cnt = C.c_int64()
+    rc = lib.sc_sym_pair_table(int(nsb), int(world), int(rank), None, C.byref(cnt))
+    if rc != 0:
+        raise ScError(rc, "sym_pair_table: bad arguments")
+    out = np.zeros((max(cnt.value, 1), 2), dtype=np.int32)
+    rc = lib.sc_sym_pair_table(int(nsb), int(world), int(rank), out.ctypes.data, C.byref(cnt))
+    if rc != 0:
+        raise ScError(rc, "sym_pair_table: bad arguments")
+    return out[:cnt.value]

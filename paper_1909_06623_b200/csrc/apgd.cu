@@ -5,6 +5,7 @@
 // Lipschitz estimate L_k (back-tracking) and a gradient restart.  The MVOP is the same as
 // BBPGD's (D-gather, mobility, D^T); these kernels are the per-constraint vector steps and
 // the fixed-order reductions around it.  One GPU (replicas under a multi-GPU context).
+#include "lcp_common.cuh"
 #include "sc_internal.h"
 
 namespace sc {
@@ -30,16 +31,14 @@ __device__ __forceinline__ void reduce4(double v[4], double* red) {
 
 // gamma_new = max(0, y - t g) (projected gradient step from the extrapolated point y);
 // chunk partials: g.(gamma_new - y), |gamma_new - y|^2, g.(gamma_new - gamma), 0.
-__global__ void __launch_bounds__(kA) apgd_step_kernel(const int32_t* __restrict__ first_ptr, int64_t n,
+__global__ void __launch_bounds__(kA) apgd_step_kernel(const int32_t* __restrict__ first_ptr, int64_t n, int64_t nc,
                                                        const double* __restrict__ y, const double* __restrict__ g,
                                                        const double* __restrict__ gam, double t,
                                                        double* __restrict__ gam_new, double* __restrict__ part) {
   __shared__ double red[4 * kA];
   const int64_t c = blockIdx.x;
-  int64_t blo = c * kChunkBodies, bhi = blo + kChunkBodies;
-  if (blo > n) blo = n;
-  if (bhi > n) bhi = n;
-  const int32_t l0 = first_ptr[blo], l1 = first_ptr[bhi];
+  int32_t l0, l1;
+  chunk_bounds(first_ptr, n, nc, c, l0, l1);  // the chunking of the D^T kernels
   double p[4] = {0, 0, 0, 0};
   for (int32_t l = l0 + threadIdx.x; l < l1; l += kA) {
     const double x = y[l] - t * g[l];
@@ -80,8 +79,9 @@ __global__ void __launch_bounds__(kA) sum_chunks_kernel(const double* __restrict
 
 int apgd_launch_step(sc_ctx* ctx, const double* y, const double* g, const double* gam, double t, double* gam_new) {
   timer_begin(ctx, SC_K_MISC);
-  apgd_step_kernel<<<static_cast<unsigned>(ctx->nchunks), kA, 0, ctx->stream>>>(ctx->first_ptr.p, ctx->n, y, g, gam,
-                                                                                t, gam_new, ctx->chunk_part.p);
+  const int32_t* fp = ctx->kind == kRods ? nullptr : ctx->first_ptr.p;
+  apgd_step_kernel<<<static_cast<unsigned>(ctx->nchunks), kA, 0, ctx->stream>>>(fp, ctx->n, ctx->nc, y, g, gam, t,
+                                                                                gam_new, ctx->chunk_part.p);
   timer_end(ctx, SC_K_MISC);
   return check_launch(ctx, "apgd_step");
 }

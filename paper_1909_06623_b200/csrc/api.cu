@@ -91,6 +91,7 @@ struct Stager {
     size_t bytes;
   };
   std::vector<Pending> outs;
+  bool staged_in = false;  // a host input was copied: finish() waits for it (the caller may reuse it)
   explicit Stager(sc_ctx* c) : ctx(c) {}
   ~Stager() {
     for (size_t k : slots) ctx->stage_busy[k] = false;
@@ -120,6 +121,7 @@ struct Stager {
     if (int rc = acquire(count * sizeof(T), &b)) return rc;
     cudaError_t e = cudaMemcpyAsync(b, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "stage in");
+    staged_in = true;
     *out = reinterpret_cast<const T*>(b);
     return 0;
   }
@@ -142,6 +144,7 @@ struct Stager {
     if (*o != p) {
       cudaError_t e = cudaMemcpyAsync(*o, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "stage inout");
+      staged_in = true;
     }
     return 0;
   }
@@ -150,11 +153,12 @@ struct Stager {
       cudaError_t e = cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDeviceToHost, ctx->stream);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "stage out");
     }
-    if (!outs.empty()) {
+    if (!outs.empty() || staged_in) {  // host staging is synchronous (include/stokescol.h)
       cudaError_t e = cudaStreamSynchronize(ctx->stream);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "stage sync");
     }
     outs.clear();
+    staged_in = false;
     return 0;
   }
 };
@@ -243,16 +247,20 @@ struct Dist {
     NCCL_CHECK(ncclGroupEnd());
     return 0;
   }
-  // u4 = RPY(f4).  Symmetric kernel: every rank evaluates its super-block pairs, combines
-  // the slots it wrote (owned rows also get the self and near terms) and the partial
-  // velocities are all-reduced.  Target-row kernel: own rows, then all-gather of the rows.
+  // u4 = RPY(f4).  Symmetric kernel: every rank evaluates its super-block pairs into fixed-point
+  // row accumulators, the int64 limbs are all-reduced (exact), and every rank combines all rows.
+  // Target-row kernel: own rows, then all-gather of the rows.
   int rpy(double mu, const int32_t* done) {
     if (rpy_use_sym(ctx)) {
-      if (!on) return rpy_apply_sym(ctx, ctx->f4.p, mu, ctx->u4.p, done, 1, mine, 0);
-      if (emul) return rpy_apply_sym(ctx, ctx->f4.p, mu, ctx->u4.p, done, W, mine, 1);
-      if (int rc = rpy_apply_sym(ctx, ctx->f4.p, mu, ctx->u4.p, done, W, mine, 2)) return rc;
-      NCCL_CHECK(ncclAllReduce(ctx->u4.p, ctx->u4.p, ctx->npad * 4, ncclDouble, ncclSum, ctx->comm, ctx->stream));
-      return 0;
+      if (!on) return rpy_apply_sym(ctx, ctx->f4.p, mu, ctx->u4.p, done, 1, mine, 0, nullptr);
+      if (emul) return rpy_apply_sym(ctx, ctx->f4.p, mu, ctx->u4.p, done, W, mine, 1, nullptr);
+      // exact int64 sum of every rank's fixed-point limbs (9 per row): U is bitwise the 1-GPU U
+      auto reduce = [&]() -> int {
+        NCCL_CHECK(ncclAllReduce(ctx->sym_acc.p, ctx->sym_acc.p, ctx->npad * 9, ncclInt64, ncclSum, ctx->comm,
+                                 ctx->stream));
+        return 0;
+      };
+      return rpy_apply_sym(ctx, ctx->f4.p, mu, ctx->u4.p, done, W, mine, 2, reduce);
     }
     if (!on) return rpy_apply_rows(ctx, ctx->f4.p, 0, ctx->npad, mu, ctx->u4.p, done);
     for (int r : mine) {
@@ -505,6 +513,14 @@ static int create_common(sc_ctx** out, int device, void* stream) {
   cudaMemset(ctx->derr, 0, sizeof(int32_t));
   cudaMemset(ctx->dcount, 0, sizeof(unsigned int));
   cudaMemset(ctx->dsc, 0, sizeof(DevScalars));
+  // per-device setup (kernel attributes are per device: set them on this context's device)
+  size_t free_b = 0;
+  if (cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+      cudaMemGetInfo(&free_b, &ctx->total_mem) != cudaSuccess || rpy_init_device(ctx) != 0 ||
+      persist_init_device(ctx) != 0) {
+    sc_destroy(ctx);
+    return SC_ECUDA;
+  }
   if (const char* v = std::getenv("SC_SYM_VARIANT")) ctx->sym_variant = std::atoi(v);
   if (const char* v = std::getenv("SC_NO_GRAPHS")) ctx->use_graphs = std::atoi(v) == 0;
   if (const char* v = std::getenv("SC_NO_PERSIST")) ctx->use_persist = std::atoi(v) == 0;
@@ -554,7 +570,7 @@ void sc_destroy(sc_ctx* ctx) {
   release(ctx->rpy6_part); release(ctx->ft_tmp); release(ctx->row_ptr); release(ctx->inc); release(ctx->icol4); release(ctx->first_ptr); release(ctx->near_ptr); release(ctx->near_idx);
   release(ctx->q); release(ctx->gam[0]); release(ctx->gam[1]); release(ctx->g[0]); release(ctx->g[1]);
   release(ctx->w); release(ctx->gam_user); release(ctx->uc); release(ctx->prev_key); release(ctx->prev_gam); release(ctx->chunk_part); release(ctx->chunk_red);
-  release(ctx->sym_pairs); release(ctx->upart); release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);
+  release(ctx->sym_pairs); release(ctx->sym_acc); release(ctx->fx_scale); release(ctx->trace); release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);
   release(ctx->bbox_part); release(ctx->cell_of); release(ctx->cell_cnt); release(ctx->cell_start);
   release(ctx->sorted_idx); release(ctx->pair_cnt); release(ctx->pair_off); release(ctx->scan_tmp);
   release(ctx->sorted4); release(ctx->sorted_dir4); release(ctx->stage);
@@ -632,10 +648,34 @@ int sc_set_walls(sc_ctx* ctx, int n_walls, const double* walls) {
       return fail(ctx, SC_EINVAL, "set_walls: normals must be unit vectors and offsets finite");
   }
   ctx->nwalls = n_walls;
-  for (int k = 0; k < SC_MAX_WALLS; ++k)
+  for (int k = 0; k < SC_MAX_WALLS; ++k) {
     ctx->walls[k] = k < n_walls ? make_double4(walls[4 * k], walls[4 * k + 1], walls[4 * k + 2], walls[4 * k + 3])
                                 : make_double4(0, 0, 0, 0);
+    ctx->wall_vel[k][0] = ctx->wall_vel[k][1] = ctx->wall_vel[k][2] = 0.0;  // static until set
+  }
   ctx->prev_nc = 0;  // the constraint numbering changes: no warm start across this call
+  return SC_OK;
+}
+
+int sc_set_wall_velocities(sc_ctx* ctx, int n_walls, const double* vel) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (n_walls != ctx->nwalls || (n_walls > 0 && vel == nullptr))
+    return fail(ctx, SC_EINVAL, "set_wall_velocities: one velocity per wall of sc_set_walls");
+  for (int k = 0; k < n_walls * 3; ++k)
+    if (!std::isfinite(vel[k])) return fail(ctx, SC_EINVAL, "set_wall_velocities: non-finite velocity");
+  for (int k = 0; k < n_walls; ++k)
+    for (int c = 0; c < 3; ++c) ctx->wall_vel[k][c] = vel[3 * k + c];
+  return SC_OK;
+}
+
+int sc_get_walls(const sc_ctx* ctx, double* walls) {
+  if (ctx == nullptr || (ctx->nwalls > 0 && walls == nullptr)) return SC_EINVAL;
+  for (int k = 0; k < ctx->nwalls; ++k) {
+    walls[4 * k] = ctx->walls[k].x;
+    walls[4 * k + 1] = ctx->walls[k].y;
+    walls[4 * k + 2] = ctx->walls[k].z;
+    walls[4 * k + 3] = ctx->walls[k].w;
+  }
   return SC_OK;
 }
 
@@ -898,6 +938,15 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
   if (int rc = st.out(Fc_out, 6 * n, &dF)) return rc;
   if (int rc = st.out(Uc_out, 6 * n, &dU)) return rc;
 
+  ctx->trace_count = 0;
+  // warm start (opts->warm_start == 2) from the previous solve of this context: decided here;
+  // the previous gamma is then invalidated until this solve completes (an error or an empty
+  // solve below must not leave an older gamma to warm-start a later solve)
+  const bool from_prev = opts->warm_start == 2 && ctx->prev_nc > 0 && ctx->prev_n == n && nc > 0;
+  if (from_prev) {
+    if (int rc = launch_warm_match(ctx, ctx->gam[0].p)) return rc;
+  }
+  ctx->prev_nc = 0;
   if (nc == 0) {  // nothing to resolve: gamma is empty, F_c = 0, U_c = 0
     if (dF) SC_CUDA(cudaMemsetAsync(dF, 0, sizeof(double) * 6 * n, ctx->stream));
     if (dU) SC_CUDA(cudaMemsetAsync(dU, 0, sizeof(double) * 6 * n, ctx->stream));
@@ -918,6 +967,8 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
   h.max_iter = opts->max_iter;
   h.bb_mode = opts->bb_mode;
   h.fixed = opts->fixed_iters ? 1 : 0;
+  h.trace = ctx->trace_cap > 0 ? ctx->trace.p : nullptr;
+  h.trace_cap = ctx->trace_cap;
   SC_CUDA(cudaMemcpyAsync(ctx->dsc, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
   SC_CUDA(cudaMemsetAsync(ctx->derr, 0, sizeof(int32_t), ctx->stream));
   SC_CUDA(cudaMemsetAsync(ctx->chunk_part.p, 0, sizeof(double) * ctx->nchunks * kPartials, ctx->stream));
@@ -937,10 +988,9 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
 
   // Steps 1-5: gamma_0, g_0 = M gamma_0 + q, phi_0
   double* gam0 = ctx->gam[0].p;
-  const bool from_prev = opts->warm_start == 2 && ctx->prev_nc > 0 && ctx->prev_n == n;
   if (opts->warm_start == 1 || from_prev) {
     if (from_prev) {  // gamma_0 of each (i, j) = the previous solve's gamma of the same pair, else 0
-      if (int rc = launch_warm_match(ctx, gam0)) return rc;
+      // (matched above, before the previous solve's list was invalidated)
     } else {
       SC_CUDA(cudaMemcpyAsync(gam0, dgam, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
     }
@@ -956,6 +1006,7 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
   if (int rc = reduce(2)) return rc;
   stt.mvops = 1;
   if (int rc = read_scalars(ctx)) return rc;
+  ctx->trace_count = std::min(ctx->trace_cap, 1);
   int rc_final = SC_OK;
   int parity = 0;
   if (ctx->hsc->nonfinite) return fail(ctx, SC_ENONFINITE, "non-finite initial gradient");
@@ -971,7 +1022,9 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     // device work (extra iterations after convergence are no-op launches)
     const double t_iter = spheres ? 1.3e-12 * static_cast<double>(ctx->npad) * ctx->npad + 4e-5
                                   : 2e-5 + 1.2e-10 * static_cast<double>(nc + n);
-    const int batch = (dist && !D.emul) ? 1 : std::max(1, std::min(32, static_cast<int>(1e-3 / t_iter)));
+    // (multi-GPU: the done flag is identical on every rank -- K-FINALIZE runs on every rank on the
+    // all-reduced partials -- so every rank enqueues the same batches and the collectives match)
+    const int batch = std::max(1, std::min(32, static_cast<int>(1e-3 / t_iter)));
     auto enqueue_iter = [&](int pp) -> int {
       double* go = ctx->g[pp].p;
       double* gmo = ctx->gam[pp].p;
@@ -995,7 +1048,7 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     // graph and replayed, removing per-kernel launch gaps.
     cudaGraphExec_t gexec = nullptr;
     int64_t graph_kernels = 0;
-    const bool persist = !dist && persist_eligible(ctx);
+    const bool persist = !dist && persist_eligible(ctx) && opts->max_iter > 0;
     if (persist) {  // small problem: the whole loop in one cooperative launch (persist.cu)
       if (int rc = bbpgd_persistent(ctx, mu)) return rc;
       if (int rc = read_scalars(ctx)) return rc;
@@ -1045,6 +1098,7 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     if (gexec) cudaGraphExecDestroy(gexec);
     parity = ctx->hsc->iter & 1;
     stt.iters = ctx->hsc->iter;
+    ctx->trace_count = std::min(ctx->trace_cap, ctx->hsc->iter + 1);
     stt.mvops = 2 + ctx->hsc->iter;
   }
   const DevScalars& s = *ctx->hsc;
@@ -1326,6 +1380,12 @@ int sc_time_step(sc_ctx* ctx, const sc_problem* prob, const sc_bbpgd_opts* opts,
   if (int e = check_launch(ctx, "euler_update")) return e;
   if (int e = st.finish()) return e;
   SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  // moving boundaries advance with their prescribed velocity: h_k' = h_k + dt n_k . V_k
+  for (int k = 0; k < ctx->nwalls; ++k) {
+    const double4 w = ctx->walls[k];
+    const double* v = ctx->wall_vel[k];
+    ctx->walls[k].w = w.w + prob->dt * ((w.x * v[0] + w.y * v[1]) + w.z * v[2]);
+  }
   return rc;
 }
 
@@ -1353,6 +1413,51 @@ int sc_reset_timing(sc_ctx* ctx) {
   return SC_OK;
 }
 int64_t sc_launch_count(const sc_ctx* ctx) { return ctx ? ctx->launch_count : -1; }
+
+int sc_set_residual_trace(sc_ctx* ctx, int32_t capacity) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (capacity < 0) return fail(ctx, SC_EINVAL, "set_residual_trace: capacity < 0");
+  cudaSetDevice(ctx->device);
+  if (capacity > 0) {
+    if (int rc = ensure(ctx, ctx->trace, static_cast<size_t>(capacity))) return rc;
+  }
+  ctx->trace_cap = capacity;
+  ctx->trace_count = 0;
+  return SC_OK;
+}
+
+int sc_get_residual_trace(sc_ctx* ctx, double* out, int32_t capacity, int32_t* count) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (count == nullptr || capacity < 0 || (capacity > 0 && out == nullptr))
+    return fail(ctx, SC_EINVAL, "get_residual_trace: bad arguments");
+  cudaSetDevice(ctx->device);
+  const int32_t m = std::min(capacity, ctx->trace_count);
+  *count = ctx->trace_count;
+  if (m == 0) return SC_OK;
+  Stager st(ctx);
+  double* d = nullptr;
+  if (int rc = st.out(out, m, &d)) return rc;
+  SC_CUDA(cudaMemcpyAsync(d, ctx->trace.p, m * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  if (int rc = st.finish()) return rc;
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return SC_OK;
+}
+
+int sc_comm_info(const sc_ctx* ctx, int32_t* out4) {
+  if (ctx == nullptr || out4 == nullptr) return SC_EINVAL;
+  int nranks = 1, rank = 0, dev = ctx->device, ver = 0;
+  if (ctx->comm != nullptr) {
+    if (ncclCommCount(ctx->comm, &nranks) != ncclSuccess || ncclCommUserRank(ctx->comm, &rank) != ncclSuccess ||
+        ncclCommCuDevice(ctx->comm, &dev) != ncclSuccess)
+      return SC_ENCCL;
+  }
+  ncclGetVersion(&ver);
+  out4[0] = nranks;
+  out4[1] = rank;
+  out4[2] = dev;
+  out4[3] = ver;
+  return SC_OK;
+}
 
 int sc_set_rpy_kernel(sc_ctx* ctx, int mode) {
   if (ctx == nullptr) return SC_EINVAL;

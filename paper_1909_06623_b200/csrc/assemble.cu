@@ -7,6 +7,8 @@
 // row_ptr/inc lists, per body, the constraints touching it in ascending
 // constraint order with the side in bit 0, so F = D gamma is an atomic-free,
 // deterministic per-body gather.
+#include <algorithm>
+
 #include "sc_internal.h"
 
 namespace sc {
@@ -120,7 +122,9 @@ int assemble(sc_ctx* ctx) {
       if (int rc = check_launch(ctx, "incidence_columns")) return rc;
     }
   }
-  ctx->nchunks = ctx->npad / kChunkBodies;
+  // reduction chunks (lcp_common.cuh chunk_bounds): spheres 256-body blocks (multi-GPU ownership),
+  // rods 256-constraint tiles
+  ctx->nchunks = ctx->kind == kRods ? std::max<int64_t>(1, (nc + 255) / 256) : ctx->npad / kChunkBodies;
   ctx->assembled = true;
   return 0;
 }

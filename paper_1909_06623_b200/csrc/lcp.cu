@@ -8,9 +8,10 @@
 // thread (U = M_b F_b), so the rods MVOP is one gather + one D^T pass.
 // K-DT (a5): per constraint g_l = n.(U_i - U_j) [+ (r_i x n).W_i - (r_j x n).W_j] + q_l
 //   (Step 10), fused with the partial sums of s.s, s.y, y.y and min(gamma, g)^2
-//   (Steps 11, 14-15) over a FIXED chunking: chunk c = constraints
-//   whose first body lies in [256c, 256c+256).  One CTA per chunk, fixed-order
-//   tree -> the sums are independent of the launch shape and of the number of GPUs.
+//   (Steps 11, 14-15) over a FIXED chunking: spheres, chunk c = constraints
+//   whose first body lies in [256c, 256c+256); rods, 256 consecutive constraints
+//   (chunk_bounds, lcp_common.cuh).  One CTA per chunk, fixed-order tree -> the sums are
+//   independent of the launch shape (spheres: and of the number of GPUs).
 // K-FINALIZE: one CTA sums the chunk partials in fixed order and applies the
 //   BB1/BB2 update, the convergence test and the breakdown rule (reading A5).
 #include <cmath>
@@ -48,6 +49,13 @@ __global__ void __launch_bounds__(kT) gather_kernel(
   const double alpha = MODE == kProj ? dsc->alpha : 0.0;
   double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
   const int32_t e0 = real ? row_ptr[b] : 0, e1 = real ? row_ptr[b + 1] : 0;
+  // rods: the body's axis and drag coefficients are independent of the incidence chain -- issue
+  // their loads first so they overlap it
+  double4 tb = make_double4(0, 0, 0, 0), mb = make_double4(0, 0, 0, 0);
+  if (OUT == kOutRodU && real && k == 0) {
+    tb = dir4[b];
+    mb = mob4[b];
+  }
 #pragma unroll 2
   for (int32_t e = e0 + k; e < e1; e += LPB) {
     const int32_t v = inc[e];
@@ -107,8 +115,8 @@ __global__ void __launch_bounds__(kT) gather_kernel(
     o[0] = fx; o[1] = fy; o[2] = fz; o[3] = tx; o[4] = ty; o[5] = tz;
   } else {
     // rods: U = (1/zeta_par) t t^T F + (1/zeta_perp) (I - t t^T) F ; W = T / zeta_rot
-    const double4 t = dir4[b];
-    const double4 m = mob4[b];
+    const double4 t = tb;
+    const double4 m = mb;
     const double tf = fma(t.z, fz, fma(t.y, fy, t.x * fx));
     const double cpar = (m.x - m.y) * tf;
     out4[2 * b] = make_double4(fma(m.y, fx, cpar * t.x), fma(m.y, fy, cpar * t.y), fma(m.y, fz, cpar * t.z), 0.0);
@@ -130,7 +138,7 @@ enum DtMode { kDtIter = 0, kDtAlpha0 = 1, kDtG0 = 2, kDtInitQ = 3, kDtGrad = 4 }
 // the same fixed-order sums as the separate finalize kernel.
 template <int KIND, int MODE, bool FUSE>
 __global__ void __launch_bounds__(kR) dt_kernel(
-    const int32_t* __restrict__ first_ptr, int64_t n, int64_t c0, const int32_t* __restrict__ ci,
+    const int32_t* __restrict__ first_ptr, int64_t n, int64_t nc, int64_t c0, const int32_t* __restrict__ ci,
     const int32_t* __restrict__ cj, const double4* __restrict__ nrm4, const double4* __restrict__ rxn4,
     const double4* __restrict__ u4, const double* __restrict__ q, const double* __restrict__ gam_new,
     const double* __restrict__ gam_old, const double* __restrict__ g_old, double* __restrict__ g_out,
@@ -139,10 +147,8 @@ __global__ void __launch_bounds__(kR) dt_kernel(
   if (done != nullptr && *done) return;
   __shared__ double red[4 * kR];
   const int64_t c = c0 + blockIdx.x;
-  int64_t blo = c * kChunkBodies, bhi = blo + kChunkBodies;
-  if (blo > n) blo = n;
-  if (bhi > n) bhi = n;
-  const int32_t l0 = first_ptr[blo], l1 = first_ptr[bhi];
+  int32_t l0, l1;
+  chunk_bounds(first_ptr, n, nc, c, l0, l1);
   double p[4] = {0, 0, 0, 0};
   for (int32_t l = l0 + threadIdx.x; l < l1; l += kR) {
     double v = 0.0;
@@ -283,12 +289,12 @@ __global__ void rod_unpack_kernel(const double4* __restrict__ u4, int64_t n, dou
   o[0] = u.x; o[1] = u.y; o[2] = u.z; o[3] = w.x; o[4] = w.y; o[5] = w.z;
 }
 
-// out_l = D_l^T UW (+ gap_l * qscale if addq)
+// out_l = D_l^T UW (+ gap_l * qscale if addq; minus n_k . V_k for a constraint with moving wall k)
 template <int KIND>
 __global__ void dt_user_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj,
                                const double4* __restrict__ nrm4, const double4* __restrict__ rxn4,
                                const double* __restrict__ UW, int64_t nc, int64_t n, int addgap, double inv_dt,
-                               double* __restrict__ out) {
+                               WallRates wr, double* __restrict__ out) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (l >= nc) return;
   const double zero6[6] = {0, 0, 0, 0, 0, 0};
@@ -300,6 +306,7 @@ __global__ void dt_user_kernel(const int32_t* __restrict__ ci, const int32_t* __
     const double4 ra = rxn4[2 * l], rb = rxn4[2 * l + 1];
     v += (ra.x * ui[3] + ra.y * ui[4] + ra.z * ui[5]) - (rb.x * uj[3] + rb.y * uj[4] + rb.z * uj[5]);
   }
+  if (addgap && cj[l] >= n) v -= wr.r[cj[l] - n];  // moving boundary
   out[l] = addgap ? nv.w * inv_dt + v : v;  // q = Phi/dt + D^T U_nc
 }
 
@@ -399,15 +406,16 @@ int launch_dt(sc_ctx* ctx, int mode, const double* gam_new, const double* gam_ol
   const double4* u4 = ctx->u4.p;
   double* part = ctx->chunk_part.p;
   const double* q = ctx->q.p;
+  const int32_t* fp = ctx->kind == kRods ? nullptr : ctx->first_ptr.p;  // rods: constraint tiles
 #define SC_DT(KIND, MODE)                                                                                       \
   do {                                                                                                          \
     if (fuse)                                                                                                   \
       dt_kernel<KIND, MODE, true><<<grid, kR, 0, ctx->stream>>>(                                                \
-          ctx->first_ptr.p, ctx->n, c0, ctx->ci.p, ctx->cj.p, ctx->nrm4.p, ctx->rxn4.p, u4, q, gam_new, gam_old, \
+          fp, ctx->n, ctx->nc, c0, ctx->ci.p, ctx->cj.p, ctx->nrm4.p, ctx->rxn4.p, u4, q, gam_new, gam_old,        \
           g_old, g_out, part, done, ctx->nchunks, ctx->dsc, ctx->dcount);                                       \
     else                                                                                                        \
       dt_kernel<KIND, MODE, false><<<grid, kR, 0, ctx->stream>>>(                                               \
-          ctx->first_ptr.p, ctx->n, c0, ctx->ci.p, ctx->cj.p, ctx->nrm4.p, ctx->rxn4.p, u4, q, gam_new, gam_old, \
+          fp, ctx->n, ctx->nc, c0, ctx->ci.p, ctx->cj.p, ctx->nrm4.p, ctx->rxn4.p, u4, q, gam_new, gam_old,        \
           g_old, g_out, part, done, ctx->nchunks, ctx->dsc, ctx->dcount);                                       \
   } while (0)
   timer_begin(ctx, SC_K_DT);
@@ -476,13 +484,20 @@ int launch_rod_unpack(sc_ctx* ctx, const double4* u4, double* UW) {
 int launch_dt_user(sc_ctx* ctx, const double* UW, double* out, const double* addq, double qscale) {
   if (ctx->nc == 0) return 0;
   const int addgap = addq != nullptr ? 1 : 0;
+  WallRates wr;
+  for (int k = 0; k < SC_MAX_WALLS; ++k) {  // n_k . V_k (q only; D^T itself never sees the walls)
+    const double4 w = ctx->walls[k];
+    const double* v = ctx->wall_vel[k];
+    wr.r[k] = addgap ? (w.x * v[0] + w.y * v[1]) + w.z * v[2] : 0.0;
+  }
   timer_begin(ctx, SC_K_DT);
   if (ctx->kind == kSpheres)
     dt_user_kernel<kSpheres><<<nblk(ctx->nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, ctx->nrm4.p, nullptr,
-                                                                     UW, ctx->nc, ctx->n, addgap, qscale, out);
+                                                                     UW, ctx->nc, ctx->n, addgap, qscale, wr, out);
   else
     dt_user_kernel<kRods><<<nblk(ctx->nc), kT, 0, ctx->stream>>>(ctx->ci.p, ctx->cj.p, ctx->nrm4.p,
-                                                                  ctx->rxn4.p, UW, ctx->nc, ctx->n, addgap, qscale, out);
+                                                                  ctx->rxn4.p, UW, ctx->nc, ctx->n, addgap, qscale, wr,
+                                                                  out);
   timer_end(ctx, SC_K_DT);
   return check_launch(ctx, "dt_user");
 }

@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kPT) bbpgd_persistent_kernel(PersistArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) p[k] += __ldcg(a.part + c * 4 + k);
       }
-      finalize_scalars(p, 0, &s);
+      finalize_scalars(p, 0, &s, blockIdx.x == 0);
     }
     __syncthreads();
   }
@@ -216,23 +216,27 @@ __global__ void __launch_bounds__(kPT) bbpgd_persistent_kernel(PersistArgs a) {
 bool persist_eligible(const sc_ctx* ctx) {
   // (a forced RPY kernel choice, sc_set_rpy_kernel, keeps the launch-per-kernel path)
   return ctx->use_persist && ctx->rpy_mode == 0 && ctx->kind == kSpheres && ctx->world == 1 &&
-         ctx->emul_world == 1 && ctx->npad <= kPersistMaxBodies && ctx->nc > 0;
+         ctx->emul_world == 1 && ctx->npad <= kPersistMaxBodies && ctx->nc > 0 && ctx->persist_grid > 0;
+}
+
+// Per-device setup (sc_create): the kernel's shared-memory attribute and its grid (one CTA per SM
+// of this context's device, if it can be resident).
+int persist_init_device(sc_ctx* ctx) {
+  const size_t smem_max = 2 * sizeof(double4) * kPersistMaxBodies;
+  cudaError_t e = cudaFuncSetAttribute(bbpgd_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem_max));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaFuncSetAttribute(bbpgd_persistent)");
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bbpgd_persistent_kernel, kPT, smem_max);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "occupancy(bbpgd_persistent)");
+  ctx->persist_grid = occ >= 1 ? ctx->num_sms : 0;  // one CTA per SM: cheapest grid barrier
+  return 0;
 }
 
 // Steps 7-16 of Alg. 1 in one cooperative launch (the scalars in ctx->dsc after Step 6).
 int bbpgd_persistent(sc_ctx* ctx, double mu) {
-  static int grid = 0;
-  if (grid == 0) {
-    int dev = 0, nsm = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const size_t smem_max = 2 * sizeof(double4) * kPersistMaxBodies;
-    cudaFuncSetAttribute(bbpgd_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem_max));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bbpgd_persistent_kernel, kPT, smem_max);
-    grid = occ >= 1 ? nsm : 0;  // one CTA per SM: cheapest grid barrier (measured vs 2 and 4 per SM)
-    if (grid <= 0) return fail(ctx, SC_ECUDA, "persistent BBPGD kernel cannot be resident");
-  }
+  const int grid = ctx->persist_grid;
+  if (grid <= 0) return fail(ctx, SC_ECUDA, "persistent BBPGD kernel cannot be resident");
   PersistArgs a;
   a.n = ctx->n;
   a.npad = ctx->npad;

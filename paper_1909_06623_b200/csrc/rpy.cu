@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <functional>
 #include <vector>
 
 #include "rpy_common.cuh"
@@ -65,6 +66,89 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// ---------------------------------------------------------------------------------------
+// Exact, order-independent accumulation of the symmetric kernel's partial sums (DESIGN.md
+// "K-RPY"): every partial sum v (a CTA's forward sum for one of its target rows, or its reverse
+// sum for one of its source rows) is rounded ONCE to the fixed-point integer X = round(v 2^s)
+// (|X| < 2^100 by the choice of s, fx_shift) and added with integer atomics into three int64
+// limbs per (row, component): X = x2 2^86 + x1 2^43 + x0, 0 <= x0, x1 < 2^43.  Integer addition
+// is associative, so the sums -- hence U -- are bitwise independent of the CTA schedule and of
+// the number of GPUs (the limbs of every rank are all-reduced exactly as int64); each limb sum
+// stays below 2^63 for up to 2^20 contributions per row.  Memory: 72 B per row (O(N)), instead
+// of one double slot per (partner super-block, row) (O(N^2/512)).
+struct FxScale {
+  unsigned long long maxf_bits;    // max_j |f_j| (components), as the bits of a non-negative double
+  unsigned long long maxinva_bits; // max_j 1/a_j
+  int32_t bad;                     // a non-finite partial sum was met
+  int32_t pad;
+};
+constexpr long long kM43 = (1LL << 43) - 1;
+
+// s such that any row sum (npad sources, each |T_ij f_j| <= 2 max|f| / a_min per component) is
+// below 2^100 in magnitude after scaling by 2^s.
+__device__ __forceinline__ int fx_shift(const FxScale* fs, int64_t npad) {
+  const double mf = __longlong_as_double(static_cast<long long>(fs->maxf_bits));
+  const double mi = __longlong_as_double(static_cast<long long>(fs->maxinva_bits));
+  const double B = 2.0 * mf * mi * static_cast<double>(npad);
+  if (!(B > 0.0) || !isfinite(B)) return 0;
+  int sh = 100 - (ilogb(B) + 1);
+  return sh < -1000 ? -1000 : (sh > 1000 ? 1000 : sh);
+}
+__device__ __forceinline__ double pow2(int k) {  // exact 2^k, |k| <= 1000
+  const int h = k / 2;
+  return __longlong_as_double(static_cast<long long>(1023 + h) << 52) *
+         __longlong_as_double(static_cast<long long>(1023 + k - h) << 52);
+}
+// v 2^s rounded to the nearest integer (ties away from zero) in 128-bit two's complement, as limbs
+__device__ __forceinline__ void fx_limbs(double v, double scale, long long& x0, long long& x1, long long& x2,
+                                         bool& bad) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v * scale));
+  const int e = static_cast<int>((b >> 52) & 0x7ff);
+  unsigned __int128 X = 0;
+  if (e == 0x7ff) {
+    bad = true;  // NaN / Inf
+  } else if (e != 0) {
+    const unsigned long long m = (b & ((1ull << 52) - 1)) | (1ull << 52);
+    const int sh = e - 1075;  // |v 2^s| = m 2^sh
+    if (sh > 48) {
+      bad = true;  // outside the bound of fx_shift (cannot happen for finite inputs)
+    } else if (sh >= 0) {
+      X = static_cast<unsigned __int128>(m) << sh;
+    } else if (sh >= -53) {
+      X = (m + (1ull << (-sh - 1))) >> (-sh);
+    }
+  }
+  const __int128 Xs = (b >> 63) ? -static_cast<__int128>(X) : static_cast<__int128>(X);
+  x0 = static_cast<long long>(Xs & kM43);
+  x1 = static_cast<long long>((Xs >> 43) & kM43);
+  x2 = static_cast<long long>(Xs >> 86);
+}
+__device__ __forceinline__ void fx_red3(long long* acc /* [3 comps][3 limbs] */, double vx, double vy, double vz,
+                                        double scale, bool& bad) {
+  const double v[3] = {vx, vy, vz};
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    long long x0, x1, x2;
+    fx_limbs(v[c], scale, x0, x1, x2, bad);
+    unsigned long long* a = reinterpret_cast<unsigned long long*>(acc + 3 * c);
+    if (x0) atomicAdd(a + 0, static_cast<unsigned long long>(x0));  // RED.E.ADD.64 (no return)
+    if (x1) atomicAdd(a + 1, static_cast<unsigned long long>(x1));
+    if (x2) atomicAdd(a + 2, static_cast<unsigned long long>(x2));
+  }
+}
+// limb sums -> double (carry-normalised; one rounding), times 2^-s
+__device__ __forceinline__ double fx_value(const long long* l, double inv_scale) {
+  long long S0 = l[0], S1 = l[1], S2 = l[2];
+  long long c = S0 >> 43;
+  S0 &= kM43;
+  S1 += c;
+  c = S1 >> 43;
+  S1 &= kM43;
+  S2 += c;
+  const long long hi = S2 * (1LL << 43) + S1;  // |S2| <= 2^14
+  return fma(static_cast<double>(hi), 0x1p43, static_cast<double>(S0)) * inv_scale;
 }
 
 struct Consts {
@@ -333,7 +417,8 @@ constexpr size_t kSymSmem = 2 * kSymSB * sizeof(double4) + 3 * kSymSB * sizeof(d
 template <bool POLY, int NW, int TPT, int MINB, int HS>
 __global__ void __launch_bounds__(NW * 32, MINB)
     rpy_sym_kernel(const double4* __restrict__ pos4, const double4* __restrict__ f4, const int2* __restrict__ pairs,
-                   int64_t npad, Consts k, double* __restrict__ part, const int32_t* __restrict__ done) {
+                   int64_t npad, Consts k, long long* __restrict__ acc, FxScale* __restrict__ fs,
+                   const int32_t* __restrict__ done) {
   constexpr int hs = HS;  // source parts per super-block pair (compile-time: no index math at HS = 1)
   static_assert(NW * TPT * 32 == kSymSB, "super-block size");
   constexpr int kSymThreads = NW * 32;
@@ -475,29 +560,57 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       }
     }
   }
-  // forward sums: rows of SI, slot (SJ, h)
+  // forward sums (rows of SI) and reverse sums (rows of part h of SJ) -> fixed-point limbs
+  const double scale = pow2(fx_shift(fs, npad));
+  bool bad = false;
 #pragma unroll
   for (int m = 0; m < TPT; ++m) {
     const int64_t row = SI * kSymSB + (w + NW * m) * 32 + lane;
-    double* o = part + ((SJ * hs + h) * npad + row) * 3;
-    o[0] = ax[m];
-    o[1] = ay[m];
-    o[2] = az[m];
+    fx_red3(acc + row * 9, ax[m], ay[m], az[m], scale, bad);
   }
-  if (rev) {  // reverse sums: rows of part h of SJ, slot (SI, h)
+  if (rev) {
     __syncthreads();
-    double* o = part + ((SI * hs + h) * npad + SJ * kSymSB + src0) * 3;
-    if (kPerWarp) {  // fixed order over the warps' accumulators
-      constexpr int kPart = kSymSB / HS;
-      for (int q = tid; q < 3 * kPart; q += kSymThreads) {
-        double v = 0.0;
+    constexpr int kPart = kSymSB / HS;
+    for (int q = tid; q < kPart; q += kSymThreads) {
+      double v[3];
+      if (kPerWarp) {  // fixed order over the warps' accumulators
 #pragma unroll
-        for (int ww = 0; ww < NW; ++ww) v += sacc[ww * 3 * kPart + q];
-        o[q] = v;
+        for (int c = 0; c < 3; ++c) {
+          double t = 0.0;
+#pragma unroll
+          for (int ww = 0; ww < NW; ++ww) t += sacc[ww * 3 * kPart + 3 * q + c];
+          v[c] = t;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] = sacc[3 * (src0 + q) + c];
       }
-    } else {
-      for (int q = tid; q < 3 * (kSymSB / hs); q += kSymThreads) o[q] = sacc[3 * src0 + q];
+      fx_red3(acc + (SJ * kSymSB + src0 + q) * 9, v[0], v[1], v[2], scale, bad);
     }
+  }
+  if (bad) fs->bad = 1;
+}
+
+// max_j |f_j| and max_j 1/a_j (for the fixed-point scale); fs zeroed before the launch
+__global__ void fx_prep_kernel(const double4* __restrict__ pos4, const double4* __restrict__ f4, int64_t npad,
+                               FxScale* __restrict__ fs, const int32_t* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  double mf = 0.0, mi = 0.0;
+  for (int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < npad;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double4 f = f4[b];
+    mf = fmax(mf, fmax(fabs(f.x), fmax(fabs(f.y), fabs(f.z))));
+    mi = fmax(mi, 0.5 / pos4[b].w);  // w = a/2
+  }
+  if (!(mf <= 1.7e308)) mf = 1.7e308;  // NaN / Inf forces: the kernel flags them (fx_limbs)
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    mf = fmax(mf, __shfl_xor_sync(0xffffffffu, mf, o));
+    mi = fmax(mi, __shfl_xor_sync(0xffffffffu, mi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&fs->maxf_bits, static_cast<unsigned long long>(__double_as_longlong(mf)));
+    atomicMax(&fs->maxinva_bits, static_cast<unsigned long long>(__double_as_longlong(mi)));
   }
 }
 
@@ -506,16 +619,9 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 bool rpy_use_sym(const sc_ctx* ctx) {
   if (ctx->rpy_mode == 1) return false;
   if (ctx->rpy_mode == 2) return true;
-  // auto: enough super-blocks to fill the machine, and the per-(partner, row) slots
-  // (NS x npad x 24 B: 3.2 GB at N = 262,144, 51 GB at N = 2^20, growing as N^2) within 40% of HBM
-  if (ctx->npad < 8 * kSymSB) return false;
-  static size_t total_b = 0;  // device memory, queried once (cudaMemGetInfo is not free)
-  if (total_b == 0) {
-    size_t free_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) total_b = size_t(1) << 40;
-  }
-  const double slot_bytes = static_cast<double>(ctx->npad / kSymSB) * ctx->npad * 3 * sizeof(double);
-  return slot_bytes <= 0.4 * static_cast<double>(total_b);
+  // auto: enough super-blocks to fill the machine (the fixed-point accumulators are O(N): no
+  // memory limit beyond the bodies themselves)
+  return ctx->npad >= 8 * kSymSB;
 }
 
 // Cyclic-half assignment of super-block pairs: super-block S evaluates (S, S) and
@@ -540,34 +646,51 @@ static void sym_rank_range(int64_t NS, int W, int r, int64_t* s0, int64_t* s1) {
   *s1 = std::min<int64_t>(NS, (r + 1) * spr);
 }
 
-// Combine for the symmetric kernel: sums, in increasing slot order (TwoSum), the slots this
-// rank wrote for the row (all of them when s0 = 0, s1 = NS), adds the self and near-list
-// terms for owned rows, scales by 1/(8 pi mu).
+}  // namespace sc
+
+// Host-only C ABI helper (include/stokescol.h): rank r's super-block pairs of the symmetric kernel.
+extern "C" int sc_sym_pair_table(int64_t nsb, int world, int rank, int32_t* pairs, int64_t* count) {
+  if (nsb < 1 || world < 1 || rank < 0 || rank >= world || count == nullptr) return SC_EINVAL;
+  int64_t a0, a1, k = 0;
+  sc::sym_rank_range(nsb, world, rank, &a0, &a1);
+  for (int64_t S = a0; S < a1; ++S)
+    for (int64_t d = 0; d < nsb; ++d) {
+      if (d != 0 && !sc::sym_in_D(S, d, nsb)) continue;
+      if (pairs != nullptr) {
+        pairs[2 * k] = static_cast<int32_t>(S);
+        pairs[2 * k + 1] = static_cast<int32_t>((S + d) % nsb);
+      }
+      ++k;
+    }
+  *count = k;
+  return SC_OK;
+}
+
+namespace sc {
+
+// Combine for the symmetric kernel: the row's exact fixed-point sum (all ranks' contributions
+// after the int64 all-reduce), then the self term and the near-list swap (TwoSum), scaled by
+// 1/(8 pi mu).  Reads the limbs and zeroes them for the next apply.
 template <bool POLY>
-__global__ void rpy_sym_combine_kernel(const double* __restrict__ part, int64_t NS, int64_t s0, int64_t s1,
-                                       int64_t npad, int64_t n, double scale, const double4* __restrict__ pos4,
+__global__ void rpy_sym_combine_kernel(long long* __restrict__ acc, const FxScale* __restrict__ fs, int64_t npad,
+                                       int64_t n, double scale, const double4* __restrict__ pos4,
                                        const double4* __restrict__ f4, const int32_t* __restrict__ near_ptr,
                                        const int32_t* __restrict__ near_idx, double4* __restrict__ out,
                                        const int32_t* __restrict__ done, int32_t* __restrict__ err) {
   if (done != nullptr && *done) return;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (row >= npad) return;
-  const int64_t T = row / kSymSB;
-  const bool own_row = T >= s0 && T < s1;
-  const bool all = s0 == 0 && s1 == NS;
-  double hx = 0, hy = 0, hz = 0, lx = 0, ly = 0, lz = 0;
-  for (int64_t s = 0; s < NS; ++s) {
-    if (!all) {
-      const bool fwd = own_row && (s == T || sym_in_D_dev(T, (s - T + NS) % NS, NS));
-      const bool rev = s >= s0 && s < s1 && s != T && sym_in_D_dev(s, (T - s + NS) % NS, NS);
-      if (!fwd && !rev) continue;
-    }
-    const double* p = part + (s * npad + row) * 3;
-    two_sum_acc(hx, lx, p[0]);
-    two_sum_acc(hy, ly, p[1]);
-    two_sum_acc(hz, lz, p[2]);
+  long long* a = acc + row * 9;
+  long long l[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    l[k] = a[k];
+    a[k] = 0;
   }
-  if (row < n && own_row) {
+  const double inv = pow2(-fx_shift(fs, npad));
+  double hx = fx_value(l + 0, inv), hy = fx_value(l + 3, inv), hz = fx_value(l + 6, inv);
+  double lx = 0, ly = 0, lz = 0;
+  if (row < n) {
     const double4 pi = pos4[row];
     const double4 fi = f4[row];
     const double cs = (2.0 / 3.0) / pi.w;  // self: 4/(3 a_i)
@@ -606,23 +729,10 @@ __global__ void rpy_sym_combine_kernel(const double* __restrict__ part, int64_t 
       two_sum_acc(hz, lz, fma(t, dz, fma(c1, fj.z, -fz_)));
     }
   }
-  out[row] = row < n ? make_double4(scale * (hx + lx), scale * (hy + ly), scale * (hz + lz), 0.0)
-                     : make_double4(0.0, 0.0, 0.0, 0.0);
-}
-
-__global__ void sum_ranks_kernel(const double4* __restrict__ parts, int W, int64_t npad, double4* __restrict__ u4,
-                                 const int32_t* __restrict__ done) {
-  if (done != nullptr && *done) return;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (row >= npad) return;
-  double4 s = parts[row];
-  for (int r = 1; r < W; ++r) {
-    const double4 v = parts[r * npad + row];
-    s.x += v.x;
-    s.y += v.y;
-    s.z += v.z;
-  }
-  u4[row] = s;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  out[row] = fs->bad ? make_double4(nan, nan, nan, 0.0)  // non-finite forces: propagate (SC_ENONFINITE)
+             : row < n ? make_double4(scale * (hx + lx), scale * (hy + ly), scale * (hz + lz), 0.0)
+                       : make_double4(0.0, 0.0, 0.0, 0.0);
 }
 
 static Consts make_consts(double a) {
@@ -638,12 +748,30 @@ static Consts make_consts(double a) {
   return k;
 }
 
+int rpy_init_device(sc_ctx* ctx) {
+  cudaError_t e = cudaSuccess;
+#define SC_ATTR(P, NW, TPT, MINB, HS)                                                                              \
+  if (e == cudaSuccess)                                                                                          \
+  e = cudaFuncSetAttribute(rpy_sym_kernel<P, NW, TPT, MINB, HS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           kSymSmem)
+  SC_ATTR(false, 4, 4, 3, 1); SC_ATTR(true, 4, 4, 3, 1); SC_ATTR(false, 4, 4, 3, 2); SC_ATTR(true, 4, 4, 3, 2);
+  SC_ATTR(false, 4, 4, 3, 4); SC_ATTR(true, 4, 4, 3, 4); SC_ATTR(false, 4, 4, 3, 8); SC_ATTR(true, 4, 4, 3, 8);
+  SC_ATTR(false, 8, 2, 2, 1); SC_ATTR(true, 8, 2, 2, 1); SC_ATTR(false, 16, 1, 1, 1); SC_ATTR(true, 16, 1, 1, 1);
+#undef SC_ATTR
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(rpy_partial_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRpySmem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(rpy_partial_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRpySmem);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaFuncSetAttribute(rpy)");
+  return 0;
+}
+
 // u4 = RPY(f4) with the symmetric kernel.  ranks: the ranks whose pairs this process
-// evaluates (W = 1: everything).  mode 0: one GPU -> combine all slots into u4;
-// mode 1: emulated world -> per-rank combine into ctx->upart, rank-ordered sum into u4;
-// mode 2: real multi-GPU -> this rank's combine into u4 (the caller all-reduces it).
+// evaluates (W = 1: everything).  mode 0: one GPU; mode 1: emulated world (every rank's pairs on
+// this GPU, same accumulators); mode 2: real multi-GPU -> `reduce` all-reduces the int64 limbs
+// between the pair kernel and the combine.  The result is bitwise the same in every mode.
 int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done, int W,
-                  const std::vector<int>& ranks, int mode) {
+                  const std::vector<int>& ranks, int mode, const std::function<int()>& reduce) {
   const int64_t NS = ctx->npad / kSymSB;
   if (NS * kSymSB != ctx->npad) return fail(ctx, SC_EINVAL, "symmetric RPY needs npad % 512 == 0");
   if (ctx->sym_nsb != NS || ctx->sym_world != W) {  // pair tables of every rank, concatenated
@@ -667,14 +795,14 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
     ctx->sym_world = W;
     ctx->sym_off = off;
   }
-  // small N on one GPU: split every super-block pair's sources in hs parts so the grid fills
-  // 148 SMs x 3 CTAs (slots (partner, part); the unwritten ones are zeroed)
-  // hs minimises the makespan ceil(units / (3 x 148 resident CTAs)) / hs, with ~2% per-unit
-  // prologue cost per halving (C2: 136 pairs -> hs = 8, 1,088 units in 2.45 waves instead of
-  // 544 in 1.23); large N keeps hs = 1 (C3: 8,256 pairs)
+  // small N: split every super-block pair's sources in hs parts so the grid fills 148 SMs x 3
+  // CTAs; hs minimises the makespan ceil(units / (3 x 148 resident CTAs)) / hs, with ~2% per-unit
+  // prologue cost per halving (C2: 136 pairs -> hs = 8); large N keeps hs = 1.  hs depends on N
+  // only (all pairs, not this rank's), so every partial sum -- and U -- is the same for any P.
   int hs = 1;
-  if (mode == 0 && ctx->sym_variant == 0) {
-    const double units = static_cast<double>(ctx->sym_off[1] - ctx->sym_off[0]), slots = 3.0 * 148.0;
+  if (ctx->sym_variant == 0) {
+    const double units = 0.5 * static_cast<double>(NS) * static_cast<double>(NS + 1);
+    const double slots = 3.0 * (ctx->num_sms > 0 ? ctx->num_sms : 148);
     double best = 1e300;
     for (int c = 1; c <= 8; c *= 2) {
       const double cost = std::ceil(units * c / slots) / c * (1.0 + 0.02 * c);
@@ -684,29 +812,31 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
       }
     }
   }
-  if (int rc = ensure(ctx, ctx->rpy_part, static_cast<size_t>(NS) * hs * ctx->npad * 3)) return rc;
-  if (hs > 1)
-    SC_CUDA(cudaMemsetAsync(ctx->rpy_part.p, 0, sizeof(double) * NS * hs * ctx->npad * 3, ctx->stream));
+  const int64_t npad = ctx->npad;
+  const size_t nacc = static_cast<size_t>(npad) * 9;
+  if (ctx->sym_acc.n < nacc || ctx->sym_acc.p == nullptr) ctx->sym_acc_dirty = true;
+  if (int rc = ensure(ctx, ctx->sym_acc, nacc)) return rc;
+  if (int rc = ensure(ctx, ctx->fx_scale, 4)) return rc;
+  if (ctx->sym_acc_dirty)  // first use, or an apply that did not reach its combine
+    SC_CUDA(cudaMemsetAsync(ctx->sym_acc.p, 0, nacc * sizeof(long long), ctx->stream));
+  ctx->sym_acc_dirty = true;
+  FxScale* fs = reinterpret_cast<FxScale*>(ctx->fx_scale.p);
+  SC_CUDA(cudaMemsetAsync(fs, 0, sizeof(FxScale), ctx->stream));
+  timer_begin(ctx, SC_K_COMBINE);
+  fx_prep_kernel<<<static_cast<unsigned>(std::min<int64_t>((npad + 255) / 256, 4 * 148)), 256, 0, ctx->stream>>>(
+      ctx->pos4.p, f4, npad, fs, done);
+  timer_end(ctx, SC_K_COMBINE);
+  if (int rc = check_launch(ctx, "fx_prep")) return rc;
   const Consts k = make_consts(ctx->a_const);
-  static bool attr_set = false;
-  if (!attr_set) {
-#define SC_ATTR(P, NW, TPT, MINB, HS) \
-  cudaFuncSetAttribute(rpy_sym_kernel<P, NW, TPT, MINB, HS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymSmem)
-    SC_ATTR(false, 4, 4, 3, 1); SC_ATTR(true, 4, 4, 3, 1); SC_ATTR(false, 4, 4, 3, 2); SC_ATTR(true, 4, 4, 3, 2);
-    SC_ATTR(false, 4, 4, 3, 4); SC_ATTR(true, 4, 4, 3, 4); SC_ATTR(false, 4, 4, 3, 8); SC_ATTR(true, 4, 4, 3, 8);
-    SC_ATTR(false, 8, 2, 2, 1); SC_ATTR(true, 8, 2, 2, 1); SC_ATTR(false, 16, 1, 1, 1); SC_ATTR(true, 16, 1, 1, 1);
-#undef SC_ATTR
-    attr_set = true;
-  }
+  long long* acc = ctx->sym_acc.p;
   for (int r : ranks) {
     const int64_t p0 = ctx->sym_off[r], np = ctx->sym_off[r + 1] - p0;
     if (np == 0) continue;
     const unsigned g = static_cast<unsigned>(np * hs);
     const int2* pt = ctx->sym_pairs.p + p0;
     timer_begin(ctx, SC_K_RPY);
-#define SC_SYM(P, NW, TPT, MINB, HS)                                                                     \
-  rpy_sym_kernel<P, NW, TPT, MINB, HS><<<g, NW * 32, kSymSmem, ctx->stream>>>(ctx->pos4.p, f4, pt, ctx->npad, k, \
-                                                                             ctx->rpy_part.p, done)
+#define SC_SYM(P, NW, TPT, MINB, HS) \
+  rpy_sym_kernel<P, NW, TPT, MINB, HS><<<g, NW * 32, kSymSmem, ctx->stream>>>(ctx->pos4.p, f4, pt, npad, k, acc, fs, done)
     switch (ctx->sym_variant) {
       case 1: if (ctx->poly) SC_SYM(true, 8, 2, 2, 1); else SC_SYM(false, 8, 2, 2, 1); break;
       case 3: if (ctx->poly) SC_SYM(true, 16, 1, 1, 1); else SC_SYM(false, 16, 1, 1, 1); break;
@@ -726,38 +856,22 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
     timer_end(ctx, SC_K_RPY);
     if (int rc = check_launch(ctx, "rpy_sym")) return rc;
   }
+  if (mode == 2 && reduce) {
+    if (int rc = reduce()) return rc;
+  }
   const double scale = 1.0 / (8.0 * 3.14159265358979323846 * mu);
-  const int64_t npad = ctx->npad;
   const unsigned nb = static_cast<unsigned>((npad + 255) / 256);
-  auto combine = [&](int64_t s0, int64_t s1, double4* out, int64_t nse) -> int {
-    timer_begin(ctx, SC_K_COMBINE);
-    if (ctx->poly)
-      rpy_sym_combine_kernel<true><<<nb, 256, 0, ctx->stream>>>(ctx->rpy_part.p, nse, s0, s1, npad, ctx->n, scale,
-                                                               ctx->pos4.p, f4, ctx->near_ptr.p, ctx->near_idx.p,
-                                                               out, done, ctx->derr);
-    else
-      rpy_sym_combine_kernel<false><<<nb, 256, 0, ctx->stream>>>(ctx->rpy_part.p, nse, s0, s1, npad, ctx->n, scale,
-                                                                ctx->pos4.p, f4, ctx->near_ptr.p, ctx->near_idx.p,
-                                                                out, done, ctx->derr);
-    timer_end(ctx, SC_K_COMBINE);
-    return check_launch(ctx, "rpy_sym_combine");
-  };
-  if (mode == 0) return combine(0, NS * hs, u4, NS * hs);  // (all slots, in order)
-  if (mode == 2) {
-    int64_t a0, a1;
-    sym_rank_range(NS, W, ranks.front(), &a0, &a1);
-    return combine(a0, a1, u4, NS);
-  }
-  if (int rc = ensure(ctx, ctx->upart, static_cast<size_t>(W) * npad)) return rc;
-  for (int r = 0; r < W; ++r) {
-    int64_t a0, a1;
-    sym_rank_range(NS, W, r, &a0, &a1);
-    if (int rc = combine(a0, a1, ctx->upart.p + r * npad, NS)) return rc;
-  }
   timer_begin(ctx, SC_K_COMBINE);
-  sum_ranks_kernel<<<nb, 256, 0, ctx->stream>>>(ctx->upart.p, W, npad, u4, done);
+  if (ctx->poly)
+    rpy_sym_combine_kernel<true><<<nb, 256, 0, ctx->stream>>>(acc, fs, npad, ctx->n, scale, ctx->pos4.p, f4,
+                                                             ctx->near_ptr.p, ctx->near_idx.p, u4, done, ctx->derr);
+  else
+    rpy_sym_combine_kernel<false><<<nb, 256, 0, ctx->stream>>>(acc, fs, npad, ctx->n, scale, ctx->pos4.p, f4,
+                                                              ctx->near_ptr.p, ctx->near_idx.p, u4, done, ctx->derr);
   timer_end(ctx, SC_K_COMBINE);
-  return check_launch(ctx, "sum_ranks");
+  if (int rc = check_launch(ctx, "rpy_sym_combine")) return rc;
+  ctx->sym_acc_dirty = false;
+  return 0;
 }
 
 namespace {
@@ -789,12 +903,6 @@ int rpy_apply_rows(sc_ctx* ctx, const double4* f4, int64_t row0, int64_t nrows, 
   const double n2 = 4.0 * a * a;
   k.near_bits = *reinterpret_cast<const long long*>(&n2);
   dim3 grid(static_cast<unsigned>(nrows / kRpyRows), static_cast<unsigned>(ns));
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(rpy_partial_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRpySmem);
-    cudaFuncSetAttribute(rpy_partial_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRpySmem);
-    attr_set = true;
-  }
   timer_begin(ctx, SC_K_RPY);
   if (ctx->poly)
     rpy_partial_kernel<true><<<grid, kRpyThreads, kRpySmem, ctx->stream>>>(

@@ -6,6 +6,7 @@
 #include <nccl.h>
 #include <stdint.h>
 
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -40,7 +41,8 @@ struct DevScalars {
   int32_t bb_mode;
   int32_t fixed;
   int32_t err;       // contact degeneracy etc.
-  int32_t pad;
+  int32_t trace_cap; // residual trace: phi_0, phi_1, ... of the solve (sc_set_residual_trace)
+  double* trace;     // device buffer of trace_cap doubles (NULL: off)
 };
 
 struct KernelTimer {
@@ -80,6 +82,7 @@ struct sc_ctx {
   double rod_b = 0.5;
   int nwalls = 0;               // NEXT row f2: static planar walls (sc_set_walls)
   double4 walls[SC_MAX_WALLS] = {};  // (nx, ny, nz, h): plane n.x = h, unit n into the fluid
+  double wall_vel[SC_MAX_WALLS][3] = {};  // prescribed wall velocities V_k (moving boundaries)
   sc::DBuf<double4> pos4;       // spheres: (x,y,z,a/2); rods: (x,y,z,L)
   sc::DBuf<double4> dir4;       // rods: (tx,ty,tz,0)
   sc::DBuf<double4> rodmob4;    // rods: (1/zeta_par, 1/zeta_perp, 1/zeta_rot, mu) for rod_mu
@@ -126,7 +129,15 @@ struct sc_ctx {
   int sym_world = -1;           // ... and the number of ranks
   sc::DBuf<int2> sym_pairs;     // (SI, SJ) of every rank, concatenated (cyclic-half assignment)
   std::vector<int64_t> sym_off; // rank r's pairs: [sym_off[r], sym_off[r+1])
-  sc::DBuf<double4> upart;      // emulated world: per-rank partial velocities
+  sc::DBuf<long long> sym_acc;  // symmetric kernel: fixed-point limbs [npad][3 comps][3 limbs] (rpy.cu)
+  sc::DBuf<unsigned long long> fx_scale;  // ... and its per-apply scale (FxScale)
+  bool sym_acc_dirty = true;    // limbs not known to be zero (first use / interrupted apply)
+  sc::DBuf<double> trace;          // residual trace (phi per iteration) of the last solve
+  int32_t trace_cap = 0, trace_count = 0;
+  // per-device setup, done in sc_create on this context's device (kernel attributes, sizes)
+  size_t total_mem = 0;            // device memory (bytes)
+  int num_sms = 0;
+  int persist_grid = 0;            // persistent BBPGD kernel: CTAs (one per SM; 0 = not resident)
   sc::DevScalars* dsc = nullptr;   // device scalars
   sc::DevScalars* hsc = nullptr;   // pinned mirror
   int32_t* derr = nullptr;         // device error flag
@@ -198,11 +209,14 @@ int assemble(sc_ctx* ctx);
 int rpy_apply_rows(sc_ctx* ctx, const double4* f4, int64_t row0, int64_t nrows, double mu,
                    double4* u4, const int32_t* done);
 int choose_nsplit(int64_t npad, int world);
+// per-device kernel attributes (max dynamic shared memory); called by sc_create
+int rpy_init_device(sc_ctx* ctx);
+int persist_init_device(sc_ctx* ctx);
 // NEXT row f4(ii): UW (n x 6, device) = full 6N RPY grand mobility of the packed (f4, t4).
 int rpy6_apply(sc_ctx* ctx, const double4* f4, const double4* t4, double mu, double* UW);
 bool rpy_use_sym(const sc_ctx* ctx);
 int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done, int W,
-                  const std::vector<int>& ranks, int mode);
+                  const std::vector<int>& ranks, int mode, const std::function<int()>& reduce);
 
 // ---- LCP kernels (lcp.cu) -------------------------------------------------
 // gather F = D v (mode raw) or F = D max(0, gam_old - alpha g_old) with the owner
@@ -218,6 +232,8 @@ int launch_proj_own(sc_ctx* ctx, const double* gam_old, const double* g_old, dou
 int launch_dt(sc_ctx* ctx, int mode, const double* gam_new, const double* gam_old,
               const double* g_old, double* g_out, int64_t c0, int64_t c1, bool fuse);
 int launch_dt_user(sc_ctx* ctx, const double* UW, double* out, const double* addq, double qscale);
+// q = gap/dt + D^T U_nc - n_k . V_k on the constraints with moving walls
+int launch_lcp_q(sc_ctx* ctx, const double* U_nc, double inv_dt, double* q);
 int launch_finalize(sc_ctx* ctx, int mode, const double* part);
 int launch_init_g0(sc_ctx* ctx, const double* q, double* g0, int64_t c0, int64_t c1);
 int launch_pack_ft(sc_ctx* ctx, const double* FT, double4* f4, double4* t4);
@@ -227,6 +243,9 @@ int launch_rod_unpack(sc_ctx* ctx, const double4* u4, double* UW);
 int launch_count_active(sc_ctx* ctx, const double* gam, int32_t* out);
 int launch_minmap(sc_ctx* ctx, const double* gam, const double* g, int64_t nc, double* out);
 int launch_q(sc_ctx* ctx, double dt, const double* dtu, double* q);
+struct WallRates {
+  double r[SC_MAX_WALLS];  // n_k . V_k of each wall (moving boundaries; 0: static)
+};
 
 // ---- persistent small-problem BBPGD loop (persist.cu) ------------------------
 bool persist_eligible(const sc_ctx* ctx);

@@ -140,3 +140,108 @@ def test_gloo_world2_bbpgd_matches_oracle(tmp_path, name, n):
     assert m1[3] == ref["system"].ct.nc
     rel = np.linalg.norm(g0 - ref["gamma"]) / np.linalg.norm(ref["gamma"])
     assert rel < 1e-8, rel
+
+
+# ------------------------------------------------------------- symmetric RPY decomposition
+SB = 512
+
+
+def _fx_scale(force, radius, npad):
+    """The fixed-point shift s of rpy.cu (fx_shift): |row sum| * 2^s < 2^100."""
+    mf = float(np.abs(force[:, :3]).max())
+    mi = float((1.0 / radius).max())
+    B = 2.0 * mf * mi * npad
+    if not B > 0:
+        return 0
+    return int(100 - (np.floor(np.log2(B)) + 1))
+
+
+def _to_fixed(v, s):
+    """round(v 2^s) (ties away from zero) as a Python int, split in 3 limbs of 43 bits."""
+    from fractions import Fraction
+    x = Fraction(v) * (Fraction(2) ** s)
+    X = int(abs(x) + Fraction(1, 2)) * (1 if x >= 0 else -1)
+    m = (1 << 43) - 1
+    return X & m, (X >> 43) & m, X >> 86
+
+
+def _sym_rank_main(rank, world, port, name, n, outdir):
+    """Rank r evaluates its super-block pairs (the library's own table), rounds each (pair, row)
+    partial sum to the fixed-point limbs and the limbs are all-reduced (int64 sum) -- the design
+    of rpy.cu; the oracle's RPY rows stand in for the kernel."""
+    from paper_1909_06623_b200 import sym_pair_table
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p = make_problem(name, n=n)
+    n = p.n
+    npad = -(-n // SB) * SB
+    nsb = npad // SB
+    rng = np.random.default_rng(3)
+    FT = np.zeros((n, 6))
+    FT[:, :3] = rng.normal(size=(n, 3)) * 10.0 ** rng.uniform(-3, 3, size=(n, 1))
+    s = _fx_scale(FT, p.radius, npad)
+    limbs = np.zeros((npad, 3, 3), dtype=np.int64)
+
+    def add(rows, vals):
+        for r, v in zip(rows, vals):
+            for c in range(3):
+                x0, x1, x2 = _to_fixed(float(v[c]), s)
+                limbs[r, c, 0] += x0
+                limbs[r, c, 1] += x1
+                limbs[r, c, 2] += x2
+
+    def block(ti, sj):  # rows of super-block ti from the sources of super-block sj
+        r0, r1 = ti * SB, min(n, ti * SB + SB)
+        s0, s1 = sj * SB, min(n, sj * SB + SB)
+        if r1 <= r0 or s1 <= s0:
+            return np.arange(0), np.zeros((0, 3))
+        F = np.zeros_like(FT)
+        F[s0:s1] = FT[s0:s1]
+        return np.arange(r0, r1), oracle.rpy_apply_rows(p.pos, p.radius, p.mu, F, r0, r1)[:, :3]
+
+    for si, sj in sym_pair_table(nsb, world, rank):
+        add(*block(si, sj))  # forward
+        if si != sj:
+            add(*block(sj, si))  # reverse
+    t = torch.from_numpy(limbs.reshape(-1).copy())
+    dist.all_reduce(t)  # exact int64 sum
+    L = t.numpy().reshape(npad, 3, 3)[:n]
+    # carry-normalise and convert (rpy.cu fx_value), exact to one rounding
+    U = np.zeros((n, 3))
+    for i in range(n):
+        for c in range(3):
+            X = int(L[i, c, 0]) + (int(L[i, c, 1]) << 43) + (int(L[i, c, 2]) << 86)
+            U[i, c] = float(X) * 2.0 ** (-s)
+    np.save(os.path.join(outdir, f"Usym_w{world}_r{rank}.npy"), U)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,n", [("C5", 1400), ("C2", 1900)])
+def test_gloo_symmetric_rpy_decomposition(tmp_path, name, n):
+    """The default multi-GPU RPY split (symmetric super-block pairs, cyclic-half table per rank,
+    fixed-point limbs, int64 all-reduce): every rank's U equals the full oracle apply to rounding,
+    and is BITWISE the same for world 1, 2 and 3 (integer sums are order-free)."""
+    from paper_1909_06623_b200 import sym_pair_table
+    npad = -(-n // SB) * SB
+    nsb = npad // SB
+    for world in (1, 2, 3):  # the tables tile every unordered super-block pair exactly once
+        allp = np.concatenate([sym_pair_table(nsb, world, r) for r in range(world)])
+        key = {(min(a, b), max(a, b)) for a, b in allp}
+        assert len(allp) == len(key) == nsb * (nsb + 1) // 2
+    res = {}
+    for world in (1, 2, 3):
+        mp.spawn(_sym_rank_main, args=(world, _free_port(), name, n, str(tmp_path)), nprocs=world, join=True)
+        Us = [np.load(tmp_path / f"Usym_w{world}_r{r}.npy") for r in range(world)]
+        for u in Us[1:]:
+            np.testing.assert_array_equal(u, Us[0])
+        res[world] = Us[0]
+    np.testing.assert_array_equal(res[2], res[1])
+    np.testing.assert_array_equal(res[3], res[1])
+    p = make_problem(name, n=n)
+    rng = np.random.default_rng(3)
+    FT = np.zeros((n, 6))
+    FT[:, :3] = rng.normal(size=(n, 3)) * 10.0 ** rng.uniform(-3, 3, size=(n, 1))
+    ref = oracle.rpy_apply(p.pos, p.radius, p.mu, FT)[:, :3]
+    assert np.linalg.norm(res[1] - ref) / np.linalg.norm(ref) < 1e-13

@@ -64,11 +64,12 @@ def test_emulated_world_more_ranks_than_blocks(ctx):
     assert torch.equal(r["gamma"], ref["gamma"]) and torch.equal(r["Uc"], ref["Uc"])
 
 
-@pytest.mark.parametrize("name,n,max_iter,fixed", [("C5", 9000, 25, True), ("C3", 6000, 40, True)])
-def test_emulated_ranks_symmetric_kernel(ctx, name, n, max_iter, fixed):
-    """The symmetric RPY kernel's multi-GPU unit: ranks evaluate disjoint super-block pairs,
-    combine the slots they wrote and the partial velocities are summed (all-reduce).  Equal to
-    one GPU up to the grouping of that final sum."""
+@pytest.mark.parametrize("name,n,max_iter,fixed", [("C5", 9000, 25, True), ("C3", 6000, 40, True),
+                                                    ("C2", 5000, 5000, False)])
+def test_emulated_ranks_symmetric_kernel_bitwise(ctx, name, n, max_iter, fixed):
+    """The symmetric RPY kernel's multi-GPU unit: ranks evaluate disjoint super-block pairs into
+    fixed-point row accumulators whose int64 limbs are summed (all-reduce): integer sums are exact
+    and order-free, so U -- and the whole solve -- is BITWISE the one-GPU result for every P."""
     p = make_problem(name, n=n)
 
     def solve(world):
@@ -87,8 +88,6 @@ def test_emulated_ranks_symmetric_kernel(ctx, name, n, max_iter, fixed):
     ref = solve(1)
     for world in (2, 3, 8):
         r = solve(world)
-        du = (r["U_ext"] - ref["U_ext"]).norm() / ref["U_ext"].norm()
-        assert du <= 1e-14, (world, float(du))
-        dg = (r["gamma"] - ref["gamma"]).norm() / ref["gamma"].norm()
-        assert dg <= 1e-9, (world, float(dg))
-        assert r["iters"] == ref["iters"]
+        assert r["iters"] == ref["iters"] and r["residual"] == ref["residual"], world
+        for k in ("gamma", "g", "Fc", "Uc", "U_ext"):
+            assert torch.equal(r[k], ref[k]), (world, k)

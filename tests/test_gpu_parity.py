@@ -353,49 +353,41 @@ def test_c2_full_size_converged_solve(ctx):
     assert _relL2(_np(r["Fc"]), o["Fc"]) <= 1e-6
 
 
+def _full_certificate(p, r):
+    """One oracle MVOP on the GPU's gamma over EVERY constraint (SURVEY.md section 8(c) "Large
+    LCPs"; Eq. abserrcqp): g_oracle = gap/dt + D^T M (F_ext + D gamma) with the
+    oracle's contacts, D and long-double RPY sums -- independent of every GPU kernel."""
+    gam = _np(r["gamma"])
+    sysm = oracle.system_for(p)
+    F = oracle.apply_D(p.n, sysm.ct, gam) + p.force
+    go = sysm.lcp_q(p.dt, sysm.mobility(F))
+    return gam, go, float(np.linalg.norm(np.minimum(gam, go)))
+
+
 def test_c3_full_size_converged_certificate(ctx):
-    """C3 at full size, converged: the GPU's gamma certified by the oracle's RPY rows on sampled
-    constraints (g_l = n.(U_i - U_j) + q_l with U = RPY(F_ext + D gamma)); complementarity holds."""
+    """C3 at full size (65,536 spheres, phi = 0.5), converged: gamma_GPU >= 0 and the
+    complementarity residual phi(gamma_GPU, g_oracle) over all 148k constraints within the
+    tolerance; the GPU's own g agrees with the oracle's to 1e-8 absolute everywhere."""
     p = make_problem("C3")
     r = _gpu_solve(ctx, p)
     assert r["status"] == 0 and r["converged"] == 1 and r["residual"] < 1e-8
-    gam = _np(r["gamma"])
-    ct = oracle.contacts_spheres(p.pos, p.radius, p.gap_abs, p.gap_rel)
-    F = oracle.apply_D(p.n, ct, gam) + p.force
-    rng = np.random.default_rng(8)
-    ls = rng.choice(ct.nc, 24, replace=False)
-    g = _np(r["g"])
-    for l in ls:
-        i, j = ct.i[l], ct.j[l]
-        ui = oracle.rpy_apply_rows(p.pos, p.radius, p.mu, F, i, i + 1)[0]
-        uj = oracle.rpy_apply_rows(p.pos, p.radius, p.mu, F, j, j + 1)[0]
-        go = float(np.dot(ct.normal[l], ui[:3] - uj[:3])) + ct.gap[l] / p.dt
-        assert abs(g[l] - go) <= 1e-8 * (1 + abs(go)), (l, g[l], go)
-        assert min(gam[l], go) > -1e-8 and (gam[l] == 0 or abs(go) < 1e-7 * (1 + gam[l]))
+    gam, go, phi = _full_certificate(p, r)
+    assert gam.min() >= 0.0
+    assert np.abs(_np(r["g"]) - go).max() <= 1e-8
+    assert phi <= 1e-8, phi
 
 
 def test_c5_full_size_converged_certificate(ctx):
-    """C5 at full size (262,144 spheres) solved to convergence (~500 iterations, ~45 s): a
-    converged oracle run is hours, so the GPU's gamma is certified by the oracle's RPY rows on
-    sampled constraints (half of them active): g_l = n.(U_i - U_j) + gap_l/dt with
-    U = RPY(F_ext + D gamma) matches the GPU's g, and min(gamma_l, g_l) ~ 0."""
+    """C5 at full size (262,144 spheres) solved to convergence: a converged oracle run is hours,
+    so the GPU's gamma is certified by one oracle MVOP over all 358,609 constraints (~3 min on
+    the host cores): gamma >= 0, phi(gamma_GPU, g_oracle) within the tolerance."""
     p = make_problem("C5", fixed_iters=0)
     r = _gpu_solve(ctx, p)
     assert r["status"] == 0 and r["converged"] == 1 and r["residual"] < 1e-8
-    gam = _np(r["gamma"])
+    gam, go, phi = _full_certificate(p, r)
     assert gam.min() >= 0.0
-    ct = oracle.contacts_spheres(p.pos, p.radius, p.gap_abs, p.gap_rel)
-    F = oracle.apply_D(p.n, ct, gam) + p.force
-    rng = np.random.default_rng(11)
-    ls = np.concatenate([rng.choice(np.flatnonzero(gam > 0), 12, replace=False), rng.choice(ct.nc, 12, replace=False)])
-    g = _np(r["g"])
-    for l in ls:
-        i, j = ct.i[l], ct.j[l]
-        ui = oracle.rpy_apply_rows(p.pos, p.radius, p.mu, F, i, i + 1)[0]
-        uj = oracle.rpy_apply_rows(p.pos, p.radius, p.mu, F, j, j + 1)[0]
-        go = float(np.dot(ct.normal[l], ui[:3] - uj[:3])) + ct.gap[l] / p.dt
-        assert abs(g[l] - go) <= 1e-8 * (1 + abs(go)), (l, g[l], go)
-        assert abs(min(gam[l], go)) < 1e-9, (l, gam[l], go)
+    assert np.abs(_np(r["g"]) - go).max() <= 1e-8
+    assert phi <= 1e-8, phi
 
 
 @pytest.mark.parametrize("name,n,walls", [("C1", None, None), ("C2", 1000, None), ("C1", None, "box"),

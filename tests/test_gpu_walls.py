@@ -197,3 +197,92 @@ def test_full_rpy_with_floor(ctx):
     assert r["status"] == 0 and o["status"] == 0 and r["residual"] < 1e-8
     assert _relL2(_np(r["gamma"]), o["gamma"]) <= 1e-6
     assert _relL2(_np(r["Uc"]), o["Uc"]) <= 1e-6
+
+
+def test_bb_breakdown_rule_squeezed_sphere(ctx):
+    """Reading A5 on the GPU (and the oracle), a case where s^T y = 0 really occurs: sphere A
+    (a = 1) squeezed between a floor z = 0 and a ceiling z = 1.5 (both gaps -0.25, bitwise equal),
+    and sphere B (a = 0.5) near A (pair gap 0.02 > 0), no external force.  The two wall columns of
+    A are +e_z and -e_z, so z = (1, 1, 0) spans null(D^T M D); q = (g_w/dt, g_w/dt, 0.02/dt).
+    alpha_0 = |q|^2 / q^T M q is finite (the pair column), gamma_1 = -alpha_0 (q_1, q_1, 0) is in
+    null(M): y = 0, s^T y = 0 -> breakdown; the LCP is infeasible (A cannot leave both walls), so
+    every iteration breaks down, gamma grows linearly, status SC_NOT_CONVERGED and
+    bb_breakdowns = iterations on both sides (Steps 14-15 run at j = j_max too)."""
+    pos = np.array([[0.0, 0.0, 0.75], [1.52, 0.0, 0.75]])
+    rad = np.array([1.0, 0.5])
+    walls = np.array([[0.0, 0.0, 1.0, 0.0], [0.0, 0.0, -1.0, -1.5]])
+    F = np.zeros((2, 6))
+    dt = 0.01
+    ctx.set_walls(walls)
+    for J in (1, 5, 40):
+        ctx.build_contacts_spheres(_cuda(pos), _cuda(rad), 0.0, 0.1)
+        c = ctx.get_contacts()
+        np.testing.assert_array_equal(_np(c["i"]), [0, 0, 0])
+        np.testing.assert_array_equal(_np(c["j"]), [1, 2, 3])
+        ctx.assemble_D()
+        U = ctx.mobility_apply(_cuda(F))
+        ctx.lcp_q(dt, U)
+        r = ctx.bbpgd_solve(tol=1e-8, max_iter=J)
+        ct = oracle.merge_contacts(oracle.contacts_spheres(pos, rad, 0.0, 0.1),
+                                   oracle.contacts_walls("spheres", pos, walls, radius=rad, gap_abs=0.0,
+                                                         gap_rel=0.1))
+        sysm = oracle.System(oracle.ORC_SPHERES, 2, ct, pos=pos, radius=rad)
+        q = sysm.lcp_q(dt, sysm.mobility(F))
+        o = sysm.bbpgd(q, tol=1e-8, max_iter=J)
+        gam = _np(r["gamma"])
+        assert r["status"] == 1 and o["status"] == 1
+        assert r["bb_breakdowns"] == J and o["bb_breakdowns"] == J and r["iters"] == J == o["iters"]
+        assert gam[1] == gam[2] and gam[0] == 0.0 and gam[1] > 0  # grows along the null direction
+        np.testing.assert_allclose(gam, o["gamma"], rtol=1e-12, atol=0)
+        # gamma_J = J alpha_0 |q_w| (alpha kept at alpha_0; g_j = q)
+        assert gam[1] == pytest.approx(J * r["alpha"] * abs(q[1]), rel=1e-12)
+    ctx.set_walls(None)
+
+
+@pytest.mark.parametrize("name,n,walls", [("C2", 3000, "floor"), ("C4", 20000, "box"), ("C1", None, "box")])
+def test_moving_walls_q_and_solve_vs_oracle(ctx, name, n, walls):
+    """Moving boundaries: q = gap/dt + D^T U_ext - n_k.V_k on wall rows (the
+    oracle's orc_lcp_q_moving_walls), and the converged solve against the oracle's."""
+    p = make_problem(name, n=n, walls=walls, fixed_iters=0)
+    rng = np.random.default_rng(7)
+    V = rng.normal(size=(len(p.walls), 3)) * 5.0
+    _gpu_contacts(ctx, p)
+    ctx.set_wall_velocities(V)
+    ctx.assemble_D()
+    F = _cuda(p.force)
+    U = ctx.mobility_apply(F, mu=p.mu)
+    q = _np(ctx.lcp_q(p.dt, U))
+    r = ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=p.max_iter)
+    sysm = oracle.system_for(p)
+    Uo = sysm.mobility(p.force)
+    qo = sysm.lcp_q_moving_walls(p.dt, Uo, V)
+    np.testing.assert_allclose(q, qo, rtol=0, atol=1e-12 * np.abs(qo).max())
+    o = sysm.bbpgd(qo, tol=p.tol, max_iter=p.max_iter)
+    assert r["status"] == 0 and o["status"] == 0
+    assert _relL2(_np(r["gamma"]), o["gamma"]) <= 1e-6
+    ctx.set_walls(None)
+
+
+def test_moving_floor_closed_form_and_time_step(ctx):
+    """One sphere above a floor moving up with V (F = 0): gamma = max(0, 6 pi (V - gap/dt)); the
+    time step moves the plane to h + dt V_z and the sphere with the floor when in contact."""
+    dt = 0.01
+    pos = np.array([[0.0, 0.0, 1.05]])
+    for V, expect in ((10.0, 6 * np.pi * (10.0 - 5.0)), (3.0, 0.0)):
+        ctx.set_walls([[0.0, 0.0, 1.0, 0.0]])
+        ctx.set_wall_velocities([[0.5, 0.0, V]])
+        ctx.build_contacts_spheres(_cuda(pos), None, 0.0, 0.1)
+        ctx.assemble_D()
+        ctx.lcp_q(dt, ctx.mobility_apply(_cuda(np.zeros((1, 6)))))
+        r = ctx.bbpgd_solve(tol=1e-10, max_iter=50)
+        assert float(r["gamma"][0]) == pytest.approx(expect, rel=1e-12, abs=1e-12)
+        quat = torch.tensor([[1.0, 0.0, 0.0, 0.0]], dtype=torch.float64, device="cuda")
+        out = ctx.time_step("spheres", _cuda(pos), _cuda(np.zeros((1, 6))), dt=dt, tol=1e-10, quat=quat)
+        w = ctx.get_walls()
+        assert w[0, 3] == pytest.approx(dt * V, rel=1e-15)
+        z1 = float(out["pos"][0, 2])
+        if expect > 0:  # pushed by the floor: the linearised gap closes exactly at the step end
+            assert z1 == pytest.approx(1.0 + dt * V, rel=1e-12)
+        else:
+            assert z1 == 1.05
+    ctx.set_walls(None)

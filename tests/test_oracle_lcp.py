@@ -212,3 +212,42 @@ def test_torques_are_inert_for_spheres():
     p.force[:, 3:] = 0.0
     r2 = oracle.solve_problem(p, max_iter=30, fixed_iters=1)
     np.testing.assert_array_equal(r1["gamma"], r2["gamma"])
+
+
+# ---------------------------------------------------------------- reading A5 (BB breakdown)
+def test_bb_breakdown_step_in_null_space_closed_form():
+    """Reading A5 pinned by a closed form.  M = [[1,-1,0],[-1,1,0],[0,0,1]] is SPSD with null
+    vector z = (1,1,0); q = (-1,-1,1).  Step 6: alpha_0 = |q|^2 / q^T M q = 3/1 = 3.  Step 8-9:
+    gamma_1 = max(0, -3q) = (3,3,0) = 3z, so s = 3z lies in null(M): y = M s = 0 and s^T y = 0 --
+    a BB breakdown (BB1 3/0 and BB2 0/0 are both undefined).  Rule A5 keeps alpha = 3, so
+    g_j = q for every j and gamma_j = 3j (1,1,0) exactly (integers), phi_j = |(-1,-1,0)| = sqrt 2
+    (the LCP is infeasible: q^T z < 0), and every iteration, the last included (Steps 14-15 are in
+    the loop body of Alg. 1), counts one breakdown.  A slip (accepting the undefined
+    step, not counting it, or skipping the rule) changes gamma, the status or the count."""
+    M = np.array([[1.0, -1.0, 0.0], [-1.0, 1.0, 0.0], [0.0, 0.0, 1.0]])
+    q = np.array([-1.0, -1.0, 1.0])
+    for bb_mode in (0, 1, 2):
+        for J in (1, 2, 7):
+            r = oracle.bbpgd_dense(M, q, tol=1e-8, max_iter=J, bb_mode=bb_mode)
+            assert r["status"] == 1 and r["converged"] == 0
+            np.testing.assert_array_equal(r["gamma"], [3.0 * J, 3.0 * J, 0.0])
+            np.testing.assert_array_equal(r["g"], q)
+            assert r["bb_breakdowns"] == J and r["iters"] == J and r["mvops"] == J + 2
+            assert r["residual"] == pytest.approx(np.sqrt(2.0), rel=1e-15)
+
+
+def test_bb_breakdown_negative_curvature_keeps_alpha():
+    """Reading A5 on s^T y < 0 (a plausible slip would accept the negative BB1 step).
+    M = diag(1, -2), q = (3, -1) (M indefinite: a unit pin of the rule, not a physical system).
+    alpha_0 = |q|^2 / q^T M q = 10/7; gamma_1 = max(0, -alpha_0 q) = (0, 10/7); s = gamma_1,
+    y = M s = (0, -20/7), s^T y = -200/49 < 0: breakdown, alpha stays 10/7; g_1 = (3, -27/7);
+    gamma_2 = max(0, gamma_1 - (10/7) g_1) = (0, 340/49); again s^T y < 0: 2 breakdowns."""
+    M = np.diag([1.0, -2.0])
+    q = np.array([3.0, -1.0])
+    r = oracle.bbpgd_dense(M, q, tol=1e-12, max_iter=2)
+    assert r["bb_breakdowns"] == 2 and r["iters"] == 2
+    np.testing.assert_allclose(r["gamma"], [0.0, 340.0 / 49.0], rtol=1e-14, atol=0)
+    r1 = oracle.bbpgd_dense(M, q, tol=1e-12, max_iter=1)
+    np.testing.assert_allclose(r1["gamma"], [0.0, 10.0 / 7.0], rtol=1e-15, atol=0)
+    np.testing.assert_allclose(r1["g"], [3.0, -27.0 / 7.0], rtol=1e-15, atol=0)
+    assert r1["bb_breakdowns"] == 1

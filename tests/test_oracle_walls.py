@@ -155,3 +155,49 @@ def test_floor_lcp_vs_enumeration(n, seed):
     assert best is not None
     r = sysm.bbpgd(q, tol=1e-10, max_iter=20000)
     np.testing.assert_allclose(r["gamma"], best, rtol=0, atol=1e-6 * (1 + np.abs(best).max()))
+
+
+# ------------------------------------------------------------------ moving boundaries
+def test_moving_floor_single_sphere_closed_form():
+    """A boundary may move with a prescribed velocity; D is unchanged and the gap
+    rate becomes n.(U_i - V_k), so q = gap/dt + D^T U_ext - n.V.  One sphere (a = mu = 1) at
+    height z above a floor n = e_z moving with V, pushed down by F: A = 1/(6 pi), q = (z - 1)/dt
+    - F/(6 pi) - V_z, gamma = max(0, -q/A) = max(0, F + 6 pi (V_z - (z - 1)/dt)).  Tangential
+    floor velocity does not enter (n.V = 0)."""
+    dt = 0.01
+    walls = np.array([[0.0, 0.0, 1.0, 0.0]])
+    for z, F, V in [(1.05, 0.0, 10.0), (1.05, 0.0, 3.0), (0.98, 1.0, -1.0), (1.0, 0.0, 0.0),
+                    (1.02, 5.0, 0.5), (1.05, 2.0, -20.0)]:
+        pos = np.array([[0.3, -0.2, z]])
+        ct = oracle.contacts_walls("spheres", pos, walls, radius=np.ones(1), gap_abs=0.0, gap_rel=0.1)
+        assert ct.nc == 1
+        sysm = oracle.System(oracle.ORC_SPHERES, 1, ct, pos=pos, radius=np.ones(1))
+        FT = np.zeros((1, 6))
+        FT[0, 2] = -F
+        U = sysm.mobility(FT)
+        for vel, vz in (([0.0, 0.0, V], V), ([2.0, -1.5, V], V)):
+            q = sysm.lcp_q_moving_walls(dt, U, [vel])
+            assert q[0] == pytest.approx((z - 1.0) / dt - F / (6 * np.pi) - vz, rel=1e-14, abs=1e-12)
+            r = sysm.bbpgd(q, tol=1e-10, max_iter=50)
+            expect = max(0.0, F + 6 * np.pi * (vz - (z - 1.0) / dt))
+            assert r["gamma"][0] == pytest.approx(expect, rel=1e-12, abs=1e-12)
+        # static wall: the moving-wall q with V = 0 is the static q
+        np.testing.assert_array_equal(sysm.lcp_q_moving_walls(dt, U, [[0.0, 0.0, 0.0]]), sysm.lcp_q(dt, U))
+
+
+def test_moving_walls_only_shift_wall_rows_of_q():
+    """Pair constraints are untouched by wall velocities; each wall row moves by -n_k.V_k."""
+    p = make_problem("C2", n=600, walls="box")
+    sysm = oracle.system_for(p)
+    U = sysm.mobility(p.force)
+    q0 = sysm.lcp_q(p.dt, U)
+    rng = np.random.default_rng(4)
+    V = rng.normal(size=(len(p.walls), 3))
+    q1 = sysm.lcp_q_moving_walls(p.dt, U, V)
+    ct = sysm.ct
+    wall = ct.j >= p.n
+    assert wall.sum() > 0
+    np.testing.assert_array_equal(q1[~wall], q0[~wall])
+    k = ct.j[wall] - p.n
+    np.testing.assert_allclose(q1[wall], q0[wall] - np.einsum("lc,lc->l", ct.normal[wall], V[k]), rtol=0,
+                               atol=1e-12 * np.abs(q0).max())
