@@ -6,7 +6,10 @@ fixed 50 iterations (BASELINE.json configs[4]: 262,144 spheres, volume fraction
 0.3).  All inside one C-ABI call (sc_collision_step) with inputs resident in HBM.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-  torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: RPY rows sharded)
+  torchrun --nproc-per-node N bench.py --gpus N ...
+      (N > 1: each rank evaluates its share of the symmetric RPY kernel's super-block pairs into
+       fixed-point row accumulators, all-reduced exactly as int64 over NCCL; constraints are owned
+       by the rank of their first body)
 
 Prints ONE JSON line on rank 0.  value = whole-job RPY pair-interactions per
 second (every executed RPY apply counts N(N-1) pairs), device-timed with CUDA
@@ -184,6 +187,9 @@ def main():
 
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL's communicator-init lines (nranks, ring/NVLS setup) go to stderr for the driver
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -245,9 +251,8 @@ def main():
     value = applies_per_step * pairs_per_apply / (ms_step / 1e3)
     # roofline of the dominant kernel (RPY), live CUDA-event timing on the library stream
     rpy_ms, rpy_n = tim["rpy"]
-    rows_here = ctx_rows(n, world, rank)
     rpy_avg_ms = rpy_ms / max(rpy_n, 1)
-    flops_launch = FLOPS_PER_PAIR * rows_here * (n - 1)
+    flops_launch = FLOPS_PER_PAIR * rank_ordered_pairs(n, world, rank)
     achieved = flops_launch / (rpy_avg_ms / 1e3) / 1e12
     kern = "rpy_sym_kernel" if n >= 4096 else "rpy_partial_kernel"
     prof = ncu_profile_summary(kern)
@@ -270,7 +275,8 @@ def main():
            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": _config(args, world),
            "bbpgd_iters_per_s": FIXED_ITERS / (ms_step / 1e3), "pct_fp64_peak": 100 * roofline["frac"],
            "n_c": r["nc"], "mvops": r["mvops"], "residual": r["residual"], "roofline": roofline,
-           "kernel_time_share": share, "clocks": clocks, "gpu_launches": launches}
+           "kernel_time_share": share, "clocks": clocks, "gpu_launches": launches,
+           "nccl": ctx.comm_info()}
     # e2e: the same call with HOST (pinned) buffers, copies inside the timed region
     if not args.no_e2e:
         hpos = torch.as_tensor(p.pos).pin_memory()
@@ -302,38 +308,77 @@ def main():
         dist.destroy_process_group()
 
 
+HBM_GBS = 6534.5  # MEASURED_PEAKS.json hbm_gbs (copy bandwidth) on this pool; read live when present
+
+
+def _hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_GBS, "measured (round-1 copy of MEASURED_PEAKS.json)"
+
+
 def other_configs():
-    """Time to solution (device-timed, CUDA events on the library stream around one
-    sc_collision_step, inputs resident) of the converged BASELINE configs that take
-    milliseconds: C1 (512 spheres, the persistent loop), C2 (8,192 polydisperse spheres) and C4
-    (200,000 rods).  Context for the
-    BBPGD-iterations/s half of the metric; not part of `value`."""
+    """Time to solution (device-timed, CUDA events on the library stream around the solve, inputs
+    resident) of the converged BASELINE configs: C1 (512 spheres, persistent loop), C2 (8,192
+    polydisperse spheres), C3 (65,536 spheres, phi = 0.5), C4 (200,000 rods, persistent loop) and
+    C5 converged (262,144 spheres).  Plus the HBM roofline of the D-gather (a3) and D^T (a5)
+    kernels from a second solve with CUDA events around every launch (algorithmic bytes of
+    SURVEY.md section 8(d): spheres 96 B/constraint + 28 B/body and 120 B/constraint, rods
+    144 B/constraint + 84 B/body and 216 B/constraint).  Context for the BBPGD-iterations/s half of
+    the metric; not part of `value`."""
     import torch
 
     from paper_1909_06623_b200 import Context
     from paper_1909_06623_b200.synthetic import make_problem
+    peak, peak_kind = _hbm_peak()
     res = {}
-    for name in ("C1", "C2", "C4"):
+    for name, reps in (("C1", 5), ("C2", 5), ("C4", 5), ("C3", 1), ("C5", 1)):
         p = make_problem(name, fixed_iters=0)
         t = lambda a: None if a is None else torch.as_tensor(a, device="cuda:0")
         ctx = Context(0)
-        args = (p.kind, t(p.pos), t(p.force))
-        kw = dict(radius=t(p.radius), direction=t(p.direction), length=t(p.length), b=p.rod_radius,
-                  gap_abs=p.gap_abs, gap_rel=p.gap_rel, mu=p.mu, dt=p.dt, tol=p.tol, max_iter=p.max_iter)
-        ctx.collision_step(*args, **kw)
+        if p.kind == "spheres":
+            nc = ctx.build_contacts_spheres(t(p.pos), t(p.radius), p.gap_abs, p.gap_rel)
+        else:
+            nc = ctx.build_contacts_rods(t(p.pos), t(p.direction), t(p.length), p.rod_radius, p.gap_abs)
+        ctx.assemble_D()
+        ctx.lcp_q(p.dt, ctx.mobility_apply(t(p.force), mu=p.mu))
+        solve = lambda: ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=p.max_iter, want_Fc=False, want_Uc=False)
+        solve()
         s = ctx.torch_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(s)
-        reps = 5
         for _ in range(reps):
-            r = ctx.collision_step(*args, **kw)
+            r = solve()
         e1.record(s)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
-        res[name] = {"n": p.n, "n_c": r["nc"], "bbpgd_iters": r["iters"], "residual": r["residual"],
-                     "converged": r["converged"], "time_to_solution_ms": ms,
-                     "bbpgd_iters_per_s": r["iters"] / (ms / 1e3)}
+        d = {"n": p.n, "n_c": nc, "bbpgd_iters": r["iters"], "residual": r["residual"],
+             "converged": r["converged"], "time_to_solution_ms": ms,
+             "bbpgd_iters_per_s": r["iters"] / (ms / 1e3), "us_per_iter": 1e3 * ms / max(r["iters"], 1)}
+        if name in ("C4", "C5"):  # HBM roofline of the a3 / a5 kernels (event-timed launch path)
+            ctx.set_timing(True)
+            ctx.reset_timing()
+            r2 = ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=min(p.max_iter, 60), fixed_iters=True,
+                                 want_Fc=False, want_Uc=False)
+            tim = ctx.get_timing()
+            ctx.set_timing(False)
+            rods = p.kind == "rods"
+            gb = (144 if rods else 96) * nc + (84 if rods else 28) * p.n
+            db = (216 if rods else 120) * nc
+            gus = 1e3 * tim["gather"][0] / max(tim["gather"][1], 1)
+            dus = 1e3 * tim["dt"][0] / max(tim["dt"][1], 1)
+            d["roofline_hbm"] = {
+                "peak_gbs": peak, "peak_kind": peak_kind, "l2": "not flushed (the loop's working set)",
+                "gather": {"algorithmic_bytes": gb, "avg_launch_us": gus, "achieved_gbs": gb / gus / 1e3,
+                           "frac": gb / gus / 1e3 / peak, "launches": tim["gather"][1]},
+                "dt": {"algorithmic_bytes": db, "avg_launch_us": dus, "achieved_gbs": db / dus / 1e3,
+                       "frac": db / dus / 1e3 / peak, "launches": tim["dt"][1]},
+                "iteration_frac": (gb + db) / (d["us_per_iter"] * 1e3) / peak,
+                "note": "iteration_frac: algorithmic bytes of gather + D^T per iteration / time to solution "
+                        "per iteration (the persistent rods loop has no per-kernel events)"}
+        res[name] = d
         ctx.close()
     return res
 
@@ -367,10 +412,18 @@ def ncu_profile_summary(kernel):
     return best
 
 
-def ctx_rows(n, world, rank):
-    from paper_1909_06623_b200 import plan_partition
-    pp = plan_partition(n, world, rank)
-    return pp["row_hi"] - pp["row_lo"]
+def rank_ordered_pairs(n, world, rank):
+    """Ordered RPY pairs this rank's kernel launches evaluate per apply: the symmetric kernel's
+    super-block pairs of this rank (a diagonal super-block pair holds 512 x 511 ordered pairs, an
+    off-diagonal one 2 x 512^2), or the target-row kernel's rows x (N - 1) below N = 4096."""
+    from paper_1909_06623_b200 import plan_partition, sym_pair_table
+    if n < 4096:
+        pp = plan_partition(n, world, rank)
+        return (pp["row_hi"] - pp["row_lo"]) * (n - 1)
+    nsb = -(-n // 512)
+    t = sym_pair_table(nsb, world, rank)
+    diag = int((t[:, 0] == t[:, 1]).sum())
+    return diag * 512 * 511 + (len(t) - diag) * 2 * 512 * 512
 
 
 if __name__ == "__main__":

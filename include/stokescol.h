@@ -162,6 +162,19 @@ int sc_lcp_q(sc_ctx* ctx, double dt, const double* U_nc, double* q_out);
  * D^T M D only involves the translational blocks).  On a multi-GPU context every rank
  * evaluates all rows of this apply.  Errors: SC_EINVAL for another model. */
 int sc_set_mobility_model(sc_ctx* ctx, int model);
+/* ---------------------------- NEXT row f4(i): fast O(N) summation of the RPY apply */
+/* model 2 (sc_set_mobility_model): the BASELINE RPY mobility (model 0's operator) evaluated by a
+ * Chebyshev-interpolation ("black-box") FMM on a uniform octree, the O(N) route the paper takes
+ * with KIFMM: far field = the RPY far branch between the Chebyshev nodes of
+ * well-separated boxes (n^3 nodes per box, n = order), near field (the 27 leaves around a body,
+ * every overlapping pair included) = the exact pair sum.  Approximate: the relative error of the
+ * apply falls with the order (measured rel. L2 errors); every sum is in a
+ * fixed order (deterministic).  Monodisperse spheres on a 1-GPU context (SC_EINVAL otherwise); used
+ * by sc_mobility_apply, sc_lcp_q's U_ext and every BBPGD MVOP.  leaf_level 0 = chosen from N and the
+ * order (leaf side >= 2a).  Errors: SC_EINVAL (order not 4/6/8, leaf_level outside 0..8). */
+int sc_set_fmm_params(sc_ctx* ctx, int order, int leaf_level);
+/* out3 = {order, leaf level of the current tree (0: not built yet), tree built (0/1)} */
+int sc_get_fmm_info(const sc_ctx* ctx, int32_t* out3);
 
 /* ------------------------------------------------------- residual (SPEC) */
 /* phi = || min(gamma, g) ||_2, the min-map complementarity residual of the LCP (

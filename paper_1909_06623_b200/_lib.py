@@ -27,6 +27,7 @@ EXPORTS = [
     "sc_plan_partition", "sc_set_emulated_world", "sc_set_rpy_kernel", "sc_time_step", "sc_apgd_solve",
     "sc_set_walls", "sc_set_mobility_model", "sc_minmap_residual", "sc_set_residual_trace",
     "sc_get_residual_trace", "sc_comm_info", "sc_sym_pair_table", "sc_set_wall_velocities", "sc_get_walls",
+    "sc_set_fmm_params", "sc_get_fmm_info",
 ]
 
 
@@ -103,11 +104,15 @@ def load(build_if_missing: bool = True):
         "sc_sym_pair_table": (ci, [i64, ci, ci, vp, C.POINTER(i64)]),
         "sc_set_wall_velocities": (ci, [vp, ci, vp]),
         "sc_get_walls": (ci, [vp, vp]),
+        "sc_set_fmm_params": (ci, [vp, ci, ci]),
+        "sc_get_fmm_info": (ci, [vp, vp]),
         "sc_apgd_solve": (ci, [vp, C.POINTER(BbpgdOpts), vp, vp, C.POINTER(BbpgdStats)]),
         "sc_time_step": (ci, [vp, C.POINTER(Problem), C.POINTER(BbpgdOpts), vp, vp, vp, vp, C.POINTER(i64),
                               C.POINTER(BbpgdStats)]),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("SC_LIB") and not hasattr(lib, name):
+            continue  # an older A/B build without this entry point
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args

@@ -166,10 +166,22 @@ class Context:
 
     # --------------------------------------------------- NEXT row f4(ii)
     def set_mobility_model(self, model):
-        """"rpy" (BASELINE: translational RPY + self rotation) or "rpy6" (full 6N RPY grand
-        mobility with the translation-rotation and rotation-rotation pair blocks)."""
-        m = {"rpy": 0, "rpy6": 1}[model] if isinstance(model, str) else int(model)
+        """"rpy" (BASELINE: translational RPY + self rotation), "rpy6" (full 6N RPY grand
+        mobility with the translation-rotation and rotation-rotation pair blocks) or "rpy_fmm"
+        (the "rpy" operator by the fast O(N) summation, NEXT row f4(i))."""
+        m = {"rpy": 0, "rpy6": 1, "rpy_fmm": 2}[model] if isinstance(model, str) else int(model)
         self._rc(self.lib.sc_set_mobility_model(self._h, m))
+
+    # --------------------------------------------------- NEXT row f4(i)
+    def set_fmm_params(self, order=6, leaf_level=0):
+        """Order (Chebyshev nodes per dimension: 4, 6 or 8) and leaf level (0: automatic) of the
+        fast RPY summation used with set_mobility_model("rpy_fmm")."""
+        self._rc(self.lib.sc_set_fmm_params(self._h, int(order), int(leaf_level)))
+
+    def fmm_info(self) -> dict:
+        out = (C.c_int32 * 3)()
+        self._rc(self.lib.sc_get_fmm_info(self._h, out))
+        return dict(zip(["order", "leaf_level", "ready"], list(out)))
 
     # ------------------------------------------------------------- (a1)
     def build_contacts_spheres(self, pos, radius=None, gap_abs=0.0, gap_rel=0.1) -> int:

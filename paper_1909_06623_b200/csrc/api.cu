@@ -251,6 +251,10 @@ struct Dist {
   // row accumulators, the int64 limbs are all-reduced (exact), and every rank combines all rows.
   // Target-row kernel: own rows, then all-gather of the rows.
   int rpy(double mu, const int32_t* done) {
+    if (ctx->mobility_model == 2) {  // NEXT row f4(i): the fast summation (one GPU)
+      if (on && !emul) return fail(ctx, SC_EINVAL, "the fast RPY summation runs on a 1-GPU context");
+      return fmm_apply(ctx, ctx->f4.p, mu, ctx->u4.p, done);
+    }
     if (rpy_use_sym(ctx)) {
       if (!on) return rpy_apply_sym(ctx, ctx->f4.p, mu, ctx->u4.p, done, 1, mine, 0, nullptr);
       if (emul) return rpy_apply_sym(ctx, ctx->f4.p, mu, ctx->u4.p, done, W, mine, 1, nullptr);
@@ -362,6 +366,7 @@ __global__ void rod_mob_kernel(const double4* __restrict__ pos4, int64_t n, doub
 static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 static int prepare_bodies(sc_ctx* ctx, int kind, int64_t n) {
+  ctx->fmm_ready = false;  // (the fast summation's tree follows the bodies)
   ctx->kind = kind;
   ctx->n = n;
   ctx->npad = round_up(std::max<int64_t>(n, 1), kNpadQuantum);
@@ -570,6 +575,7 @@ void sc_destroy(sc_ctx* ctx) {
   release(ctx->rpy6_part); release(ctx->ft_tmp); release(ctx->row_ptr); release(ctx->inc); release(ctx->icol4); release(ctx->first_ptr); release(ctx->near_ptr); release(ctx->near_idx);
   release(ctx->q); release(ctx->gam[0]); release(ctx->gam[1]); release(ctx->g[0]); release(ctx->g[1]);
   release(ctx->w); release(ctx->gam_user); release(ctx->uc); release(ctx->prev_key); release(ctx->prev_gam); release(ctx->chunk_part); release(ctx->chunk_red);
+  release(ctx->fmm_key); release(ctx->fmm_idx0); release(ctx->fmm_sidx); release(ctx->fmm_cnt); release(ctx->fmm_lstart); release(ctx->fmm_cubtmp); release(ctx->fmm_spos4); release(ctx->fmm_sf4); release(ctx->fmm_M); release(ctx->fmm_L); release(ctx->fmm_lev_off_dev);
   release(ctx->sym_pairs); release(ctx->sym_acc); release(ctx->fx_scale); release(ctx->trace); release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);
   release(ctx->bbox_part); release(ctx->cell_of); release(ctx->cell_cnt); release(ctx->cell_start);
   release(ctx->sorted_idx); release(ctx->pair_cnt); release(ctx->pair_off); release(ctx->scan_tmp);
@@ -631,8 +637,27 @@ int sc_minmap_residual(sc_ctx* ctx, int64_t n_c, const double* gamma, const doub
 // ------------------------------------------------------------ NEXT row f4(ii)
 int sc_set_mobility_model(sc_ctx* ctx, int model) {
   if (ctx == nullptr) return SC_EINVAL;
-  if (model != 0 && model != 1) return fail(ctx, SC_EINVAL, "set_mobility_model: 0 (RPY) or 1 (full 6N RPY)");
+  if (model < 0 || model > 2)
+    return fail(ctx, SC_EINVAL, "set_mobility_model: 0 (RPY), 1 (full 6N RPY) or 2 (RPY by the fast summation)");
   ctx->mobility_model = model;
+  return SC_OK;
+}
+
+int sc_set_fmm_params(sc_ctx* ctx, int order, int leaf_level) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if ((order != 4 && order != 6 && order != 8) || leaf_level < 0 || leaf_level > 8)
+    return fail(ctx, SC_EINVAL, "set_fmm_params: order 4, 6 or 8; leaf_level 0 (auto) .. 8");
+  ctx->fmm_order = order;
+  ctx->fmm_leaf_level = leaf_level;
+  ctx->fmm_ready = false;
+  return SC_OK;
+}
+
+int sc_get_fmm_info(const sc_ctx* ctx, int32_t* out3) {
+  if (ctx == nullptr || out3 == nullptr) return SC_EINVAL;
+  out3[0] = ctx->fmm_order;
+  out3[1] = ctx->fmm_ready ? ctx->fmm_L_used : 0;
+  out3[2] = ctx->fmm_ready ? 1 : 0;
   return SC_OK;
 }
 

@@ -66,6 +66,23 @@ __global__ void incidence_columns(const int32_t* __restrict__ inc, const int32_t
   }
 }
 
+// Rods (SC_ROD_ICOL): the signed 6-vector column (sigma n, sigma r_side x n) of every incidence,
+// 3 double2 per incidence, streamed by the D-gather in incidence order.
+__global__ void rod_incidence_columns(const int32_t* __restrict__ inc, const int32_t* __restrict__ ninc_dev,
+                                      int64_t ninc, const double4* __restrict__ nrm4,
+                                      const double4* __restrict__ rxn4, double2* __restrict__ icolr) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= ninc || e >= *ninc_dev) return;
+  const int32_t v = inc[e];
+  const int32_t l = v >> 1;
+  const int side = v & 1;
+  const double sg = side ? -1.0 : 1.0;
+  const double4 n = nrm4[l], r = rxn4[2 * l + side];
+  icolr[3 * e] = make_double2(sg * n.x, sg * n.y);
+  icolr[3 * e + 1] = make_double2(sg * n.z, sg * r.x);
+  icolr[3 * e + 2] = make_double2(sg * r.y, sg * r.z);
+}
+
 __global__ void rod_columns(const double4* __restrict__ nrm4, const double4* __restrict__ lev4, int64_t nc,
                             double4* __restrict__ rxn4) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -111,6 +128,15 @@ int assemble(sc_ctx* ctx) {
       rod_columns<<<nblk(nc), kT, 0, ctx->stream>>>(ctx->nrm4.p, ctx->lev4.p, nc, ctx->rxn4.p);
       timer_end(ctx, SC_K_ASSEMBLE);
       if (int rc = check_launch(ctx, "rod_columns")) return rc;
+      // signed 6-vector columns in incidence order (the rods gathers stream them)
+      if (int rc = ensure(ctx, ctx->icol4, 3 * nc + 1)) return rc;  // 3 double2 per incidence
+      timer_begin(ctx, SC_K_ASSEMBLE);
+      rod_incidence_columns<<<nblk(2 * nc), kT, 0, ctx->stream>>>(ctx->inc.p, ctx->row_ptr.p + n, 2 * nc, ctx->nrm4.p,
+                                                                  ctx->rxn4.p,
+                                                                  reinterpret_cast<double2*>(ctx->icol4.p));
+      timer_end(ctx, SC_K_ASSEMBLE);
+      if (int rc = check_launch(ctx, "rod_incidence_columns")) return rc;
+
     }
     if (ctx->kind == kSpheres) {  // (rods gather from the per-constraint columns)
       const int64_t ninc = 2 * nc;

@@ -1,0 +1,609 @@
+// fmm.cu -- NEXT row f4(i): a fast O(N) summation of the RPY mobility apply (spheres, FP64).
+//
+// The paper evaluates its all-to-all operators in O(N) with the kernel-independent FMM (KIFMM,
+// P:L888-L896); its accuracy is set by the equivalent-point density (m = 8).  Here the
+// BASELINE RPY sum U_i = F_i/(6 pi mu a) + sum_{j != i} T(r_ij) F_j (configs[0]) is evaluated with
+// a black-box (Chebyshev-interpolation) FMM on a uniform octree -- the configs are uniform
+// suspensions -- in the same spirit: the far field of every well-separated box pair is the RPY far
+// branch T(r) = (1/(8 pi mu)) [(1/r + 2a^2/(3r^3)) I + (1/r^3)(1 - 2a^2/r^2) r r^T] evaluated
+// between the pseudo-particles at the boxes' Chebyshev nodes, and the near field (the 27 leaves
+// around a body, incl. every overlapping pair, r < 2a) is the exact pair sum.  The interpolation
+// order n (nodes per dimension) sets the accuracy (measured errors).
+//
+//   P2M   leaf node strengths  M_B(m) = sum_{j in B} S(m, u_j) F_j            (anterpolation)
+//   M2M   parent from children M_P(m') = sum_c sum_m S_P(m', xi_c(m)) M_c(m)   (levels L-1 .. 2)
+//   M2L   L_T(m) = sum_{S in IL(T)} sum_n T(x_T(m) - y_S(n)) M_S(n)           (levels 2 .. L)
+//   L2L   L_C(m) += sum_m' S_P(m', xi_C(m)) L_P(m')                          (levels 3 .. L)
+//   L2P+P2P  U_i = sum_m S(m, u_i) L_B(m) + sum_{j in the 27 leaves around B} T_ij F_j
+// S(m, u) = prod_d (1/n + (2/n) sum_{q=1}^{n-1} T_q(xbar_{m_d}) T_q(u_d)) with the Chebyshev nodes
+// xbar_k = cos((2k+1) pi / (2n)); IL(T) = the children of the parent's neighbours that are not
+// adjacent to T (at most 189).  Every sum is in a fixed order (deterministic); monodisperse radii.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "rpy_common.cuh"
+#include "sc_internal.h"
+
+namespace sc {
+namespace {
+
+constexpr int kNmax = 10;
+__constant__ double c_xbar[kNmax];             // Chebyshev nodes
+__constant__ double c_T[kNmax * kNmax];        // T_q(xbar_k) at [k * n + q]
+__constant__ double c_P[2 * kNmax * kNmax];    // [sigma][m'][m] = S(xbar_m', (xbar_m + s)/2), s = -1, +1
+
+struct Geom {
+  double ox, oy, oz;  // root cube corner
+  double H;           // root cube side
+  double a;           // sphere radius (monodisperse)
+  int L;              // leaf level
+};
+
+__host__ __device__ inline int64_t nbox(int l) { return int64_t(1) << (3 * l); }
+
+// 1-D interpolation weights w[k] = S_n(xbar_k, u), u in [-1, 1]
+template <int NN>
+__device__ __forceinline__ void cheb_w(double u, double w[NN]) {
+  double T[NN];
+  T[0] = 1.0;
+  if (NN > 1) T[1] = u;
+#pragma unroll
+  for (int q = 2; q < NN; ++q) T[q] = 2.0 * u * T[q - 1] - T[q - 2];
+#pragma unroll
+  for (int k = 0; k < NN; ++k) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 1; q < NN; ++q) s = fma(c_T[k * NN + q], T[q], s);
+    w[k] = (1.0 + 2.0 * s) / NN;
+  }
+}
+
+// RPY far branch (scaled by 8 pi mu): acc += c1 f + c2 (d.f) d, d = y - x
+__device__ __forceinline__ void far_pair(double dx, double dy, double dz, double fx, double fy, double fz,
+                                         double a2, double& ax, double& ay, double& az) {
+  const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+  const double y = rsqrt_dp(r2);
+  const double h = y * y, e = y * h;
+  const double c1 = fma(2.0 / 3.0 * a2, e, y);
+  const double c2 = e * fma(-2.0 * a2, h, 1.0) * fma(dz, fz, fma(dy, fy, dx * fx));
+  ax = fma(c2, dx, fma(c1, fx, ax));
+  ay = fma(c2, dy, fma(c1, fy, ay));
+  az = fma(c2, dz, fma(c1, fz, az));
+}
+
+__device__ __forceinline__ void box_center(const Geom& g, int l, int64_t bi, double& cx, double& cy, double& cz,
+                                           double& w) {
+  const int D = 1 << l;
+  const int ix = static_cast<int>(bi % D), iy = static_cast<int>((bi / D) % D), iz = static_cast<int>(bi / D / D);
+  const double h = g.H / D;
+  w = 0.5 * h;
+  cx = g.ox + h * (ix + 0.5);
+  cy = g.oy + h * (iy + 0.5);
+  cz = g.oz + h * (iz + 0.5);
+}
+
+__global__ void leaf_of_kernel(const double4* __restrict__ pos4, int64_t n, Geom g, uint32_t* __restrict__ key,
+                               int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int D = 1 << g.L;
+  const double h = g.H / D;
+  const double4 p = pos4[i];
+  int ix = static_cast<int>(floor((p.x - g.ox) / h)), iy = static_cast<int>(floor((p.y - g.oy) / h)),
+      iz = static_cast<int>(floor((p.z - g.oz) / h));
+  ix = min(max(ix, 0), D - 1);
+  iy = min(max(iy, 0), D - 1);
+  iz = min(max(iz, 0), D - 1);
+  const uint32_t b = static_cast<uint32_t>((iz * D + iy) * D + ix);
+  key[i] = b;
+  idx[i] = static_cast<int32_t>(i);
+  atomicAdd(&cnt[b], 1);
+}
+
+__global__ void gather_sorted_kernel(const int32_t* __restrict__ sidx, int64_t n, const double4* __restrict__ src,
+                                     double4* __restrict__ dst) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  dst[k] = src[sidx[k]];
+}
+
+// P2M: one CTA per leaf, thread m = node (blockDim >= n^3)
+template <int NN>
+__global__ void p2m_kernel(const double4* __restrict__ spos, const double4* __restrict__ sf,
+                           const int32_t* __restrict__ lstart, Geom g, double* __restrict__ M,
+                           const int32_t* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  constexpr int NB = NN * NN * NN;
+  constexpr int CH = 64;
+  __shared__ double sw[CH][3][NN];
+  __shared__ double sfrc[CH][3];
+  const int64_t b = blockIdx.x;
+  double cx, cy, cz, w;
+  box_center(g, g.L, b, cx, cy, cz, w);
+  const int32_t j0 = lstart[b], j1 = lstart[b + 1];
+  const int m = threadIdx.x;
+  const int mx = m % NN, my = (m / NN) % NN, mz = m / (NN * NN);
+  double ax = 0, ay = 0, az = 0;
+  for (int32_t c0 = j0; c0 < j1; c0 += CH) {
+    const int cn = min(CH, j1 - c0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < 3 * cn; t += blockDim.x) {
+      const int jj = t / 3, d = t % 3;
+      const double4 p = spos[c0 + jj];
+      const double x = d == 0 ? p.x - cx : (d == 1 ? p.y - cy : p.z - cz);
+      double u = x / w;
+      u = fmin(1.0, fmax(-1.0, u));
+      double ww[NN];
+      cheb_w<NN>(u, ww);
+#pragma unroll
+      for (int k = 0; k < NN; ++k) sw[jj][d][k] = ww[k];
+      if (d == 0) {
+        const double4 f = sf[c0 + jj];
+        sfrc[jj][0] = f.x;
+        sfrc[jj][1] = f.y;
+        sfrc[jj][2] = f.z;
+      }
+    }
+    __syncthreads();
+    if (m < NB) {
+      for (int jj = 0; jj < cn; ++jj) {
+        const double s = sw[jj][0][mx] * sw[jj][1][my] * sw[jj][2][mz];
+        ax = fma(s, sfrc[jj][0], ax);
+        ay = fma(s, sfrc[jj][1], ay);
+        az = fma(s, sfrc[jj][2], az);
+      }
+    }
+  }
+  if (m < NB) {
+    double* o = M + (b * NB + m) * 3;
+    o[0] = ax;
+    o[1] = ay;
+    o[2] = az;
+  }
+}
+
+// M2M (child level l+1 -> parent level l) and L2L (parent l -> children l+1): the 1-D transfer
+// matrices c_P of the child's position sigma in its parent.
+template <int NN, bool UP>
+__global__ void transfer_kernel(int l, double* __restrict__ Xp, double* __restrict__ Xc,
+                                const int32_t* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  constexpr int NB = NN * NN * NN;
+  __shared__ double s[NB * 3];
+  const int m = threadIdx.x;
+  const int mx = m % NN, my = (m / NN) % NN, mz = m / (NN * NN);
+  if (UP) {  // parent box blockIdx.x at level l: sum over its 8 children
+    const int D = 1 << l;
+    const int64_t p = blockIdx.x;
+    const int px = static_cast<int>(p % D), py = static_cast<int>((p / D) % D), pz = static_cast<int>(p / D / D);
+    double ax = 0, ay = 0, az = 0;
+    for (int c = 0; c < 8; ++c) {
+      const int sx = c & 1, sy = (c >> 1) & 1, sz = c >> 2;
+      const int64_t ci = ((2 * pz + sz) * (2 * D) + (2 * py + sy)) * (2 * D) + (2 * px + sx);
+      __syncthreads();
+      for (int t = threadIdx.x; t < 3 * NB; t += blockDim.x) s[t] = Xc[ci * NB * 3 + t];
+      __syncthreads();
+      if (m < NB) {
+        const double* Px = c_P + sx * NN * NN + mx * NN;
+        const double* Py = c_P + sy * NN * NN + my * NN;
+        const double* Pz = c_P + sz * NN * NN + mz * NN;
+        for (int kz = 0; kz < NN; ++kz)
+          for (int ky = 0; ky < NN; ++ky) {
+            const double pyz = Py[ky] * Pz[kz];
+#pragma unroll
+            for (int kx = 0; kx < NN; ++kx) {
+              const double wgt = Px[kx] * pyz;
+              const double* v = s + ((kz * NN + ky) * NN + kx) * 3;
+              ax = fma(wgt, v[0], ax);
+              ay = fma(wgt, v[1], ay);
+              az = fma(wgt, v[2], az);
+            }
+          }
+      }
+    }
+    if (m < NB) {
+      double* o = Xp + (p * NB + m) * 3;
+      o[0] = ax;
+      o[1] = ay;
+      o[2] = az;
+    }
+  } else {  // child box blockIdx.x at level l+1: add its parent's local expansion at its nodes
+    const int D = 2 << l;
+    const int64_t c = blockIdx.x;
+    const int cx = static_cast<int>(c % D), cy = static_cast<int>((c / D) % D), cz = static_cast<int>(c / D / D);
+    const int64_t pi = ((cz / 2) * (D / 2) + cy / 2) * (D / 2) + cx / 2;
+    for (int t = threadIdx.x; t < 3 * NB; t += blockDim.x) s[t] = Xp[pi * NB * 3 + t];
+    __syncthreads();
+    if (m < NB) {
+      const int sx = cx & 1, sy = cy & 1, sz = cz & 1;
+      double ax = 0, ay = 0, az = 0;
+      for (int kz = 0; kz < NN; ++kz)
+        for (int ky = 0; ky < NN; ++ky) {
+          const double pyz = c_P[sy * NN * NN + ky * NN + my] * c_P[sz * NN * NN + kz * NN + mz];
+#pragma unroll
+          for (int kx = 0; kx < NN; ++kx) {
+            const double wgt = c_P[sx * NN * NN + kx * NN + mx] * pyz;
+            const double* v = s + ((kz * NN + ky) * NN + kx) * 3;
+            ax = fma(wgt, v[0], ax);
+            ay = fma(wgt, v[1], ay);
+            az = fma(wgt, v[2], az);
+          }
+        }
+      double* o = Xc + (c * NB + m) * 3;
+      o[0] += ax;
+      o[1] += ay;
+      o[2] += az;
+    }
+  }
+}
+
+// M2L: one CTA per target box (all levels 2..L: blockIdx.x over the concatenated levels),
+// thread m = target node; the source boxes of the interaction list in a fixed order.
+template <int NN>
+__global__ void m2l_kernel(Geom g, const int64_t* __restrict__ lev_off /* box offset of level l */,
+                           const double* __restrict__ M, double* __restrict__ Lc, const int32_t* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  constexpr int NB = NN * NN * NN;
+  __shared__ double4 sy[NB];  // source node positions
+  __shared__ double4 sm[NB];  // source node strengths
+  int64_t gb = blockIdx.x;
+  int l = 2;
+  while (l < g.L && gb >= lev_off[l + 1] - lev_off[2]) ++l;
+  const int64_t t = gb - (lev_off[l] - lev_off[2]);
+  const int D = 1 << l;
+  const int tx = static_cast<int>(t % D), ty = static_cast<int>((t / D) % D), tz = static_cast<int>(t / D / D);
+  double cx, cy, cz, w;
+  box_center(g, l, t, cx, cy, cz, w);
+  const int m = threadIdx.x;
+  const int mx = m % NN, my = (m / NN) % NN, mz = m / (NN * NN);
+  const double x = cx + w * c_xbar[mx], y = cy + w * c_xbar[my], z = cz + w * c_xbar[mz];
+  const double a2 = g.a * g.a;
+  double ax = 0, ay = 0, az = 0;
+  const int px = tx >> 1, py = ty >> 1, pz = tz >> 1, Dp = D >> 1;
+  for (int oz = -1; oz <= 1; ++oz)
+    for (int oy = -1; oy <= 1; ++oy)
+      for (int ox = -1; ox <= 1; ++ox) {
+        const int qx = px + ox, qy = py + oy, qz = pz + oz;
+        if (qx < 0 || qy < 0 || qz < 0 || qx >= Dp || qy >= Dp || qz >= Dp) continue;
+        for (int c = 0; c < 8; ++c) {
+          const int sx = 2 * qx + (c & 1), sy_ = 2 * qy + ((c >> 1) & 1), sz = 2 * qz + (c >> 2);
+          if (abs(sx - tx) <= 1 && abs(sy_ - ty) <= 1 && abs(sz - tz) <= 1) continue;  // adjacent: near
+          const int64_t s = (static_cast<int64_t>(sz) * D + sy_) * D + sx;
+          double scx, scy, scz, sw;
+          box_center(g, l, s, scx, scy, scz, sw);
+          __syncthreads();
+          for (int q = threadIdx.x; q < NB; q += blockDim.x) {
+            const int qx_ = q % NN, qy_ = (q / NN) % NN, qz_ = q / (NN * NN);
+            sy[q] = make_double4(scx + sw * c_xbar[qx_], scy + sw * c_xbar[qy_], scz + sw * c_xbar[qz_], 0.0);
+            const double* v = M + ((lev_off[l] + s) * NB + q) * 3;
+            sm[q] = make_double4(v[0], v[1], v[2], 0.0);
+          }
+          __syncthreads();
+          if (m < NB) {
+#pragma unroll 4
+            for (int q = 0; q < NB; ++q) {
+              const double4 p = sy[q], f = sm[q];
+              far_pair(p.x - x, p.y - y, p.z - z, f.x, f.y, f.z, a2, ax, ay, az);
+            }
+          }
+        }
+      }
+  if (m < NB) {
+    double* o = Lc + ((lev_off[l] + t) * NB + m) * 3;
+    o[0] = ax;
+    o[1] = ay;
+    o[2] = az;
+  }
+}
+
+// L2P + P2P: one CTA per leaf; thread = target body (chunks of blockDim); sources of the 27
+// neighbouring leaves through shared memory (exact RPY incl. the overlap branch and the self term).
+template <int NN>
+__global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict__ spos,
+                                                      const double4* __restrict__ sf,
+                                                      const int32_t* __restrict__ sidx,
+                                                      const int32_t* __restrict__ lstart, Geom g,
+                                                      const double* __restrict__ Lc, int64_t loff_L, double scale,
+                                                      double4* __restrict__ u4, int32_t* __restrict__ err,
+                                                      const int32_t* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  constexpr int NB = NN * NN * NN;
+  constexpr int TS = 128;
+  __shared__ double sl[NB * 3];
+  __shared__ double4 sp[TS], sfs[TS];
+  const int64_t b = blockIdx.x;
+  const int32_t i0 = lstart[b], i1 = lstart[b + 1];
+  if (i0 == i1) return;
+  const int D = 1 << g.L;
+  const int bx = static_cast<int>(b % D), by = static_cast<int>((b / D) % D), bz = static_cast<int>(b / D / D);
+  double cx, cy, cz, w;
+  box_center(g, g.L, b, cx, cy, cz, w);
+  for (int t = threadIdx.x; t < 3 * NB; t += blockDim.x) sl[t] = Lc[(loff_L + b) * NB * 3 + t];
+  const double a = g.a, a2 = a * a, ia = 1.0 / a;
+  const long long near_bits = __double_as_longlong(4.0 * a2);
+  for (int32_t k0 = i0; k0 < i1; k0 += TS) {
+    const int32_t k = k0 + threadIdx.x;
+    const bool act = k < i1;
+    double4 pi = make_double4(0, 0, 0, 0), fi = pi;
+    if (act) {
+      pi = spos[k];
+      fi = sf[k];
+    }
+    double ux = 0, uy = 0, uz = 0;
+    __syncthreads();  // (sl ready; sp / sfs free)
+    if (act) {  // far field: interpolate the leaf's local expansion
+      double wx[NN], wy[NN], wz[NN];
+      cheb_w<NN>(fmin(1.0, fmax(-1.0, (pi.x - cx) / w)), wx);
+      cheb_w<NN>(fmin(1.0, fmax(-1.0, (pi.y - cy) / w)), wy);
+      cheb_w<NN>(fmin(1.0, fmax(-1.0, (pi.z - cz) / w)), wz);
+#pragma unroll
+      for (int mz = 0; mz < NN; ++mz)
+#pragma unroll
+        for (int my = 0; my < NN; ++my) {
+          const double wyz = wy[my] * wz[mz];
+#pragma unroll
+          for (int mx = 0; mx < NN; ++mx) {
+            const double s = wx[mx] * wyz;
+            const double* v = sl + ((mz * NN + my) * NN + mx) * 3;
+            ux = fma(s, v[0], ux);
+            uy = fma(s, v[1], uy);
+            uz = fma(s, v[2], uz);
+          }
+        }
+    }
+    // near field: the 27 leaves around b (incl. b), fixed order
+    for (int oz = -1; oz <= 1; ++oz)
+      for (int oy = -1; oy <= 1; ++oy)
+        for (int ox = -1; ox <= 1; ++ox) {
+          const int qx = bx + ox, qy = by + oy, qz = bz + oz;
+          if (qx < 0 || qy < 0 || qz < 0 || qx >= D || qy >= D || qz >= D) continue;
+          const int64_t q = (static_cast<int64_t>(qz) * D + qy) * D + qx;
+          const int32_t j0 = lstart[q], j1 = lstart[q + 1];
+          for (int32_t c0 = j0; c0 < j1; c0 += TS) {
+            const int cn = min(TS, j1 - c0);
+            __syncthreads();
+            if (threadIdx.x < cn) {
+              sp[threadIdx.x] = spos[c0 + threadIdx.x];
+              sfs[threadIdx.x] = sf[c0 + threadIdx.x];
+            }
+            __syncthreads();
+            if (act) {
+              for (int jj = 0; jj < cn; ++jj) {
+                if (c0 + jj == k) continue;  // self: below
+                const double4 pj = sp[jj], fj = sfs[jj];
+                double dx, dy, dz;
+                const double r2 = rpy_r2(pi, pj, dx, dy, dz);
+                if (!rpy_is_near(r2, 0.0, false, near_bits)) {
+                  far_pair(dx, dy, dz, fj.x, fj.y, fj.z, a2, ux, uy, uz);
+                } else {  // overlap branch: (4/(3a))(1 - 9r/(32a)) I + (1/(8a^2 r)) d d^T
+                  double rs = 0.0, rr = 0.0;
+                  if (r2 > 0.0) {
+                    rs = rsqrt_dp(r2);
+                    rr = r2 * rs;
+                  } else {
+                    atomicExch(err, 1);  // coincident centres (reading A12)
+                  }
+                  const double c1 = (4.0 / 3.0) * ia * fma(-9.0 / 32.0 * ia, rr, 1.0);
+                  const double c2 = 0.125 * ia * ia * rs * fma(dz, fj.z, fma(dy, fj.y, dx * fj.x));
+                  ux = fma(c2, dx, fma(c1, fj.x, ux));
+                  uy = fma(c2, dy, fma(c1, fj.y, uy));
+                  uz = fma(c2, dz, fma(c1, fj.z, uz));
+                }
+              }
+            }
+          }
+        }
+    if (act) {
+      const double cs = (4.0 / 3.0) * ia;  // self: F/(6 pi mu a) = (1/(8 pi mu)) (4/(3a)) F
+      ux = fma(cs, fi.x, ux);
+      uy = fma(cs, fi.y, uy);
+      uz = fma(cs, fi.z, uz);
+      u4[sidx[k]] = make_double4(scale * ux, scale * uy, scale * uz, 0.0);
+    }
+  }
+}
+
+template <int NN>
+int fmm_launch(sc_ctx* ctx, const Geom& g, const double4* f4, double mu, double4* u4, const int32_t* done) {
+  constexpr int NB = NN * NN * NN;
+  const int nb = (NB + 31) / 32 * 32;
+  const int L = g.L;
+  const int64_t n = ctx->n;
+  const int64_t* loff = ctx->fmm_lev_off_dev.p;
+  const std::vector<int64_t>& lo = ctx->fmm_lev_off;
+  double* M = ctx->fmm_M.p;
+  double* Lc = ctx->fmm_L.p;
+  timer_begin(ctx, SC_K_RPY);
+  gather_sorted_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->fmm_sidx.p, n, f4,
+                                                                                       ctx->fmm_sf4.p);
+  p2m_kernel<NN><<<static_cast<unsigned>(nbox(L)), nb, 0, ctx->stream>>>(ctx->fmm_spos4.p, ctx->fmm_sf4.p,
+                                                                         ctx->fmm_lstart.p, g, M + lo[L] * NB * 3,
+                                                                         done);
+  for (int l = L - 1; l >= 2; --l)
+    transfer_kernel<NN, true><<<static_cast<unsigned>(nbox(l)), nb, 0, ctx->stream>>>(
+        l, M + lo[l] * NB * 3, M + lo[l + 1] * NB * 3, done);
+  m2l_kernel<NN><<<static_cast<unsigned>(lo[L + 1] - lo[2]), nb, 0, ctx->stream>>>(g, loff, M, Lc, done);
+  for (int l = 2; l < L; ++l)
+    transfer_kernel<NN, false><<<static_cast<unsigned>(nbox(l + 1)), nb, 0, ctx->stream>>>(
+        l, Lc + lo[l] * NB * 3, Lc + lo[l + 1] * NB * 3, done);
+  const double scale = 1.0 / (8.0 * 3.14159265358979323846 * mu);
+  l2p_p2p_kernel<NN><<<static_cast<unsigned>(nbox(L)), 128, 0, ctx->stream>>>(
+      ctx->fmm_spos4.p, ctx->fmm_sf4.p, ctx->fmm_sidx.p, ctx->fmm_lstart.p, g, Lc, lo[L], scale, u4, ctx->derr,
+      done);
+  timer_end(ctx, SC_K_RPY);
+  ctx->launch_count += 4 + 2 * (L - 2);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "fmm");
+  if (ctx->npad > n)
+    SC_CUDA(cudaMemsetAsync(u4 + n, 0, sizeof(double4) * (ctx->npad - n), ctx->stream));
+  return 0;
+}
+
+__global__ void bbox_kernel(const double4* __restrict__ pos4, int64_t n, double* __restrict__ out /* 6 */) {
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double4 p = pos4[i];
+    lo[0] = fmin(lo[0], p.x); lo[1] = fmin(lo[1], p.y); lo[2] = fmin(lo[2], p.z);
+    hi[0] = fmax(hi[0], p.x); hi[1] = fmax(hi[1], p.y); hi[2] = fmax(hi[2], p.z);
+  }
+  __shared__ double s[6][256];
+  for (int d = 0; d < 3; ++d) {
+    s[d][threadIdx.x] = lo[d];
+    s[3 + d][threadIdx.x] = hi[d];
+  }
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int d = 0; d < 3; ++d) {
+        s[d][threadIdx.x] = fmin(s[d][threadIdx.x], s[d][threadIdx.x + w]);
+        s[3 + d][threadIdx.x] = fmax(s[3 + d][threadIdx.x], s[3 + d][threadIdx.x + w]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int d = 0; d < 6; ++d) out[blockIdx.x * 6 + d] = s[d][0];
+}
+
+double cheb_S(int n, double xk, double u) {  // host: S_n(xbar_k, u)
+  double s = 0.0, t0 = 1.0, t1 = u, tk0 = 1.0, tk1 = xk;
+  for (int q = 1; q < n; ++q) {
+    s += tk1 * t1;
+    const double t2 = 2.0 * u * t1 - t0, tk2 = 2.0 * xk * tk1 - tk0;
+    t0 = t1; t1 = t2; tk0 = tk1; tk1 = tk2;
+  }
+  return (1.0 + 2.0 * s) / n;
+}
+
+}  // namespace
+
+// Tree of the current bodies (after build_contacts): root cube, leaf level, bodies sorted by leaf.
+int fmm_setup(sc_ctx* ctx) {
+  const int nn = ctx->fmm_order;
+  if (nn != 4 && nn != 6 && nn != 8) return fail(ctx, SC_EINVAL, "fmm order must be 4, 6 or 8");
+  if (ctx->kind != kSpheres || ctx->poly) return fail(ctx, SC_EINVAL, "the fast RPY summation needs monodisperse spheres");
+  const int64_t n = ctx->n;
+  // node tables
+  double xb[kNmax], T[kNmax * kNmax], P[2 * kNmax * kNmax];
+  const double pi = 3.14159265358979323846;
+  for (int k = 0; k < nn; ++k) xb[k] = std::cos((2 * k + 1) * pi / (2 * nn));
+  for (int k = 0; k < nn; ++k) {
+    double t0 = 1.0, t1 = xb[k];
+    T[k * nn] = 1.0;
+    if (nn > 1) T[k * nn + 1] = xb[k];
+    for (int q = 2; q < nn; ++q) {
+      const double t2 = 2.0 * xb[k] * t1 - t0;
+      T[k * nn + q] = t2;
+      t0 = t1;
+      t1 = t2;
+    }
+  }
+  for (int sg = 0; sg < 2; ++sg)
+    for (int mp = 0; mp < nn; ++mp)
+      for (int m = 0; m < nn; ++m) P[sg * nn * nn + mp * nn + m] = cheb_S(nn, xb[mp], 0.5 * (xb[m] + (sg ? 1.0 : -1.0)));
+  SC_CUDA(cudaMemcpyToSymbolAsync(c_xbar, xb, sizeof(double) * nn, 0, cudaMemcpyHostToDevice, ctx->stream));
+  SC_CUDA(cudaMemcpyToSymbolAsync(c_T, T, sizeof(double) * nn * nn, 0, cudaMemcpyHostToDevice, ctx->stream));
+  SC_CUDA(cudaMemcpyToSymbolAsync(c_P, P, sizeof(double) * 2 * nn * nn, 0, cudaMemcpyHostToDevice, ctx->stream));
+  // bounding cube
+  const int nbb = 64;
+  if (int rc = ensure(ctx, ctx->bbox_part, 6 * nbb)) return rc;
+  bbox_kernel<<<nbb, 256, 0, ctx->stream>>>(ctx->pos4.p, n, ctx->bbox_part.p);
+  if (int rc = check_launch(ctx, "fmm_bbox")) return rc;
+  std::vector<double> hb(6 * nbb);
+  SC_CUDA(cudaMemcpyAsync(hb.data(), ctx->bbox_part.p, sizeof(double) * 6 * nbb, cudaMemcpyDeviceToHost, ctx->stream));
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int b = 0; b < nbb; ++b)
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = std::min(lo[d], hb[b * 6 + d]);
+      hi[d] = std::max(hi[d], hb[b * 6 + 3 + d]);
+    }
+  double ext = std::max(hi[0] - lo[0], std::max(hi[1] - lo[1], hi[2] - lo[2]));
+  const double a = ctx->a_const;
+  ext = std::max(ext, 4.0 * a) * (1.0 + 1e-9) + 1e-9;
+  // leaf level: largest useful L with leaf side >= 2a (far branch between well-separated boxes,
+  // every overlapping pair in neighbouring leaves), chosen to balance the P2P and M2L work
+  int L = ctx->fmm_leaf_level;
+  const int Lmax = std::max(2, static_cast<int>(std::floor(std::log2(ext / (2.0 * a)))));
+  if (L <= 0) {
+    double best = 1e300;
+    const double nb3 = static_cast<double>(nn) * nn * nn;
+    for (int l = 2; l <= std::min(Lmax, 7); ++l) {
+      const double leaves = static_cast<double>(nbox(l));
+      const double p2p = static_cast<double>(n) * 27.0 * (static_cast<double>(n) / leaves);
+      const double m2l = 1.15 * leaves * 189.0 * nb3 * nb3;
+      if (p2p + m2l < best) {
+        best = p2p + m2l;
+        L = l;
+      }
+    }
+  }
+  L = std::max(2, std::min(L, Lmax));
+  ctx->fmm_L_used = L;
+  ctx->fmm_geom[0] = 0.5 * (lo[0] + hi[0]) - 0.5 * ext;
+  ctx->fmm_geom[1] = 0.5 * (lo[1] + hi[1]) - 0.5 * ext;
+  ctx->fmm_geom[2] = 0.5 * (lo[2] + hi[2]) - 0.5 * ext;
+  ctx->fmm_geom[3] = ext;
+  Geom g{ctx->fmm_geom[0], ctx->fmm_geom[1], ctx->fmm_geom[2], ext, a, L};
+  // bodies sorted by leaf (stable radix sort: within a leaf by body index -> deterministic sums)
+  const int64_t nleaf = nbox(L);
+  if (int rc = ensure(ctx, ctx->fmm_key, 2 * std::max<int64_t>(n, 1))) return rc;
+  if (int rc = ensure(ctx, ctx->fmm_idx0, std::max<int64_t>(n, 1))) return rc;
+  if (int rc = ensure(ctx, ctx->fmm_sidx, std::max<int64_t>(n, 1))) return rc;
+  if (int rc = ensure(ctx, ctx->fmm_cnt, nleaf + 1)) return rc;
+  if (int rc = ensure(ctx, ctx->fmm_lstart, nleaf + 1)) return rc;
+  if (int rc = ensure(ctx, ctx->scan_tmp, scan_tmp_size(nleaf + 1) + 1)) return rc;
+  SC_CUDA(cudaMemsetAsync(ctx->fmm_cnt.p, 0, sizeof(int32_t) * (nleaf + 1), ctx->stream));
+  uint32_t* key_in = reinterpret_cast<uint32_t*>(ctx->fmm_key.p);
+  uint32_t* key_out = key_in + std::max<int64_t>(n, 1);
+  leaf_of_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->pos4.p, n, g, key_in,
+                                                                                  ctx->fmm_idx0.p, ctx->fmm_cnt.p);
+  if (int rc = check_launch(ctx, "fmm_leaf_of")) return rc;
+  if (int rc = exclusive_scan_i32(ctx, ctx->fmm_cnt.p, ctx->fmm_lstart.p, nleaf, ctx->scan_tmp.p)) return rc;
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key_in, key_out, ctx->fmm_idx0.p, ctx->fmm_sidx.p,
+                                  static_cast<int>(n), 0, 3 * L, ctx->stream);
+  if (int rc = ensure(ctx, ctx->fmm_cubtmp, tmp_bytes + 16)) return rc;
+  SC_CUDA(cub::DeviceRadixSort::SortPairs(ctx->fmm_cubtmp.p, tmp_bytes, key_in, key_out, ctx->fmm_idx0.p,
+                                          ctx->fmm_sidx.p, static_cast<int>(n), 0, 3 * L, ctx->stream));
+  if (int rc = ensure(ctx, ctx->fmm_spos4, std::max<int64_t>(n, 1))) return rc;
+  if (int rc = ensure(ctx, ctx->fmm_sf4, std::max<int64_t>(n, 1))) return rc;
+  gather_sorted_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->fmm_sidx.p, n,
+                                                                                       ctx->pos4.p, ctx->fmm_spos4.p);
+  if (int rc = check_launch(ctx, "fmm_sort")) return rc;
+  // expansions of levels 2..L (box offsets per level)
+  ctx->fmm_lev_off.assign(L + 2, 0);
+  int64_t off = 0;
+  for (int l = 0; l <= L + 1; ++l) {
+    ctx->fmm_lev_off[l] = off;
+    if (l >= 2 && l <= L) off += nbox(l);
+  }
+  // (offsets relative to level 2: lev_off[l] = boxes of levels 2..l-1)
+  const int64_t nb3 = static_cast<int64_t>(nn) * nn * nn;
+  if (int rc = ensure(ctx, ctx->fmm_M, static_cast<size_t>(off) * nb3 * 3)) return rc;
+  if (int rc = ensure(ctx, ctx->fmm_L, static_cast<size_t>(off) * nb3 * 3)) return rc;
+  if (int rc = ensure(ctx, ctx->fmm_lev_off_dev, L + 2)) return rc;
+  SC_CUDA(cudaMemcpyAsync(ctx->fmm_lev_off_dev.p, ctx->fmm_lev_off.data(), sizeof(int64_t) * (L + 2),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->fmm_ready = true;
+  return 0;
+}
+
+int fmm_apply(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done) {
+  if (!ctx->fmm_ready) {
+    if (int rc = fmm_setup(ctx)) return rc;
+  }
+  Geom g{ctx->fmm_geom[0], ctx->fmm_geom[1], ctx->fmm_geom[2], ctx->fmm_geom[3], ctx->a_const, ctx->fmm_L_used};
+  switch (ctx->fmm_order) {
+    case 4: return fmm_launch<4>(ctx, g, f4, mu, u4, done);
+    case 6: return fmm_launch<6>(ctx, g, f4, mu, u4, done);
+    default: return fmm_launch<8>(ctx, g, f4, mu, u4, done);
+  }
+}
+
+}  // namespace sc

@@ -56,36 +56,29 @@ __global__ void __launch_bounds__(kT) gather_kernel(
     tb = dir4[b];
     mb = mob4[b];
   }
+  if (KIND == kRods) {  // the signed columns of the incidences, streamed (assemble.cu)
+    double f[6] = {0, 0, 0, 0, 0, 0};
+    rods_gather_lane<LPB, MODE == kProj>(e0, e1, k, alpha, inc, a, g_old, gam_new,
+                                         reinterpret_cast<const double2*>(icol4), f);
+    fx = f[0]; fy = f[1]; fz = f[2]; tx = f[3]; ty = f[4]; tz = f[5];
+  } else {
 #pragma unroll 2
-  for (int32_t e = e0 + k; e < e1; e += LPB) {
-    const int32_t v = inc[e];
-    const int32_t l = v >> 1;
-    const int side = v & 1;
-    double gm;
-    if (MODE == kProj) {
-      const double x = __dsub_rn(a[l], __dmul_rn(alpha, g_old[l]));  // gamma - alpha g (Step 8)
-      gm = x > 0.0 ? x : 0.0;                                        // projection (Step 9)
-      if (side == 0) gam_new[l] = gm;                                 // owner = first body
-    } else {
-      gm = a[l];
-    }
-    // incidence column (signed D_l block of this body, stored in incidence order: streamed)
-    if (KIND == kSpheres) {
+    for (int32_t e = e0 + k; e < e1; e += LPB) {
+      const int32_t v = inc[e];
+      const int32_t l = v >> 1;
+      double gm;
+      if (MODE == kProj) {
+        const double x = __dsub_rn(a[l], __dmul_rn(alpha, g_old[l]));  // gamma - alpha g (Step 8)
+        gm = x > 0.0 ? x : 0.0;                                        // projection (Step 9)
+        if ((v & 1) == 0) gam_new[l] = gm;                              // owner = first body
+      } else {
+        gm = a[l];
+      }
+      // incidence column (signed D_l block of this body, stored in incidence order: streamed)
       const double4 nv = icol4[e];
       fx = fma(gm, nv.x, fx);
       fy = fma(gm, nv.y, fy);
       fz = fma(gm, nv.z, fz);
-    } else {  // rods: per-constraint columns (i-side contiguous, j-side L2-resident) beat a
-              // 64-B-per-incidence stream here (measured: 11.5 vs 13.8 ms per C4 solve)
-      const double sgm = side ? -gm : gm;
-      const double4 nv = nrm4[l];
-      const double4 rx = rxn4[2 * l + side];
-      fx = fma(sgm, nv.x, fx);
-      fy = fma(sgm, nv.y, fy);
-      fz = fma(sgm, nv.z, fz);
-      tx = fma(sgm, rx.x, tx);
-      ty = fma(sgm, rx.y, ty);
-      tz = fma(sgm, rx.z, tz);
     }
   }
 #pragma unroll
@@ -102,10 +95,7 @@ __global__ void __launch_bounds__(kT) gather_kernel(
   if (k != 0 || b >= nout) return;
   if (!real) {  // padded source rows: zero force
     if (OUT == kOutF4) out4[b] = make_double4(0, 0, 0, 0);
-    if (OUT == kOutRodU) {
-      out4[2 * b] = make_double4(0, 0, 0, 0);
-      out4[2 * b + 1] = make_double4(0, 0, 0, 0);
-    }
+    if (OUT == kOutRodU) rods_store_uw(out4, b, make_double4(0, 0, 0, 0), make_double4(0, 0, 0, 0));
     return;
   }
   if (OUT == kOutF4) {
@@ -114,13 +104,10 @@ __global__ void __launch_bounds__(kT) gather_kernel(
     double* o = outFT + 6 * b;
     o[0] = fx; o[1] = fy; o[2] = fz; o[3] = tx; o[4] = ty; o[5] = tz;
   } else {
-    // rods: U = (1/zeta_par) t t^T F + (1/zeta_perp) (I - t t^T) F ; W = T / zeta_rot
-    const double4 t = tb;
-    const double4 m = mb;
-    const double tf = fma(t.z, fz, fma(t.y, fy, t.x * fx));
-    const double cpar = (m.x - m.y) * tf;
-    out4[2 * b] = make_double4(fma(m.y, fx, cpar * t.x), fma(m.y, fy, cpar * t.y), fma(m.y, fz, cpar * t.z), 0.0);
-    out4[2 * b + 1] = make_double4(m.z * tx, m.z * ty, m.z * tz, 0.0);
+    const double f[6] = {fx, fy, fz, tx, ty, tz};
+    double4 U, W;
+    rods_drag(tb, mb, f, U, W);
+    rods_store_uw(out4, b, U, W);
   }
 }
 
@@ -153,32 +140,19 @@ __global__ void __launch_bounds__(kR) dt_kernel(
   for (int32_t l = l0 + threadIdx.x; l < l1; l += kR) {
     double v = 0.0;
     if (MODE != kDtInitQ) {
-      const int32_t i = ci[l], j = cj[l];
-      const bool wall = j >= n;  // a wall (NEXT row f2): static, not in the mobility
-      const double4 nv = nrm4[l];
-      const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
       if (KIND == kSpheres) {
+        const int32_t i = ci[l], j = cj[l];
+        const bool wall = j >= n;  // a wall (NEXT row f2): static, not in the mobility
+        const double4 nv = nrm4[l];
+        const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
         const double4 ui = u4[i], uj = wall ? z4 : u4[j];
         v = fma(nv.z, ui.z - uj.z, fma(nv.y, ui.y - uj.y, nv.x * (ui.x - uj.x)));
       } else {
-        const double4 ui = u4[2 * i], wi = u4[2 * i + 1];
-        const double4 uj = wall ? z4 : u4[2 * j], wj = wall ? z4 : u4[2 * j + 1];
-        const double4 ra = rxn4[2 * l], rb = rxn4[2 * l + 1];
-        v = fma(nv.z, ui.z - uj.z, fma(nv.y, ui.y - uj.y, nv.x * (ui.x - uj.x)));
-        v += fma(ra.z, wi.z, fma(ra.y, wi.y, ra.x * wi.x)) - fma(rb.z, wj.z, fma(rb.y, wj.y, rb.x * wj.x));
+        v = rods_dt_value<false>(l, n, ci, cj, nrm4, rxn4, u4);
       }
     }
     if (MODE == kDtIter) {
-      const double g = v + q[l];
-      g_out[l] = g;
-      const double gn = gam_new[l];
-      const double s = gn - gam_old[l];
-      const double y = g - g_old[l];
-      const double m = gn < g ? gn : g;
-      p[0] = fma(s, s, p[0]);
-      p[1] = fma(s, y, p[1]);
-      p[2] = fma(y, y, p[2]);
-      p[3] = fma(m, m, p[3]);
+      dt_iter_terms<false>(l, v, q, gam_new, gam_old, g_old, g_out, p);
     } else if (MODE == kDtAlpha0) {
       const double g0 = g_old[l];
       p[0] = fma(g0, g0, p[0]);
@@ -199,9 +173,12 @@ __global__ void __launch_bounds__(kR) dt_kernel(
       p[3] = fma(m, m, p[3]);
     }
   }
-  block_reduce4(p, red);
+  cta_reduce4_shfl(p, red);  // fixed order, one barrier; the sums in thread 0
   if (!FUSE) {
-    if (threadIdx.x < 4) part[c * 4 + threadIdx.x] = p[threadIdx.x];
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) part[c * 4 + k] = p[k];
+    }
     return;
   }
   // last-CTA K-FINALIZE: only thread 0's partial stores must be ordered before its counter
@@ -284,7 +261,8 @@ __global__ void rod_drag_user_kernel(const double* __restrict__ FT, const double
 __global__ void rod_unpack_kernel(const double4* __restrict__ u4, int64_t n, double* __restrict__ UW) {
   const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b >= n) return;
-  const double4 u = u4[2 * b], w = u4[2 * b + 1];
+  double4 u, w;
+  rods_load_uw<false>(u4, b, u, w);
   double* o = UW + 6 * b;
   o[0] = u.x; o[1] = u.y; o[2] = u.z; o[3] = w.x; o[4] = w.y; o[5] = w.z;
 }

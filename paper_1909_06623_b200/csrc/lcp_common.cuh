@@ -46,6 +46,111 @@ __device__ __forceinline__ void block_reduce4(double v[4], double* red /* [4][kR
   for (int k = 0; k < 4; ++k) v[k] = red[k * kR];
 }
 
+// Loads of data another CTA of the same launch may have written (persistent kernels: L1 is not
+// coherent across SMs, so those go through L2 with ld.cg); plain loads elsewhere.  Same values.
+template <bool CG>
+__device__ __forceinline__ double ldv(const double* p) {
+  return CG ? __ldcg(p) : *p;
+}
+template <bool CG>
+__device__ __forceinline__ double4 ldv4(const double4* p) {
+  if (!CG) return *p;
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = __ldcg(q), b = __ldcg(q + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// Rods body velocities (U, W) in the velocity buffer u4 (64 B per body), packed as 3 double2
+// (48 B: D^T reads 3 vector loads per body instead of 4).
+__device__ __forceinline__ void rods_store_uw(double4* u4, int64_t b, const double4& U, const double4& W) {
+  double2* q = reinterpret_cast<double2*>(u4) + 3 * b;
+  q[0] = make_double2(U.x, U.y);
+  q[1] = make_double2(U.z, W.x);
+  q[2] = make_double2(W.y, W.z);
+}
+template <bool CG>
+__device__ __forceinline__ void rods_load_uw(const double4* u4, int64_t b, double4& U, double4& W) {
+  const double2* q = reinterpret_cast<const double2*>(u4) + 3 * b;
+  const double2 a = CG ? __ldcg(q) : q[0], c = CG ? __ldcg(q + 1) : q[1], d = CG ? __ldcg(q + 2) : q[2];
+  U = make_double4(a.x, a.y, c.x, 0.0);
+  W = make_double4(c.y, d.x, d.y, 0.0);
+}
+
+// Rods, one lane of the D-gather (Steps 8-9 with PROJ): lane k of body b sums the
+// incidences e0+k, e0+k+LPB, ... of gamma_l = max(0, gamma_l - alpha g_l) (PROJ; the first body
+// writes gamma_l) or gamma_l = a_l (raw) times the signed column (sigma n, sigma r x n) of the
+// incidence, streamed in incidence order (assemble.cu rod_incidence_columns, 3 double2 each).
+template <int LPB, bool PROJ>
+__device__ __forceinline__ void rods_gather_lane(int32_t e0, int32_t e1, int k, double alpha,
+                                                 const int32_t* __restrict__ inc, const double* a,
+                                                 const double* g_old, double* gam_new,
+                                                 const double2* __restrict__ icolr, double f[6]) {
+#pragma unroll 2
+  for (int32_t e = e0 + k; e < e1; e += LPB) {
+    const int32_t v = inc[e];
+    const int32_t l = v >> 1;
+    double gm;
+    if (PROJ) {
+      const double x = __dsub_rn(a[l], __dmul_rn(alpha, g_old[l]));  // Step 8
+      gm = x > 0.0 ? x : 0.0;                                        // Step 9
+      if ((v & 1) == 0) gam_new[l] = gm;                              // owner = first body
+    } else {
+      gm = a[l];
+    }
+    const double2 c0 = icolr[3 * e], c1 = icolr[3 * e + 1], c2 = icolr[3 * e + 2];
+    f[0] = fma(gm, c0.x, f[0]);
+    f[1] = fma(gm, c0.y, f[1]);
+    f[2] = fma(gm, c1.x, f[2]);
+    f[3] = fma(gm, c1.y, f[3]);
+    f[4] = fma(gm, c2.x, f[4]);
+    f[5] = fma(gm, c2.y, f[5]);
+  }
+}
+
+// Rods drag (configs[3]): U = (1/zeta_par) t t^T F + (1/zeta_perp)(I - t t^T) F, W = T / zeta_rot;
+// m = (1/zeta_par, 1/zeta_perp, 1/zeta_rot).
+__device__ __forceinline__ void rods_drag(const double4& t, const double4& m, const double f[6], double4& U,
+                                          double4& W) {
+  const double tf = fma(t.z, f[2], fma(t.y, f[1], t.x * f[0]));
+  const double cpar = (m.x - m.y) * tf;
+  U = make_double4(fma(m.y, f[0], cpar * t.x), fma(m.y, f[1], cpar * t.y), fma(m.y, f[2], cpar * t.z), 0.0);
+  W = make_double4(m.z * f[3], m.z * f[4], m.z * f[5], 0.0);
+}
+// Rods, D_l^T (U, W) for constraint l (Step 10 without q): n.(U_i - U_j) + (r_i x n).W_i
+// - (r_j x n).W_j; a wall (j >= n) is at rest.
+template <bool CG>
+__device__ __forceinline__ double rods_dt_value(int64_t l, int64_t n, const int32_t* __restrict__ ci,
+                                                const int32_t* __restrict__ cj, const double4* __restrict__ nrm4,
+                                                const double4* __restrict__ rxn4, const double4* u4) {
+  const int32_t i = ci[l], j = cj[l];
+  const bool wall = j >= n;
+  const double4 nv = nrm4[l];
+  double4 ui, wi, uj = make_double4(0.0, 0.0, 0.0, 0.0), wj = uj;
+  rods_load_uw<CG>(u4, i, ui, wi);
+  if (!wall) rods_load_uw<CG>(u4, j, uj, wj);
+  const double4 ra = rxn4[2 * l], rb = rxn4[2 * l + 1];
+  double v = fma(nv.z, ui.z - uj.z, fma(nv.y, ui.y - uj.y, nv.x * (ui.x - uj.x)));
+  v += fma(ra.z, wi.z, fma(ra.y, wi.y, ra.x * wi.x)) - fma(rb.z, wj.z, fma(rb.y, wj.y, rb.x * wj.x));
+  return v;
+}
+
+// Step 10 (g = D^T U + q, written) and the partial sums of Steps 11, 14-15 for constraint l:
+// s.s, s.y, y.y, min(gamma, g)^2 with s = gamma_new - gamma_old, y = g - g_old.
+template <bool CG>
+__device__ __forceinline__ void dt_iter_terms(int64_t l, double v, const double* __restrict__ q, const double* gam_new,
+                                              const double* gam_old, const double* g_old, double* g_out, double p[4]) {
+  const double g = v + q[l];
+  g_out[l] = g;
+  const double gn = ldv<CG>(gam_new + l);
+  const double s = gn - ldv<CG>(gam_old + l);
+  const double y = g - ldv<CG>(g_old + l);
+  const double m = gn < g ? gn : g;
+  p[0] = fma(s, s, p[0]);
+  p[1] = fma(s, y, p[1]);
+  p[2] = fma(y, y, p[2]);
+  p[3] = fma(m, m, p[3]);
+}
+
 // Fixed-order CTA reduction with one barrier: shuffle-down tree in each warp, then warp 0 sums
 // the warp results in order (result valid in thread 0).  red: >= 4 * (kR / 32) doubles.
 __device__ __forceinline__ void cta_reduce4_shfl(double v[4], double* red) {
@@ -78,15 +183,21 @@ __device__ __forceinline__ void cta_reduce4_shfl(double v[4], double* red) {
 // The scalar update of K-FINALIZE from the reduced sums p (one thread).
 __device__ __forceinline__ void finalize_scalars(const double p[4], int mode, DevScalars* s, bool writer = true);
 
-__device__ __forceinline__ void finalize_block(const double* part, int64_t nchunks, int mode, DevScalars* s, double* red) {
+__device__ __forceinline__ void finalize_block(const double* part, int64_t nchunks, int mode, DevScalars* s, double* red,
+                                               bool writer = true) {
   double p[4] = {0, 0, 0, 0};
-  for (int64_t c = threadIdx.x; c < nchunks; c += kR) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) p[k] += __ldcg(part + c * 4 + k);
+#pragma unroll 4
+  for (int64_t c = threadIdx.x; c < nchunks; c += kR) {  // (loads of several chunks in flight)
+    const double2* q = reinterpret_cast<const double2*>(part + c * 4);
+    const double2 a = __ldcg(q), b = __ldcg(q + 1);
+    p[0] += a.x;
+    p[1] += a.y;
+    p[2] += b.x;
+    p[3] += b.y;
   }
   block_reduce4(p, red);
   if (threadIdx.x != 0) return;
-  finalize_scalars(p, mode, s);
+  finalize_scalars(p, mode, s, writer);
 }
 
 // writer: this copy of the scalars records the residual trace (the persistent loop runs the

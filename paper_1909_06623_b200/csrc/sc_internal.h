@@ -97,7 +97,7 @@ struct sc_ctx {
   bool assembled = false;
   sc::DBuf<int32_t> row_ptr;    // n+1
   sc::DBuf<int32_t> inc;        // 2*nc: (l << 1) | side
-  sc::DBuf<double4> icol4;      // signed D blocks per incidence (spheres 1, rods 2 double4)
+  sc::DBuf<double4> icol4;      // signed D columns per incidence (spheres: 1 double4; rods: 3 double2)
   sc::DBuf<int32_t> first_ptr;  // n+1: constraints with first body < b start at first_ptr[b]
   sc::DBuf<int32_t> near_ptr, near_idx;  // spheres: RPY overlap-branch partners per body (CSR)
   int64_t nchunks = 0;
@@ -117,7 +117,19 @@ struct sc_ctx {
   sc::DBuf<double4> t4;         // torques for the public mobility apply [npad]
   sc::DBuf<double4> u4;         // velocities (Ux,Uy,Uz,0) [npad] (spheres) or [2*npad] (rods: U, W)
   sc::DBuf<double> rpy_part;    // nsplit * rows * 3
-  int mobility_model = 0;       // 0: BASELINE RPY (tt + self rotation); 1: full 6N RPY (NEXT row f4(ii))
+  int mobility_model = 0;       // 0: BASELINE RPY (tt + self rotation); 1: full 6N RPY (NEXT row f4(ii));
+                                // 2: BASELINE RPY by the fast summation (NEXT row f4(i), fmm.cu)
+  // fast RPY summation (fmm.cu): Chebyshev order, leaf level (0: automatic), the tree of the bodies
+  int fmm_order = 6, fmm_leaf_level = 0, fmm_L_used = 0;
+  bool fmm_ready = false;       // tree built for the current bodies
+  double fmm_geom[4] = {};      // root cube corner (x, y, z) and side
+  sc::DBuf<uint32_t> fmm_key;
+  sc::DBuf<int32_t> fmm_idx0, fmm_sidx, fmm_cnt, fmm_lstart;
+  sc::DBuf<char> fmm_cubtmp;
+  sc::DBuf<double4> fmm_spos4, fmm_sf4;
+  sc::DBuf<double> fmm_M, fmm_L;
+  std::vector<int64_t> fmm_lev_off;
+  sc::DBuf<int64_t> fmm_lev_off_dev;
   sc::DBuf<double> rpy6_part;   // full RPY: nsplit * npad * 6 partials
   sc::DBuf<double> ft_tmp;      // n x 6 scratch (F_c for the full-RPY U_c)
   int nsplit = 1;
@@ -209,6 +221,9 @@ int assemble(sc_ctx* ctx);
 int rpy_apply_rows(sc_ctx* ctx, const double4* f4, int64_t row0, int64_t nrows, double mu,
                    double4* u4, const int32_t* done);
 int choose_nsplit(int64_t npad, int world);
+// NEXT row f4(i): u4 = RPY(f4) by the Chebyshev-interpolation FMM (builds the tree on first use)
+int fmm_setup(sc_ctx* ctx);
+int fmm_apply(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done);
 // per-device kernel attributes (max dynamic shared memory); called by sc_create
 int rpy_init_device(sc_ctx* ctx);
 int persist_init_device(sc_ctx* ctx);

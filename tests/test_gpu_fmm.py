@@ -1,0 +1,129 @@
+"""NEXT row f4(i): the fast O(N) RPY summation (csrc/fmm.cu) against the oracle's direct apply.
+
+The fast summation approximates the BASELINE RPY operator; the parity bar is a stated relative L2
+error per interpolation order (from the measured errors in
+profiles/r02/fmm_scaling.jsonl, with margin), measured against the oracle's long-double direct sum
+-- nothing of the GPU direct path enters the reference.  Near field (27 leaves, every overlapping
+pair) is exact, so two spheres in one leaf must match the direct formula to rounding."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1909_06623_b200 import Context, ScError
+from paper_1909_06623_b200.synthetic import make_problem
+
+pytestmark = pytest.mark.gpu
+
+TOL = {4: 2e-4, 6: 1e-5, 8: 1e-6}  # stated rel. L2 bars of the apply
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def _cuda(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+
+
+def _relL2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("order", [4, 6, 8])
+@pytest.mark.parametrize("n,leaf_level", [(6000, 0), (20000, 0), (20000, 3)])
+def test_fmm_apply_vs_oracle(ctx, order, n, leaf_level):
+    p = make_problem("C5", n=n)
+    ctx.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+    ctx.set_mobility_model("rpy_fmm")
+    ctx.set_fmm_params(order, leaf_level)
+    rng = np.random.default_rng(1)
+    FT = rng.normal(size=(p.n, 6))
+    U = ctx.mobility_apply(_cuda(FT)).cpu().numpy()
+    info = ctx.fmm_info()
+    ctx.set_mobility_model("rpy")
+    Uo = oracle.rpy_apply(p.pos, p.radius, p.mu, FT)
+    assert info["ready"] == 1 and info["leaf_level"] >= 2 and (leaf_level == 0 or info["leaf_level"] == leaf_level)
+    err = _relL2(U[:, :3], Uo[:, :3])
+    assert err <= TOL[order], (order, n, info, err)
+    np.testing.assert_allclose(U[:, 3:], Uo[:, 3:], rtol=1e-13, atol=0)  # self rotation (exact)
+
+
+def test_fmm_error_decreases_with_order_and_is_deterministic(ctx):
+    p = make_problem("C5", n=12000)
+    ctx.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+    FT = np.random.default_rng(2).normal(size=(p.n, 6))
+    Uo = oracle.rpy_apply(p.pos, p.radius, p.mu, FT)[:, :3]
+    ctx.set_mobility_model("rpy_fmm")
+    errs = []
+    for order in (4, 6, 8):
+        ctx.set_fmm_params(order, 3)
+        U1 = ctx.mobility_apply(_cuda(FT))
+        U2 = ctx.mobility_apply(_cuda(FT))
+        assert torch.equal(U1, U2)  # fixed summation orders: bitwise repeatable
+        errs.append(_relL2(U1.cpu().numpy()[:, :3], Uo))
+    ctx.set_mobility_model("rpy")
+    assert errs[0] > errs[1] > errs[2], errs
+
+
+def test_fmm_near_field_exact_and_far_pair(ctx):
+    """Overlapping and touching pairs are in the near field (exact formula); a pair far apart goes
+    through P2M -> M2L -> L2P and must match the far branch to the interpolation accuracy."""
+    rng = np.random.default_rng(3)
+    pos = np.concatenate([np.array([[0.0, 0.0, 0.0], [1.5, 0.0, 0.0], [2.0, 2.0, 0.0]]),
+                          rng.uniform(0, 60, size=(3000, 3)) + np.array([10.0, 0.0, 0.0])])
+    pos = pos[np.r_[0:3, 3 + np.flatnonzero(np.min(np.linalg.norm(pos[3:, None, :] - pos[None, :3, :], axis=2), 1) > 2.5)]]
+    FT = np.zeros((len(pos), 6))
+    FT[:3, :3] = rng.normal(size=(3, 3))
+    FT[-1, :3] = [1.0, -2.0, 0.5]
+    ctx.build_contacts_spheres(_cuda(pos), None, 0.0, 0.1)
+    ctx.set_mobility_model("rpy_fmm")
+    ctx.set_fmm_params(8, 0)
+    U = ctx.mobility_apply(_cuda(FT)).cpu().numpy()
+    ctx.set_mobility_model("rpy")
+    Uo = oracle.rpy_apply(pos, np.ones(len(pos)), 1.0, FT)
+    np.testing.assert_allclose(U[:3, :3], Uo[:3, :3], rtol=1e-6, atol=1e-8 * np.abs(Uo).max())
+    assert _relL2(U[:, :3], Uo[:, :3]) <= TOL[8]
+
+
+def test_fmm_converged_solve_certified_by_oracle(ctx):
+    """BBPGD with the fast summation as the mobility (order 8): the converged gamma satisfies the
+    oracle's (direct) LCP to the accuracy of the operator -- phi(gamma, g_oracle) small next to
+    |q| -- and is close to the direct solve's gamma."""
+    p = make_problem("C5", n=20000, fixed_iters=0)
+    t = _cuda
+    rs = {}
+    for model in ("rpy", "rpy_fmm"):
+        ctx.set_mobility_model(model)
+        ctx.set_fmm_params(8, 0)
+        ctx.build_contacts_spheres(t(p.pos), t(p.radius), p.gap_abs, p.gap_rel)
+        ctx.assemble_D()
+        ctx.lcp_q(p.dt, ctx.mobility_apply(t(p.force), mu=p.mu))
+        rs[model] = ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=p.max_iter)
+    ctx.set_mobility_model("rpy")
+    rf, rd = rs["rpy_fmm"], rs["rpy"]
+    assert rf["status"] == 0 and rf["residual"] < p.tol
+    gf, gd = rf["gamma"].cpu().numpy(), rd["gamma"].cpu().numpy()
+    assert _relL2(gf, gd) <= 1e-3
+    sysm = oracle.system_for(p)
+    F = oracle.apply_D(p.n, sysm.ct, gf) + p.force
+    go = sysm.lcp_q(p.dt, sysm.mobility(F))
+    q = sysm.lcp_q(p.dt, sysm.mobility(p.force))
+    phi = float(np.linalg.norm(np.minimum(gf, go)))
+    assert phi <= 1e-5 * float(np.linalg.norm(q)), phi
+
+
+def test_fmm_rejects_polydisperse_and_bad_params(ctx):
+    p = make_problem("C2", n=3000)
+    ctx.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+    ctx.set_mobility_model("rpy_fmm")
+    with pytest.raises(ScError):
+        ctx.mobility_apply(_cuda(p.force))
+    ctx.set_mobility_model("rpy")
+    with pytest.raises(ScError):
+        ctx.set_fmm_params(5, 0)
