@@ -122,9 +122,20 @@ def cpu_baseline(seconds_target=15.0):
     oracle.rpy_apply_rows(p.pos, p.radius, p.mu, FT, 0, rows2)
     dt2 = time.perf_counter() - t0
     pairs = rows2 * (p.n - 1)
-    return {"value": pairs / dt2, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": pairs / dt2, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
             "sample": f"oracle RPY apply (long-double sums), {rows2} target rows x {p.n} sources of {WORKLOAD}, "
                       f"{dt2:.1f} s, OMP over rows, threads={os.environ.get('OMP_NUM_THREADS', cores)}"}
+
+
+def _cpu_model():
+    """The host CPU model (lscpu / /proc/cpuinfo), recorded beside the CPU baseline."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def run_reference(args, rank, world):
@@ -152,7 +163,8 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": _config(args, world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": _cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -316,8 +316,9 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
   __shared__ double sl[NB * 3];
   __shared__ double4 sp[TS], sfs[TS];
   const int64_t b = blockIdx.x;
-  const int32_t i0 = lstart[b], i1 = lstart[b + 1];
-  if (i0 == i1) return;
+  // grid.y: chunk of TS targets of the leaf (the leaf's targets in parallel CTAs)
+  const int32_t i0 = lstart[b] + static_cast<int32_t>(blockIdx.y) * TS, i1 = min(lstart[b + 1], i0 + TS);
+  if (i0 >= i1) return;
   const int D = 1 << g.L;
   const int bx = static_cast<int>(b % D), by = static_cast<int>((b / D) % D), bz = static_cast<int>(b / D / D);
   double cx, cy, cz, w;
@@ -431,7 +432,8 @@ int fmm_launch(sc_ctx* ctx, const Geom& g, const double4* f4, double mu, double4
     transfer_kernel<NN, false><<<static_cast<unsigned>(nbox(l + 1)), nb, 0, ctx->stream>>>(
         l, Lc + lo[l] * NB * 3, Lc + lo[l + 1] * NB * 3, done);
   const double scale = 1.0 / (8.0 * 3.14159265358979323846 * mu);
-  l2p_p2p_kernel<NN><<<static_cast<unsigned>(nbox(L)), 128, 0, ctx->stream>>>(
+  const dim3 gp(static_cast<unsigned>(nbox(L)), static_cast<unsigned>(std::max<int64_t>(1, (ctx->fmm_maxleaf + 127) / 128)));
+  l2p_p2p_kernel<NN><<<gp, 128, 0, ctx->stream>>>(
       ctx->fmm_spos4.p, ctx->fmm_sf4.p, ctx->fmm_sidx.p, ctx->fmm_lstart.p, g, Lc, lo[L], scale, u4, ctx->derr,
       done);
   timer_end(ctx, SC_K_RPY);
@@ -529,15 +531,19 @@ int fmm_setup(sc_ctx* ctx) {
   // every overlapping pair in neighbouring leaves), chosen to balance the P2P and M2L work
   int L = ctx->fmm_leaf_level;
   const int Lmax = std::max(2, static_cast<int>(std::floor(std::log2(ext / (2.0 * a)))));
-  if (L <= 0) {
+  if (L <= 0) {  // cost model: pair evaluations of P2P (27 leaves) and M2L (<= 189 boxes, n^6 node
+                 // pairs, ~0.8 of a P2P pair's cost); at least 2 CTAs per SM of leaves when N allows
     double best = 1e300;
     const double nb3 = static_cast<double>(nn) * nn * nn;
     for (int l = 2; l <= std::min(Lmax, 7); ++l) {
       const double leaves = static_cast<double>(nbox(l));
       const double p2p = static_cast<double>(n) * 27.0 * (static_cast<double>(n) / leaves);
-      const double m2l = 1.15 * leaves * 189.0 * nb3 * nb3;
-      if (p2p + m2l < best) {
-        best = p2p + m2l;
+      const double m2l = 0.8 * 1.15 * leaves * 150.0 * nb3 * nb3;
+      const double fill = std::min(1.0, leaves * std::max(1.0, static_cast<double>(n) / leaves / 128.0) /
+                                            (2.0 * std::max(ctx->num_sms, 1)));
+      const double cost = (p2p + m2l) / fill;
+      if (cost < best) {
+        best = cost;
         L = l;
       }
     }
@@ -564,6 +570,12 @@ int fmm_setup(sc_ctx* ctx) {
                                                                                   ctx->fmm_idx0.p, ctx->fmm_cnt.p);
   if (int rc = check_launch(ctx, "fmm_leaf_of")) return rc;
   if (int rc = exclusive_scan_i32(ctx, ctx->fmm_cnt.p, ctx->fmm_lstart.p, nleaf, ctx->scan_tmp.p)) return rc;
+  {  // the fullest leaf (the P2P grid's chunks per leaf)
+    std::vector<int32_t> hc(nleaf);
+    SC_CUDA(cudaMemcpyAsync(hc.data(), ctx->fmm_cnt.p, sizeof(int32_t) * nleaf, cudaMemcpyDeviceToHost, ctx->stream));
+    SC_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->fmm_maxleaf = *std::max_element(hc.begin(), hc.end());
+  }
   size_t tmp_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key_in, key_out, ctx->fmm_idx0.p, ctx->fmm_sidx.p,
                                   static_cast<int>(n), 0, 3 * L, ctx->stream);

@@ -121,6 +121,7 @@ struct sc_ctx {
                                 // 2: BASELINE RPY by the fast summation (NEXT row f4(i), fmm.cu)
   // fast RPY summation (fmm.cu): Chebyshev order, leaf level (0: automatic), the tree of the bodies
   int fmm_order = 6, fmm_leaf_level = 0, fmm_L_used = 0;
+  int64_t fmm_maxleaf = 0;      // bodies in the fullest leaf
   bool fmm_ready = false;       // tree built for the current bodies
   double fmm_geom[4] = {};      // root cube corner (x, y, z) and side
   sc::DBuf<uint32_t> fmm_key;
