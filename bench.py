@@ -392,6 +392,28 @@ def other_configs():
                         "per iteration (the persistent rods loop has no per-kernel events)"}
         res[name] = d
         ctx.close()
+    # C5 with the fast O(N) RPY summation (NEXT row f4(i), order 8, approximate operator: rel. L2
+    # error of the apply ~1e-6): the same 50 fixed iterations, for the BBPGD-iterations/s context
+    p = make_problem("C5")
+    t = lambda a: torch.as_tensor(a, device="cuda:0")
+    ctx = Context(0)
+    ctx.set_mobility_model("rpy_fmm")
+    ctx.set_fmm_params(8, 0)
+    kw = dict(radius=t(p.radius), gap_abs=p.gap_abs, gap_rel=p.gap_rel, mu=p.mu, dt=p.dt, tol=p.tol,
+              max_iter=FIXED_ITERS, fixed_iters=True)
+    ctx.collision_step("spheres", t(p.pos), t(p.force), **kw)
+    s = ctx.torch_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    r = ctx.collision_step("spheres", t(p.pos), t(p.force), **kw)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    res["C5_fast_summation_order8"] = {"n": p.n, "n_c": r["nc"], "bbpgd_iters": r["iters"], "step_ms": ms,
+                                       "bbpgd_iters_per_s": r["iters"] / (ms / 1e3), "fmm": ctx.fmm_info(),
+                                       "note": "approximate RPY operator (DESIGN.md section 11); not part of value"}
+    ctx.close()
     return res
 
 

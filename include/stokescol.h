@@ -53,6 +53,8 @@ typedef enum {
 
 /* Library version (major*10000 + minor*100 + patch). */
 int sc_version(void);
+/* Build flags: bit 0 = checked build (device-side bounds asserts, build.py -DSC_CHECKS=1). */
+int sc_build_flags(void);
 
 /* ---------------------------------------------------------------- context */
 /* One context per GPU.  device: CUDA ordinal.  stream: a cudaStream_t to

@@ -27,7 +27,7 @@ EXPORTS = [
     "sc_plan_partition", "sc_set_emulated_world", "sc_set_rpy_kernel", "sc_time_step", "sc_apgd_solve",
     "sc_set_walls", "sc_set_mobility_model", "sc_minmap_residual", "sc_set_residual_trace",
     "sc_get_residual_trace", "sc_comm_info", "sc_sym_pair_table", "sc_set_wall_velocities", "sc_get_walls",
-    "sc_set_fmm_params", "sc_get_fmm_info",
+    "sc_set_fmm_params", "sc_get_fmm_info", "sc_build_flags",
 ]
 
 
@@ -71,6 +71,7 @@ def load(build_if_missing: bool = True):
     pp = C.POINTER(C.c_void_p)
     sig = {
         "sc_version": (ci, []),
+        "sc_build_flags": (ci, []),
         "sc_create": (ci, [pp, ci, vp]),
         "sc_nccl_unique_id": (ci, [vp]),
         "sc_create_dist": (ci, [pp, ci, vp, vp, ci, ci]),

@@ -485,6 +485,7 @@ using namespace sc;
 extern "C" {
 
 int sc_version(void) { return 10000; }
+int sc_build_flags(void) { return SC_CHECKS ? 1 : 0; }
 
 static int create_common(sc_ctx** out, int device, void* stream) {
   if (out == nullptr) return SC_EINVAL;

@@ -277,6 +277,7 @@ __global__ void pair_search(const double4* __restrict__ s4, const double4* __res
         }
         if (hit) {
           if (EMIT) {
+            SC_DCHECK(o < off[i + 1]);
             ci[o] = i;
             cj[o] = j;
             ++o;
@@ -290,6 +291,7 @@ __global__ void pair_search(const double4* __restrict__ s4, const double4* __res
     double gap, P[3];
     if (wall_test<KIND>(pi, ti, walls.w[k], st, rt, gap, P)) {
       if (EMIT) {
+        SC_DCHECK(o < off[i + 1]);
         ci[o] = i;
         cj[o] = static_cast<int32_t>(n + k);
         ++o;

@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
           if (qx < 0 || qy < 0 || qz < 0 || qx >= D || qy >= D || qz >= D) continue;
           const int64_t q = (static_cast<int64_t>(qz) * D + qy) * D + qx;
           const int32_t j0 = lstart[q], j1 = lstart[q + 1];
+          SC_DCHECK(j0 >= 0 && j0 <= j1 && j1 <= lstart[int64_t(1) << (3 * g.L)]);
           for (int32_t c0 = j0; c0 < j1; c0 += TS) {
             const int cn = min(TS, j1 - c0);
             __syncthreads();
@@ -403,6 +404,7 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
       ux = fma(cs, fi.x, ux);
       uy = fma(cs, fi.y, uy);
       uz = fma(cs, fi.z, uz);
+      SC_DCHECK(sidx[k] >= 0 && sidx[k] < lstart[int64_t(1) << (3 * g.L)]);
       u4[sidx[k]] = make_double4(scale * ux, scale * uy, scale * uz, 0.0);
     }
   }

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kT) gather_kernel(
     const double* __restrict__ g_old,
     double* __restrict__ gam_new, const DevScalars* __restrict__ dsc, int64_t n, int64_t nout,
     const double4* __restrict__ dir4, const double4* __restrict__ mob4, double4* __restrict__ out4,
-    double* __restrict__ outFT, const int32_t* __restrict__ done) {
+    double* __restrict__ outFT, const int32_t* __restrict__ done, int64_t nc_chk) {
   if (done != nullptr && *done) return;
   const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t b = gt / LPB;
@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(kT) gather_kernel(
   const double alpha = MODE == kProj ? dsc->alpha : 0.0;
   double fx = 0, fy = 0, fz = 0, tx = 0, ty = 0, tz = 0;
   const int32_t e0 = real ? row_ptr[b] : 0, e1 = real ? row_ptr[b + 1] : 0;
+  SC_DCHECK(e0 >= 0 && e0 <= e1 && e1 <= 2 * nc_chk);
   // rods: the body's axis and drag coefficients are independent of the incidence chain -- issue
   // their loads first so they overlap it
   double4 tb = make_double4(0, 0, 0, 0), mb = make_double4(0, 0, 0, 0);
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(kT) gather_kernel(
     for (int32_t e = e0 + k; e < e1; e += LPB) {
       const int32_t v = inc[e];
       const int32_t l = v >> 1;
+      SC_DCHECK(l >= 0 && l < nc_chk);
       double gm;
       if (MODE == kProj) {
         const double x = __dsub_rn(a[l], __dmul_rn(alpha, g_old[l]));  // gamma - alpha g (Step 8)
@@ -137,11 +139,13 @@ __global__ void __launch_bounds__(kR) dt_kernel(
   int32_t l0, l1;
   chunk_bounds(first_ptr, n, nc, c, l0, l1);
   double p[4] = {0, 0, 0, 0};
+  SC_DCHECK(l0 >= 0 && l0 <= l1 && l1 <= nc);
   for (int32_t l = l0 + threadIdx.x; l < l1; l += kR) {
     double v = 0.0;
     if (MODE != kDtInitQ) {
       if (KIND == kSpheres) {
         const int32_t i = ci[l], j = cj[l];
+        SC_DCHECK(i >= 0 && i < n && j > i && j < n + SC_MAX_WALLS);
         const bool wall = j >= n;  // a wall (NEXT row f2): static, not in the mobility
         const double4 nv = nrm4[l];
         const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
@@ -330,11 +334,11 @@ int launch_gather_proj(sc_ctx* ctx, const double* gam_old, const double* g_old, 
   if (ctx->kind == kSpheres)
     gather_kernel<kSpheres, kProj, kOutF4, kLpbS><<<nblk(ctx->npad * kLpbS), kT, 0, ctx->stream>>>(
         ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, gam_old, g_old, gam_new, ctx->dsc, ctx->n, ctx->npad,
-        nullptr, nullptr, ctx->f4.p, nullptr, done);
+        nullptr, nullptr, ctx->f4.p, nullptr, done, ctx->nc);
   else
     gather_kernel<kRods, kProj, kOutRodU, kLpbR><<<nblk(ctx->npad * kLpbR), kT, 0, ctx->stream>>>(
         ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, gam_old, g_old, gam_new, ctx->dsc, ctx->n,
-        ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done);
+        ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done, ctx->nc);
   timer_end(ctx, SC_K_GATHER);
   return check_launch(ctx, "gather_proj");
 }
@@ -346,21 +350,21 @@ int launch_gather_raw(sc_ctx* ctx, const double* v, double mu, double* FT_user) 
     if (ctx->kind == kSpheres)
       gather_kernel<kSpheres, kRaw, kOutFT, kLpbS><<<nblk(ctx->n * kLpbS), kT, 0, ctx->stream>>>(
           ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n, ctx->n,
-          nullptr, nullptr, nullptr, FT_user, nullptr);
+          nullptr, nullptr, nullptr, FT_user, nullptr, ctx->nc);
     else
       gather_kernel<kRods, kRaw, kOutFT, kLpbR><<<nblk(ctx->n * kLpbR), kT, 0, ctx->stream>>>(
           ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n, ctx->n,
-          nullptr, nullptr, nullptr, FT_user, nullptr);
+          nullptr, nullptr, nullptr, FT_user, nullptr, ctx->nc);
   } else {
     const int32_t* done = &ctx->dsc->done;
     if (ctx->kind == kSpheres)
       gather_kernel<kSpheres, kRaw, kOutF4, kLpbS><<<nblk(ctx->npad * kLpbS), kT, 0, ctx->stream>>>(
           ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n, ctx->npad,
-          nullptr, nullptr, ctx->f4.p, nullptr, done);
+          nullptr, nullptr, ctx->f4.p, nullptr, done, ctx->nc);
     else
       gather_kernel<kRods, kRaw, kOutRodU, kLpbR><<<nblk(ctx->npad * kLpbR), kT, 0, ctx->stream>>>(
           ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n,
-          ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done);
+          ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done, ctx->nc);
   }
   timer_end(ctx, SC_K_GATHER);
   return check_launch(ctx, "gather_raw");

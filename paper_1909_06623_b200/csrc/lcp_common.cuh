@@ -89,6 +89,7 @@ __device__ __forceinline__ void rods_gather_lane(int32_t e0, int32_t e1, int k, 
   for (int32_t e = e0 + k; e < e1; e += LPB) {
     const int32_t v = inc[e];
     const int32_t l = v >> 1;
+    SC_DCHECK(l >= 0);
     double gm;
     if (PROJ) {
       const double x = __dsub_rn(a[l], __dmul_rn(alpha, g_old[l]));  // Step 8
@@ -123,6 +124,7 @@ __device__ __forceinline__ double rods_dt_value(int64_t l, int64_t n, const int3
                                                 const int32_t* __restrict__ cj, const double4* __restrict__ nrm4,
                                                 const double4* __restrict__ rxn4, const double4* u4) {
   const int32_t i = ci[l], j = cj[l];
+  SC_DCHECK(i >= 0 && i < n && j > i && j < n + SC_MAX_WALLS);
   const bool wall = j >= n;
   const double4 nv = nrm4[l];
   double4 ui, wi, uj = make_double4(0.0, 0.0, 0.0, 0.0), wj = uj;

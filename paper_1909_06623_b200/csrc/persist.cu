@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(kPT) bbpgd_persistent_kernel(PersistArgs a) {
       for (int32_t e = e0 + k; e < e1; e += 2) {
         const int32_t v = a.inc[e];
         const int32_t l = v >> 1;
+        SC_DCHECK(l >= 0 && l < a.nc);
         const double x = __dsub_rn(__ldcg(gmo + l), __dmul_rn(alpha, __ldcg(go + l)));
         const double gm = x > 0.0 ? x : 0.0;
         if ((v & 1) == 0) gmn[l] = gm;
@@ -173,6 +174,7 @@ __global__ void __launch_bounds__(kPT) bbpgd_persistent_kernel(PersistArgs a) {
       double p[4] = {0, 0, 0, 0};
       for (int32_t l = l0 + threadIdx.x; l < l1; l += kR) {
         const int32_t i = a.ci[l], j = a.cj[l];
+        SC_DCHECK(l < a.nc && i >= 0 && i < a.n && j > i && j < a.n + SC_MAX_WALLS);
         const double4 nv = a.nrm4[l];
         const double4 ui = ldcg4(&a.u4[i]);
         const double4 uj = j < a.n ? ldcg4(&a.u4[j]) : make_double4(0, 0, 0, 0);  // j >= n: a wall

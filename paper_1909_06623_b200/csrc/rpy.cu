@@ -127,6 +127,7 @@ __device__ __forceinline__ void fx_limbs(double v, double scale, long long& x0, 
 }
 __device__ __forceinline__ void fx_red3(long long* acc /* [3 comps][3 limbs] */, double vx, double vy, double vz,
                                         double scale, bool& bad) {
+  SC_DCHECK(acc != nullptr);
   const double v[3] = {vx, vy, vz};
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -432,6 +433,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   // hs > 1 (small N, one GPU): the CTA takes the source part h of SJ only (16/hs sub-blocks)
   const int2 pr = pairs[blockIdx.x / hs];
   const int h = static_cast<int>(blockIdx.x % hs);
+  SC_DCHECK(pr.x >= 0 && pr.y >= 0 && (pr.x + 1) * int64_t(kSymSB) <= npad && (pr.y + 1) * int64_t(kSymSB) <= npad);
   constexpr int nph = kSymNsub / hs;
   // HS >= 8: fewer source sub-blocks than warps -> per-warp reverse accumulators
   // (NW x 512/HS x 3 doubles, within the 512 x 3 of the shared allocation)
@@ -705,6 +707,7 @@ __global__ void rpy_sym_combine_kernel(long long* __restrict__ acc, const FxScal
     const long long near_bits = __double_as_longlong(4.0 * (a_mono * a_mono));
     for (int32_t e = near_ptr[row]; e < near_ptr[row + 1]; ++e) {
       const int32_t j = near_idx[e];
+      SC_DCHECK(j >= 0 && j < n && j != row);
       const double4 pj = pos4[j];
       const double4 fj = f4[j];
       double dx, dy, dz;

@@ -12,6 +12,18 @@
 
 #include "stokescol.h"
 
+// Checked build (-DSC_CHECKS=1, build.py): device-side bounds asserts on the indexed accesses of the
+// hot kernels (compute-sanitizer is not available on this pool; tests run against this build too).
+#ifndef SC_CHECKS
+#define SC_CHECKS 0
+#endif
+#if SC_CHECKS
+#include <cassert>
+#define SC_DCHECK(cond) assert(cond)
+#else
+#define SC_DCHECK(cond) ((void)0)
+#endif
+
 namespace sc {
 
 constexpr int kRpyThreads = 64;         // threads per RPY CTA

@@ -143,3 +143,45 @@ def test_symmetric_rpy_fixed_point_bitwise_repeatable(ctx, n):
     for u in U[1:]:
         assert torch.equal(u, U[0])
     assert float((U[0] - Ur).norm() / Ur.norm()) <= 1e-13
+
+
+@pytest.mark.parametrize("name,n", [("C1", None), ("C2", 4096), ("C4", 20000), ("C5", 9000)])
+def test_results_bitwise_stable_under_schedule_perturbation(ctx, name, n):
+    """Race proxy (compute-sanitizer is closed on this pool): a concurrent SM-occupying workload on
+    another stream changes which CTAs run when (persistent grid barriers, the symmetric kernel's
+    shared reverse accumulators and RED limbs, the last-CTA finalize); every result must stay
+    bitwise identical to an undisturbed solve."""
+    p = make_problem(name, n=n, fixed_iters=0)
+
+    def solve():
+        if p.kind == "spheres":
+            ctx.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+        else:
+            ctx.build_contacts_rods(_cuda(p.pos), _cuda(p.direction), _cuda(p.length), p.rod_radius, p.gap_abs)
+        ctx.assemble_D()
+        U = ctx.mobility_apply(_cuda(p.force), mu=p.mu)
+        ctx.lcp_q(p.dt, U)
+        r = ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=min(p.max_iter, 300))
+        return U, r
+
+    U0, r0 = solve()
+    side = torch.cuda.Stream()
+    a = torch.randn(4096, 4096, device="cuda", dtype=torch.float32)
+    for k in range(3):
+        with torch.cuda.stream(side):
+            for _ in range(20 + 10 * k):
+                a = torch.tanh(a @ a.T * 1e-3)  # keeps SMs busy while the solve is enqueued
+        U1, r1 = solve()
+        torch.cuda.synchronize()
+        assert torch.equal(U0, U1)
+        assert r1["iters"] == r0["iters"] and r1["residual"] == r0["residual"]
+        for key in ("gamma", "g", "Fc", "Uc"):
+            assert torch.equal(r0[key], r1[key]), (k, key)
+
+
+def test_checked_build_flag_matches_the_loaded_library(ctx):
+    """SC_LIB=.../libstokescol_checked.so runs the suite against the checked build (device-side
+    bounds asserts); its flag says so, so a checked run cannot silently use the release build."""
+    import os
+    want = 1 if "checked" in os.environ.get("SC_LIB", "") else 0
+    assert ctx.lib.sc_build_flags() & 1 == want
