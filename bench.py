@@ -274,9 +274,10 @@ def main():
                 "algorithmic_flops_per_pair": FLOPS_PER_PAIR,
                 "hw_fp64_instr_per_ordered_pair": 18 if kern == "rpy_sym_kernel" else 26,
                 "ncu_fp64_pipe_active_pct": prof.get("fp64_pipe_pct"), "ncu_profile": prof.get("file"),
-                "traffic_note": "DRAM bytes per launch are the fixed-order partial sums, written once per "
-                                "(partner super-block, row) slot for the deterministic combine (N^2/512 x 24 B); "
-                                "the kernel is FP64-ALU bound, that traffic is ~0.5% of HBM bandwidth over its run",
+                "traffic_note": "dram read+write of one launch (ncu --set full, profiles/r02): positions and forces "
+                                "(~17 MB) re-read across super-block pairs; the fixed-point row accumulators "
+                                "(19 MB of int64 limbs, RED.ADD.64) stay in L2 -- 0 B of DRAM writes (round 1's "
+                                "per-(partner, row) slots wrote 3.2 GB per launch)",
                 "peak_note": "FP64 derived from unit counts: 148 SM x 64 FP64 lanes x 2 flop x 1.965 GHz "
                              "(DFMA microbenchmark on this pool: 34.24 TFLOP/s); the symmetric kernel evaluates "
                              "each unordered pair once, so 37 algorithmic flops per ordered pair cost 18 FP64 "
