@@ -230,19 +230,21 @@ struct Dist {
       mine.push_back(c->rank);
   }
   const Part& own() const { return parts[emul || !on ? 0 : ctx->rank]; }
-  int proj_own(const double* gmo, const double* go, double* gmn) {
+  int proj_own(int pp) {
     for (int r : mine)
-      if (int rc = launch_proj_own(ctx, gmo, go, gmn, parts[r].l0, parts[r].l1)) return rc;
+      if (int rc = launch_proj_own(ctx, pp, parts[r].l0, parts[r].l1)) return rc;
     return 0;
   }
-  // every rank's constraint slice of v -> full vector on every rank
-  int bcast(double* v) {
+  // every rank's constraint slice of the packed state st -> full vector on every rank
+  int bcast(double2* st) {
     if (!on || emul) return 0;
     const Part& p = own();
+    double* v = reinterpret_cast<double*>(st);
     NCCL_CHECK(ncclGroupStart());
     for (int r = 0; r < W; ++r) {
       if (p.lcnt[r] == 0) continue;
-      NCCL_CHECK(ncclBroadcast(v + p.loff[r], v + p.loff[r], p.lcnt[r], ncclDouble, r, ctx->comm, ctx->stream));
+      NCCL_CHECK(ncclBroadcast(v + 2 * p.loff[r], v + 2 * p.loff[r], 2 * p.lcnt[r], ncclDouble, r, ctx->comm,
+                               ctx->stream));
     }
     NCCL_CHECK(ncclGroupEnd());
     return 0;
@@ -278,11 +280,11 @@ struct Dist {
     return 0;
   }
   // D^T over this process's chunks.  One GPU: fused with K-FINALIZE (returns fused = true).
-  int dt(int mode, const double* gam_new, const double* gam_old, const double* g_old, double* g_out, bool* fused) {
+  int dt(int mode, int pp, bool* fused) {
     *fused = !on;
-    if (!on) return launch_dt(ctx, mode, gam_new, gam_old, g_old, g_out, 0, ctx->nchunks, true);
+    if (!on) return launch_dt(ctx, mode, pp, nullptr, nullptr, 0, ctx->nchunks, true);
     for (int r : mine)
-      if (int rc = launch_dt(ctx, mode, gam_new, gam_old, g_old, g_out, parts[r].c0, parts[r].c1, false)) return rc;
+      if (int rc = launch_dt(ctx, mode, pp, nullptr, nullptr, parts[r].c0, parts[r].c1, false)) return rc;
     return 0;
   }
   // chunk partials -> reduced vector; returns the buffer K-FINALIZE reads
@@ -840,6 +842,7 @@ int sc_assemble_D(sc_ctx* ctx) {
   for (int k = 0; k < 2; ++k) {
     if (int rc = ensure(ctx, ctx->gam[k], nc)) return rc;
     if (int rc = ensure(ctx, ctx->g[k], nc)) return rc;
+    if (int rc = ensure(ctx, ctx->st[k], nc)) return rc;
   }
   if (int rc = ensure(ctx, ctx->q, nc)) return rc;
   if (int rc = ensure(ctx, ctx->chunk_part, ctx->nchunks * kPartials)) return rc;
@@ -860,7 +863,7 @@ int sc_apply_D(sc_ctx* ctx, const double* gamma, double* FT) {
   if (int rc = st.in(gamma, ctx->nc, &dg)) return rc;
   if (int rc = st.out(FT, 6 * ctx->n, &dF)) return rc;
   if (ctx->n > 0) {
-    if (int rc = launch_gather_raw(ctx, dg, 1.0, dF)) return rc;
+    if (int rc = launch_gather_raw(ctx, dg, 1, 1.0, dF)) return rc;
   }
   if (int rc = st.finish()) return rc;
   return SC_OK;
@@ -1000,11 +1003,14 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
   SC_CUDA(cudaMemsetAsync(ctx->chunk_part.p, 0, sizeof(double) * ctx->nchunks * kPartials, ctx->stream));
 
   // mvop(v): u4 = Mobility(D v)  (spheres: f4 then RPY; rods: fused gather + drag)
-  auto mvop_raw = [&](const double* v) -> int {
-    if (int rc = launch_gather_raw(ctx, v, mu, nullptr)) return rc;
+  auto mvop_raw = [&](const double* v, int vstride) -> int {
+    if (int rc = launch_gather_raw(ctx, v, vstride, mu, nullptr)) return rc;
     if (spheres) return D.rpy(mu, done);
     return 0;
   };
+  // the components of the packed state st[k] = (gamma, g) as strided vectors
+  auto st_gamma = [&](int k) { return reinterpret_cast<const double*>(ctx->st[k].p); };
+  auto st_g = [&](int k) { return reinterpret_cast<const double*>(ctx->st[k].p) + 1; };
   bool fused = false;  // set by D.dt: the D^T kernel already ran K-FINALIZE
   auto reduce = [&](int mode) -> int {
     if (fused) return 0;
@@ -1020,14 +1026,14 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     } else {
       SC_CUDA(cudaMemcpyAsync(gam0, dgam, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
     }
-    // projection onto gamma >= 0 via the proj kernel with alpha = 0 (Step 1)
-    if (int rc = launch_proj_own(ctx, gam0, gam0, gam0, 0, nc)) return rc;
-    if (int rc = mvop_raw(gam0)) return rc;
-    if (int rc = D.dt(2, gam0, nullptr, nullptr, ctx->g[0].p, &fused)) return rc;
+    // projection onto gamma >= 0 (Step 1), into the packed state
+    if (int rc = launch_pack_gamma0(ctx, gam0)) return rc;
+    if (int rc = mvop_raw(st_gamma(0), 2)) return rc;
+    if (int rc = D.dt(2, 0, &fused)) return rc;
   } else {
-    SC_CUDA(cudaMemsetAsync(gam0, 0, nc * sizeof(double), ctx->stream));
+    SC_CUDA(cudaMemsetAsync(ctx->st[0].p, 0, nc * sizeof(double2), ctx->stream));
     SC_CUDA(cudaMemsetAsync(ctx->u4.p, 0, sizeof(double4) * ctx->u4.n, ctx->stream));
-    if (int rc = D.dt(3, gam0, nullptr, nullptr, ctx->g[0].p, &fused)) return rc;
+    if (int rc = D.dt(5, 0, &fused)) return rc;
   }
   if (int rc = reduce(2)) return rc;
   stt.mvops = 1;
@@ -1038,9 +1044,9 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
   if (ctx->hsc->nonfinite) return fail(ctx, SC_ENONFINITE, "non-finite initial gradient");
   if (!ctx->hsc->done) {
     // Step 6: alpha_0 = g0.g0 / g0.M g0 (second MVOP, on the full g_0)
-    if (int rc = D.bcast(ctx->g[0].p)) return rc;
-    if (int rc = mvop_raw(ctx->g[0].p)) return rc;
-    if (int rc = D.dt(1, nullptr, nullptr, ctx->g[0].p, nullptr, &fused)) return rc;
+    if (int rc = D.bcast(ctx->st[0].p)) return rc;
+    if (int rc = mvop_raw(st_g(0), 2)) return rc;
+    if (int rc = D.dt(1, 0, &fused)) return rc;
     if (int rc = reduce(1)) return rc;
     stt.mvops = 2;
     // Steps 7-16
@@ -1052,21 +1058,17 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     // all-reduced partials -- so every rank enqueues the same batches and the collectives match)
     const int batch = std::max(1, std::min(32, static_cast<int>(1e-3 / t_iter)));
     auto enqueue_iter = [&](int pp) -> int {
-      double* go = ctx->g[pp].p;
-      double* gmo = ctx->gam[pp].p;
-      double* gmn = ctx->gam[pp ^ 1].p;
-      double* gn = ctx->g[pp ^ 1].p;
       if (dist) {  // Steps 8-9 on own constraints, then every rank needs the full gamma_j
-        if (int rc = D.proj_own(gmo, go, gmn)) return rc;
-        if (int rc = D.bcast(gmn)) return rc;
-        if (int rc = mvop_raw(gmn)) return rc;
+        if (int rc = D.proj_own(pp)) return rc;
+        if (int rc = D.bcast(ctx->st[pp ^ 1].p)) return rc;
+        if (int rc = mvop_raw(st_gamma(pp ^ 1), 2)) return rc;
       } else {  // Steps 8-9 fused into the D-gather
-        if (int rc = launch_gather_proj(ctx, gmo, go, gmn, mu)) return rc;
+        if (int rc = launch_gather_proj(ctx, pp, mu)) return rc;
         if (spheres) {
           if (int rc = D.rpy(mu, done)) return rc;
         }
       }
-      if (int rc = D.dt(0, gmn, gmo, go, gn, &fused)) return rc;  // Steps 10-15
+      if (int rc = D.dt(0, pp, &fused)) return rc;  // Steps 10-15
       return reduce(0);
     };
     // Small problems (several iterations per host read, one GPU, no per-launch timing): the
@@ -1136,21 +1138,22 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
   if (!s.conv && !opts->fixed_iters) rc_final = SC_NOT_CONVERGED;
   double* gfin = ctx->gam[parity].p;
   double* gradfin = ctx->g[parity].p;
-  if (int rc = D.bcast(gradfin)) return rc;
+  if (int rc = D.bcast(ctx->st[parity].p)) return rc;  // (every rank's g slice)
+  if (int rc = launch_unpack_state(ctx, parity, gfin, gradfin)) return rc;
   if (int rc = check_flag(ctx, SC_EDEGENERATE, "coincident centres in the RPY sum")) return rc;
   // outputs
   SC_CUDA(cudaMemcpyAsync(dgam, gfin, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   if (dg) SC_CUDA(cudaMemcpyAsync(dg, gradfin, nc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   if (dF) {
-    if (int rc = launch_gather_raw(ctx, gfin, mu, dF)) return rc;
+    if (int rc = launch_gather_raw(ctx, gfin, 1, mu, dF)) return rc;
   }
   if (dU) {
     if (stt.iters == 0 && stt.mvops >= 2) {  // j_max = 0: u4 holds the alpha_0 product, recompute
-      if (int rc = mvop_raw(gfin)) return rc;
+      if (int rc = mvop_raw(gfin, 1)) return rc;
     }
     if (spheres && ctx->mobility_model == 1) {  // U_c = M D gamma with the coupling blocks (Omega_c)
       if (int rc = ensure(ctx, ctx->ft_tmp, 6 * n)) return rc;
-      if (int rc = launch_gather_raw(ctx, gfin, mu, ctx->ft_tmp.p)) return rc;
+      if (int rc = launch_gather_raw(ctx, gfin, 1, mu, ctx->ft_tmp.p)) return rc;
       if (int rc = launch_pack_ft(ctx, ctx->ft_tmp.p, ctx->f4.p, ctx->t4.p)) return rc;
       if (int rc = rpy6_apply(ctx, ctx->f4.p, ctx->t4.p, mu, dU)) return rc;
     } else if (spheres) {
@@ -1247,18 +1250,18 @@ int sc_apgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double*
   };
   // gout = M v + q; returns (v.Mv, q.v, phi(v)^2)
   auto mvop_grad = [&](const double* v, double* gout, double* out) -> int {
-    if (int rc = launch_gather_raw(ctx, v, mu, nullptr)) return rc;
+    if (int rc = launch_gather_raw(ctx, v, 1, mu, nullptr)) return rc;
     if (spheres) {
       if (int rc = D.rpy(mu, nullptr)) return rc;
     }
-    if (int rc = launch_dt(ctx, 4, v, nullptr, nullptr, gout, 0, ctx->nchunks, false)) return rc;
+    if (int rc = launch_dt(ctx, 4, 0, v, gout, 0, ctx->nchunks, false)) return rc;
     return sums(out);
   };
   SC_CUDA(cudaMemsetAsync(ctx->dsc, 0, sizeof(DevScalars), ctx->stream));  // done = 0 for the kernels
   // gamma_0 = 0: g_0 = q (the zero-vector MVOP, counted as in BBPGD), phi_0
   SC_CUDA(cudaMemsetAsync(x, 0, nc * sizeof(double), ctx->stream));
   SC_CUDA(cudaMemsetAsync(y, 0, nc * sizeof(double), ctx->stream));
-  if (int rc = launch_dt(ctx, 3, x, nullptr, nullptr, gy, 0, ctx->nchunks, false)) return rc;
+  if (int rc = launch_dt(ctx, 3, 0, x, gy, 0, ctx->nchunks, false)) return rc;
   if (int rc = sums(hs)) return rc;
   stt.mvops = 1;
   double phi = std::sqrt(hs[3]);

@@ -36,9 +36,9 @@ enum GatherOut { kOutF4 = 0, kOutRodU = 1, kOutFT = 2 };
 template <int KIND, int MODE, int OUT, int LPB>
 __global__ void __launch_bounds__(kT) gather_kernel(
     const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ inc, const double4* __restrict__ icol4,
-    const double4* __restrict__ nrm4, const double4* __restrict__ rxn4, const double* __restrict__ a,
-    const double* __restrict__ g_old,
-    double* __restrict__ gam_new, const DevScalars* __restrict__ dsc, int64_t n, int64_t nout,
+    const double4* __restrict__ nrm4, const double4* __restrict__ rxn4, const double* __restrict__ a, int astride,
+    const double2* __restrict__ st_old, double2* __restrict__ st_new, const DevScalars* __restrict__ dsc, int64_t n,
+    int64_t nout,
     const double4* __restrict__ dir4, const double4* __restrict__ mob4, double4* __restrict__ out4,
     double* __restrict__ outFT, const int32_t* __restrict__ done, int64_t nc_chk) {
   if (done != nullptr && *done) return;
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kT) gather_kernel(
   }
   if (KIND == kRods) {  // the signed columns of the incidences, streamed (assemble.cu)
     double f[6] = {0, 0, 0, 0, 0, 0};
-    rods_gather_lane<LPB, MODE == kProj>(e0, e1, k, alpha, inc, a, g_old, gam_new,
+    rods_gather_lane<LPB, MODE == kProj>(e0, e1, k, alpha, inc, a, astride, st_old, st_new,
                                          reinterpret_cast<const double2*>(icol4), f);
     fx = f[0]; fy = f[1]; fz = f[2]; tx = f[3]; ty = f[4]; tz = f[5];
   } else {
@@ -70,11 +70,12 @@ __global__ void __launch_bounds__(kT) gather_kernel(
       SC_DCHECK(l >= 0 && l < nc_chk);
       double gm;
       if (MODE == kProj) {
-        const double x = __dsub_rn(a[l], __dmul_rn(alpha, g_old[l]));  // gamma - alpha g (Step 8)
-        gm = x > 0.0 ? x : 0.0;                                        // projection (Step 9)
-        if ((v & 1) == 0) gam_new[l] = gm;                              // owner = first body
+        const double2 st = st_old[l];                              // (gamma_l, g_l)
+        const double x = __dsub_rn(st.x, __dmul_rn(alpha, st.y));  // gamma - alpha g (Step 8)
+        gm = x > 0.0 ? x : 0.0;                                    // projection (Step 9)
+        if ((v & 1) == 0) st_new[l].x = gm;                         // owner = first body
       } else {
-        gm = a[l];
+        gm = a[static_cast<int64_t>(l) * astride];
       }
       // incidence column (signed D_l block of this body, stored in incidence order: streamed)
       const double4 nv = icol4[e];
@@ -120,7 +121,9 @@ __global__ void __launch_bounds__(kR) finalize_kernel(const double* __restrict__
   finalize_block(part, nchunks, mode, s, red);
 }
 
-enum DtMode { kDtIter = 0, kDtAlpha0 = 1, kDtG0 = 2, kDtInitQ = 3, kDtGrad = 4 };
+// BBPGD modes on the packed state st = (gamma, g): kDtIter, kDtAlpha0, kDtG0 (warm start),
+// kDtInitSt (g_0 = q); APGD modes on plain vectors: kDtInitQ, kDtGrad.
+enum DtMode { kDtIter = 0, kDtAlpha0 = 1, kDtG0 = 2, kDtInitQ = 3, kDtGrad = 4, kDtInitSt = 5 };
 
 // One CTA per chunk c in [c0, c0 + gridDim.x).  FUSE (1 GPU): the last CTA to finish
 // (threadfence + counter) also runs K-FINALIZE, saving a launch per iteration; the sums are
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(kR) dt_kernel(
     const int32_t* __restrict__ first_ptr, int64_t n, int64_t nc, int64_t c0, const int32_t* __restrict__ ci,
     const int32_t* __restrict__ cj, const double4* __restrict__ nrm4, const double4* __restrict__ rxn4,
     const double4* __restrict__ u4, const double* __restrict__ q, const double* __restrict__ gam_new,
-    const double* __restrict__ gam_old, const double* __restrict__ g_old, double* __restrict__ g_out,
+    double* __restrict__ g_out, double2* __restrict__ st_old, double2* __restrict__ st_new,
     double* __restrict__ part, const int32_t* __restrict__ done, int64_t nchunks, DevScalars* __restrict__ sc,
     unsigned int* __restrict__ counter) {
   if (done != nullptr && *done) return;
@@ -142,7 +145,7 @@ __global__ void __launch_bounds__(kR) dt_kernel(
   SC_DCHECK(l0 >= 0 && l0 <= l1 && l1 <= nc);
   for (int32_t l = l0 + threadIdx.x; l < l1; l += kR) {
     double v = 0.0;
-    if (MODE != kDtInitQ) {
+    if (MODE != kDtInitQ && MODE != kDtInitSt) {
       if (KIND == kSpheres) {
         const int32_t i = ci[l], j = cj[l];
         SC_DCHECK(i >= 0 && i < n && j > i && j < n + SC_MAX_WALLS);
@@ -156,11 +159,17 @@ __global__ void __launch_bounds__(kR) dt_kernel(
       }
     }
     if (MODE == kDtIter) {
-      dt_iter_terms<false>(l, v, q, gam_new, gam_old, g_old, g_out, p);
+      dt_iter_terms<false>(l, v, q, st_old, st_new, p);
     } else if (MODE == kDtAlpha0) {
-      const double g0 = g_old[l];
+      const double g0 = st_old[l].y;
       p[0] = fma(g0, g0, p[0]);
       p[1] = fma(g0, v, p[1]);
+    } else if (MODE == kDtG0 || MODE == kDtInitSt) {  // g0 = D^T U + q (warm start) / = q (gamma0 = 0)
+      const double g = (MODE == kDtG0 ? v : 0.0) + q[l];
+      st_old[l].y = g;
+      const double gn = st_old[l].x;
+      const double m = gn < g ? gn : g;
+      p[3] = fma(m, m, p[3]);
     } else if (MODE == kDtGrad) {  // g = M x + q for x = gam_new; x.Mx, q.x, phi(x)^2 (APGD)
       const double x = gam_new[l];
       const double g = v + q[l];
@@ -169,8 +178,8 @@ __global__ void __launch_bounds__(kR) dt_kernel(
       p[0] = fma(x, v, p[0]);
       p[1] = fma(q[l], x, p[1]);
       p[2] = fma(m, m, p[2]);
-    } else {  // kDtG0 (warm start: g0 = D^T U + q) / kDtInitQ (gamma0 = 0: g0 = q)
-      const double g = (MODE == kDtG0 ? v : 0.0) + q[l];
+    } else {  // kDtInitQ (APGD, gamma0 = 0: g0 = q)
+      const double g = q[l];
       g_out[l] = g;
       const double gn = gam_new[l];
       const double m = gn < g ? gn : g;
@@ -202,14 +211,30 @@ __global__ void __launch_bounds__(kR) dt_kernel(
   if (threadIdx.x == 0) *counter = 0u;
 }
 
-__global__ void proj_own_kernel(const double* __restrict__ gam_old, const double* __restrict__ g_old,
-                                double* __restrict__ gam_new, const DevScalars* __restrict__ dsc, int64_t l0,
-                                int64_t l1) {
+__global__ void proj_own_kernel(const double2* __restrict__ st_old, double2* __restrict__ st_new,
+                                const DevScalars* __restrict__ dsc, int64_t l0, int64_t l1) {
   if (dsc->done) return;
   const int64_t l = l0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (l >= l1) return;
-  const double x = __dsub_rn(gam_old[l], __dmul_rn(dsc->alpha, g_old[l]));
-  gam_new[l] = x > 0.0 ? x : 0.0;
+  const double2 s = st_old[l];
+  const double x = __dsub_rn(s.x, __dmul_rn(dsc->alpha, s.y));
+  st_new[l].x = x > 0.0 ? x : 0.0;
+}
+
+// st = (max(0, gamma_0), 0): the projected initial guess (Step 1) into the packed state
+__global__ void pack_gamma0_kernel(const double* __restrict__ gam0, int64_t nc, double2* __restrict__ st) {
+  const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (l >= nc) return;
+  const double x = gam0[l];
+  st[l] = make_double2(x > 0.0 ? x : 0.0, 0.0);
+}
+__global__ void unpack_state_kernel(const double2* __restrict__ st, int64_t nc, double* __restrict__ gam,
+                                    double* __restrict__ g) {
+  const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (l >= nc) return;
+  const double2 s = st[l];
+  gam[l] = s.x;
+  g[l] = s.y;
 }
 
 __global__ void pack_ft_kernel(const double* __restrict__ FT, int64_t n, int64_t npad, double4* __restrict__ f4,
@@ -327,60 +352,80 @@ __global__ void __launch_bounds__(1024) minmap_kernel(const double* __restrict__
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
-int launch_gather_proj(sc_ctx* ctx, const double* gam_old, const double* g_old, double* gam_new, double mu) {
+// Steps 8-9 + F = D gamma on the packed state: st[pp] -> st[pp ^ 1].x (owner)
+int launch_gather_proj(sc_ctx* ctx, int pp, double mu) {
   (void)mu;
   const int32_t* done = &ctx->dsc->done;
+  const double2* so = ctx->st[pp].p;
+  double2* sn = ctx->st[pp ^ 1].p;
   timer_begin(ctx, SC_K_GATHER);
   if (ctx->kind == kSpheres)
     gather_kernel<kSpheres, kProj, kOutF4, kLpbS><<<nblk(ctx->npad * kLpbS), kT, 0, ctx->stream>>>(
-        ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, gam_old, g_old, gam_new, ctx->dsc, ctx->n, ctx->npad,
-        nullptr, nullptr, ctx->f4.p, nullptr, done, ctx->nc);
+        ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, nullptr, 1, so, sn, ctx->dsc, ctx->n,
+        ctx->npad, nullptr, nullptr, ctx->f4.p, nullptr, done, ctx->nc);
   else
     gather_kernel<kRods, kProj, kOutRodU, kLpbR><<<nblk(ctx->npad * kLpbR), kT, 0, ctx->stream>>>(
-        ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, gam_old, g_old, gam_new, ctx->dsc, ctx->n,
+        ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, nullptr, 1, so, sn, ctx->dsc, ctx->n,
         ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done, ctx->nc);
   timer_end(ctx, SC_K_GATHER);
   return check_launch(ctx, "gather_proj");
 }
 
-int launch_gather_raw(sc_ctx* ctx, const double* v, double mu, double* FT_user) {
+// F = D v for v[l * vstride] (vstride 2: a component of the packed state)
+int launch_gather_raw(sc_ctx* ctx, const double* v, int vstride, double mu, double* FT_user) {
   (void)mu;
   timer_begin(ctx, SC_K_GATHER);
   if (FT_user != nullptr) {
     if (ctx->kind == kSpheres)
       gather_kernel<kSpheres, kRaw, kOutFT, kLpbS><<<nblk(ctx->n * kLpbS), kT, 0, ctx->stream>>>(
-          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n, ctx->n,
-          nullptr, nullptr, nullptr, FT_user, nullptr, ctx->nc);
+          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, vstride, nullptr, nullptr, ctx->dsc,
+          ctx->n, ctx->n, nullptr, nullptr, nullptr, FT_user, nullptr, ctx->nc);
     else
       gather_kernel<kRods, kRaw, kOutFT, kLpbR><<<nblk(ctx->n * kLpbR), kT, 0, ctx->stream>>>(
-          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n, ctx->n,
-          nullptr, nullptr, nullptr, FT_user, nullptr, ctx->nc);
+          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, vstride, nullptr, nullptr, ctx->dsc,
+          ctx->n, ctx->n, nullptr, nullptr, nullptr, FT_user, nullptr, ctx->nc);
   } else {
     const int32_t* done = &ctx->dsc->done;
     if (ctx->kind == kSpheres)
       gather_kernel<kSpheres, kRaw, kOutF4, kLpbS><<<nblk(ctx->npad * kLpbS), kT, 0, ctx->stream>>>(
-          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n, ctx->npad,
-          nullptr, nullptr, ctx->f4.p, nullptr, done, ctx->nc);
+          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, vstride, nullptr, nullptr, ctx->dsc,
+          ctx->n, ctx->npad, nullptr, nullptr, ctx->f4.p, nullptr, done, ctx->nc);
     else
       gather_kernel<kRods, kRaw, kOutRodU, kLpbR><<<nblk(ctx->npad * kLpbR), kT, 0, ctx->stream>>>(
-          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, nullptr, nullptr, ctx->dsc, ctx->n,
-          ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done, ctx->nc);
+          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, vstride, nullptr, nullptr, ctx->dsc,
+          ctx->n, ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done, ctx->nc);
   }
   timer_end(ctx, SC_K_GATHER);
   return check_launch(ctx, "gather_raw");
 }
 
-int launch_proj_own(sc_ctx* ctx, const double* gam_old, const double* g_old, double* gam_new, int64_t l0,
-                    int64_t l1) {
+int launch_proj_own(sc_ctx* ctx, int pp, int64_t l0, int64_t l1) {
   if (l1 <= l0) return 0;
   timer_begin(ctx, SC_K_GATHER);
-  proj_own_kernel<<<nblk(l1 - l0), kT, 0, ctx->stream>>>(gam_old, g_old, gam_new, ctx->dsc, l0, l1);
+  proj_own_kernel<<<nblk(l1 - l0), kT, 0, ctx->stream>>>(ctx->st[pp].p, ctx->st[pp ^ 1].p, ctx->dsc, l0, l1);
   timer_end(ctx, SC_K_GATHER);
   return check_launch(ctx, "proj_own");
 }
 
-int launch_dt(sc_ctx* ctx, int mode, const double* gam_new, const double* gam_old, const double* g_old,
-              double* g_out, int64_t c0, int64_t c1, bool fuse) {
+int launch_pack_gamma0(sc_ctx* ctx, const double* gam0) {
+  if (ctx->nc == 0) return 0;
+  timer_begin(ctx, SC_K_MISC);
+  pack_gamma0_kernel<<<nblk(ctx->nc), kT, 0, ctx->stream>>>(gam0, ctx->nc, ctx->st[0].p);
+  timer_end(ctx, SC_K_MISC);
+  return check_launch(ctx, "pack_gamma0");
+}
+
+int launch_unpack_state(sc_ctx* ctx, int pp, double* gam, double* g) {
+  if (ctx->nc == 0) return 0;
+  timer_begin(ctx, SC_K_MISC);
+  unpack_state_kernel<<<nblk(ctx->nc), kT, 0, ctx->stream>>>(ctx->st[pp].p, ctx->nc, gam, g);
+  timer_end(ctx, SC_K_MISC);
+  return check_launch(ctx, "unpack_state");
+}
+
+// D^T over chunks [c0, c1).  BBPGD modes (0 iteration, 1 alpha_0, 2 warm g_0, 5 g_0 = q) on the packed
+// state st[pp] (-> st[pp ^ 1]); APGD modes (3 g = q, 4 gradient) on plain vectors x / g_out.
+int launch_dt(sc_ctx* ctx, int mode, int pp, const double* x, double* g_out, int64_t c0, int64_t c1, bool fuse) {
   if (c1 <= c0) return 0;
   if (fuse && (c0 != 0 || c1 != ctx->nchunks)) return fail(ctx, SC_EINVAL, "fused finalize needs all chunks");
   const unsigned grid = static_cast<unsigned>(c1 - c0);
@@ -388,36 +433,37 @@ int launch_dt(sc_ctx* ctx, int mode, const double* gam_new, const double* gam_ol
   const double4* u4 = ctx->u4.p;
   double* part = ctx->chunk_part.p;
   const double* q = ctx->q.p;
+  double2* so = ctx->st[pp].p;
+  double2* sn = ctx->st[pp ^ 1].p;
   const int32_t* fp = ctx->kind == kRods ? nullptr : ctx->first_ptr.p;  // rods: constraint tiles
 #define SC_DT(KIND, MODE)                                                                                       \
   do {                                                                                                          \
     if (fuse)                                                                                                   \
-      dt_kernel<KIND, MODE, true><<<grid, kR, 0, ctx->stream>>>(                                                \
-          fp, ctx->n, ctx->nc, c0, ctx->ci.p, ctx->cj.p, ctx->nrm4.p, ctx->rxn4.p, u4, q, gam_new, gam_old,        \
-          g_old, g_out, part, done, ctx->nchunks, ctx->dsc, ctx->dcount);                                       \
+      dt_kernel<KIND, MODE, true><<<grid, kR, 0, ctx->stream>>>(fp, ctx->n, ctx->nc, c0, ctx->ci.p, ctx->cj.p,    \
+                                                                ctx->nrm4.p, ctx->rxn4.p, u4, q, x, g_out, so, sn, \
+                                                                part, done, ctx->nchunks, ctx->dsc, ctx->dcount);  \
     else                                                                                                        \
-      dt_kernel<KIND, MODE, false><<<grid, kR, 0, ctx->stream>>>(                                               \
-          fp, ctx->n, ctx->nc, c0, ctx->ci.p, ctx->cj.p, ctx->nrm4.p, ctx->rxn4.p, u4, q, gam_new, gam_old,        \
-          g_old, g_out, part, done, ctx->nchunks, ctx->dsc, ctx->dcount);                                       \
+      dt_kernel<KIND, MODE, false><<<grid, kR, 0, ctx->stream>>>(fp, ctx->n, ctx->nc, c0, ctx->ci.p, ctx->cj.p,   \
+                                                                 ctx->nrm4.p, ctx->rxn4.p, u4, q, x, g_out, so,   \
+                                                                 sn, part, done, ctx->nchunks, ctx->dsc,          \
+                                                                 ctx->dcount);                                    \
   } while (0)
+#define SC_DT_ALL(KIND)                                \
+  switch (mode) {                                      \
+    case kDtIter: SC_DT(KIND, kDtIter); break;         \
+    case kDtAlpha0: SC_DT(KIND, kDtAlpha0); break;     \
+    case kDtG0: SC_DT(KIND, kDtG0); break;             \
+    case kDtGrad: SC_DT(KIND, kDtGrad); break;         \
+    case kDtInitSt: SC_DT(KIND, kDtInitSt); break;     \
+    default: SC_DT(KIND, kDtInitQ); break;             \
+  }
   timer_begin(ctx, SC_K_DT);
   if (ctx->kind == kSpheres) {
-    switch (mode) {
-      case kDtIter: SC_DT(kSpheres, kDtIter); break;
-      case kDtAlpha0: SC_DT(kSpheres, kDtAlpha0); break;
-      case kDtG0: SC_DT(kSpheres, kDtG0); break;
-      case kDtGrad: SC_DT(kSpheres, kDtGrad); break;
-      default: SC_DT(kSpheres, kDtInitQ); break;
-    }
+    SC_DT_ALL(kSpheres)
   } else {
-    switch (mode) {
-      case kDtIter: SC_DT(kRods, kDtIter); break;
-      case kDtAlpha0: SC_DT(kRods, kDtAlpha0); break;
-      case kDtG0: SC_DT(kRods, kDtG0); break;
-      case kDtGrad: SC_DT(kRods, kDtGrad); break;
-      default: SC_DT(kRods, kDtInitQ); break;
-    }
+    SC_DT_ALL(kRods)
   }
+#undef SC_DT_ALL
 #undef SC_DT
   timer_end(ctx, SC_K_DT);
   return check_launch(ctx, "dt");

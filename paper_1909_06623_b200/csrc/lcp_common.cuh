@@ -82,8 +82,8 @@ __device__ __forceinline__ void rods_load_uw(const double4* u4, int64_t b, doubl
 // incidence, streamed in incidence order (assemble.cu rod_incidence_columns, 3 double2 each).
 template <int LPB, bool PROJ>
 __device__ __forceinline__ void rods_gather_lane(int32_t e0, int32_t e1, int k, double alpha,
-                                                 const int32_t* __restrict__ inc, const double* a,
-                                                 const double* g_old, double* gam_new,
+                                                 const int32_t* __restrict__ inc, const double* a, int astride,
+                                                 const double2* st_old, double2* st_new,
                                                  const double2* __restrict__ icolr, double f[6]) {
 #pragma unroll 2
   for (int32_t e = e0 + k; e < e1; e += LPB) {
@@ -92,11 +92,12 @@ __device__ __forceinline__ void rods_gather_lane(int32_t e0, int32_t e1, int k, 
     SC_DCHECK(l >= 0);
     double gm;
     if (PROJ) {
-      const double x = __dsub_rn(a[l], __dmul_rn(alpha, g_old[l]));  // Step 8
-      gm = x > 0.0 ? x : 0.0;                                        // Step 9
-      if ((v & 1) == 0) gam_new[l] = gm;                              // owner = first body
+      const double2 s = st_old[l];                                // (gamma_l, g_l): one 16-B load
+      const double x = __dsub_rn(s.x, __dmul_rn(alpha, s.y));     // Step 8
+      gm = x > 0.0 ? x : 0.0;                                     // Step 9
+      if ((v & 1) == 0) st_new[l].x = gm;                         // owner = first body
     } else {
-      gm = a[l];
+      gm = a[static_cast<int64_t>(l) * astride];
     }
     const double2 c0 = icolr[3 * e], c1 = icolr[3 * e + 1], c2 = icolr[3 * e + 2];
     f[0] = fma(gm, c0.x, f[0]);
@@ -137,15 +138,18 @@ __device__ __forceinline__ double rods_dt_value(int64_t l, int64_t n, const int3
 }
 
 // Step 10 (g = D^T U + q, written) and the partial sums of Steps 11, 14-15 for constraint l:
-// s.s, s.y, y.y, min(gamma, g)^2 with s = gamma_new - gamma_old, y = g - g_old.
+// s.s, s.y, y.y, min(gamma, g)^2 with s = gamma_new - gamma_old, y = g - g_old.  The BBPGD state
+// is packed per constraint, st = (gamma_l, g_l) (one 16-B access in the gathers).
 template <bool CG>
-__device__ __forceinline__ void dt_iter_terms(int64_t l, double v, const double* __restrict__ q, const double* gam_new,
-                                              const double* gam_old, const double* g_old, double* g_out, double p[4]) {
+__device__ __forceinline__ void dt_iter_terms(int64_t l, double v, const double* __restrict__ q,
+                                              const double2* st_old, double2* st_new, double p[4]) {
   const double g = v + q[l];
-  g_out[l] = g;
-  const double gn = ldv<CG>(gam_new + l);
-  const double s = gn - ldv<CG>(gam_old + l);
-  const double y = g - ldv<CG>(g_old + l);
+  const double2 snw = CG ? __ldcg(st_new + l) : st_new[l];  // (gamma_new, -): full 16-B accesses,
+  st_new[l] = make_double2(snw.x, g);                         // coalesced, instead of 8-B halves
+  const double gn = snw.x;
+  const double2 so = CG ? __ldcg(st_old + l) : st_old[l];
+  const double s = gn - so.x;
+  const double y = g - so.y;
   const double m = gn < g ? gn : g;
   p[0] = fma(s, s, p[0]);
   p[1] = fma(s, y, p[1]);

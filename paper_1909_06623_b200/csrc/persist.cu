@@ -50,10 +50,8 @@ struct PersistArgs {
   const int32_t* cj;
   const double4* nrm4;
   const double* q;
-  double* gam0;  // gamma / g ping-pong: iteration j reads [j & 1], writes [(j & 1) ^ 1]
-  double* gam1;
-  double* g0;
-  double* g1;
+  double2* st0;  // packed (gamma, g) ping-pong: iteration j reads [j & 1], writes [(j & 1) ^ 1]
+  double2* st1;
   double* part;
   DevScalars* sc;
   int32_t* err;
@@ -73,10 +71,8 @@ __global__ void __launch_bounds__(kPT) bbpgd_persistent_kernel(PersistArgs a) {
   const int64_t warp = tid >> 5, nwarps = nthreads >> 5;
   while (!s.done) {
     const int pp = s.iter & 1;
-    const double* gmo = pp ? a.gam1 : a.gam0;
-    const double* go = pp ? a.g1 : a.g0;
-    double* gmn = pp ? a.gam0 : a.gam1;
-    double* gn = pp ? a.g0 : a.g1;
+    const double2* so = pp ? a.st1 : a.st0;
+    double2* sn = pp ? a.st0 : a.st1;
     const double alpha = s.alpha;
     // ---- A: projection + D-gather, 2 lanes per body (lcp.cu gather_kernel<kSpheres, kProj, kOutF4, 2>)
     for (int64_t t = tid; t < 2 * a.npad; t += nthreads) {
@@ -89,9 +85,10 @@ __global__ void __launch_bounds__(kPT) bbpgd_persistent_kernel(PersistArgs a) {
         const int32_t v = a.inc[e];
         const int32_t l = v >> 1;
         SC_DCHECK(l >= 0 && l < a.nc);
-        const double x = __dsub_rn(__ldcg(gmo + l), __dmul_rn(alpha, __ldcg(go + l)));
+        const double2 st = __ldcg(so + l);
+        const double x = __dsub_rn(st.x, __dmul_rn(alpha, st.y));
         const double gm = x > 0.0 ? x : 0.0;
-        if ((v & 1) == 0) gmn[l] = gm;
+        if ((v & 1) == 0) sn[l].x = gm;
         const double4 nv = a.icol4[e];
         fx = fma(gm, nv.x, fx);
         fy = fma(gm, nv.y, fy);
@@ -180,10 +177,11 @@ __global__ void __launch_bounds__(kPT) bbpgd_persistent_kernel(PersistArgs a) {
         const double4 uj = j < a.n ? ldcg4(&a.u4[j]) : make_double4(0, 0, 0, 0);  // j >= n: a wall
         const double v = fma(nv.z, ui.z - uj.z, fma(nv.y, ui.y - uj.y, nv.x * (ui.x - uj.x)));
         const double g = v + a.q[l];
-        gn[l] = g;
-        const double gnw = __ldcg(gmn + l);
-        const double sd = gnw - __ldcg(gmo + l);
-        const double y = g - __ldcg(go + l);
+        const double gnw = __ldcg(&sn[l].x);
+        sn[l] = make_double2(gnw, g);
+        const double2 sto = __ldcg(so + l);
+        const double sd = gnw - sto.x;
+        const double y = g - sto.y;
         const double m = gnw < g ? gnw : g;
         p[0] = fma(sd, sd, p[0]);
         p[1] = fma(sd, y, p[1]);
@@ -256,10 +254,8 @@ int bbpgd_persistent(sc_ctx* ctx, double mu) {
   a.cj = ctx->cj.p;
   a.nrm4 = ctx->nrm4.p;
   a.q = ctx->q.p;
-  a.gam0 = ctx->gam[0].p;
-  a.gam1 = ctx->gam[1].p;
-  a.g0 = ctx->g[0].p;
-  a.g1 = ctx->g[1].p;
+  a.st0 = ctx->st[0].p;
+  a.st1 = ctx->st[1].p;
   a.part = ctx->chunk_part.p;
   a.sc = ctx->dsc;
   a.err = ctx->derr;

@@ -119,6 +119,7 @@ struct sc_ctx {
   bool have_q = false;
   sc::DBuf<double> q;
   sc::DBuf<double> gam[2], g[2], w, gam_user, uc;  // w: U_ext (n x 6); uc: U_c for time stepping
+  sc::DBuf<double2> st[2];      // BBPGD state (gamma_l, g_l), ping-pong
   sc::DBuf<double> apgd_y, apgd_sums;  // APGD: extrapolated point, reduced sums
   sc::DBuf<int64_t> prev_key;   // warm start: (i*n + j) keys of the previous solve (sorted)
   sc::DBuf<double> prev_gam;    // ... and its gamma
@@ -250,15 +251,16 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
 // gather F = D v (mode raw) or F = D max(0, gam_old - alpha g_old) with the owner
 // writing gam_new (mode proj).  Output: f4 (spheres) or u4 after the drag (rods, fused)
 // or a user FT (n x 6).
-int launch_gather_proj(sc_ctx* ctx, const double* gam_old, const double* g_old, double* gam_new,
-                       double mu);
-int launch_gather_raw(sc_ctx* ctx, const double* v, double mu, double* FT_user /*nullable*/);
-int launch_proj_own(sc_ctx* ctx, const double* gam_old, const double* g_old, double* gam_new,
-                    int64_t l0, int64_t l1);
+// The BBPGD state is packed per constraint: st[k][l] = (gamma_l, g_l), ping-pong k = 0, 1.
+int launch_gather_proj(sc_ctx* ctx, int pp, double mu);  // st[pp] -> st[pp ^ 1].x, F
+int launch_gather_raw(sc_ctx* ctx, const double* v, int vstride, double mu, double* FT_user /*nullable*/);
+int launch_proj_own(sc_ctx* ctx, int pp, int64_t l0, int64_t l1);
+int launch_pack_gamma0(sc_ctx* ctx, const double* gam0);  // st[0] = (max(0, gamma_0), 0)
+int launch_unpack_state(sc_ctx* ctx, int pp, double* gam, double* g);
 // D^T: mode 0 iteration (g_new = D^T U + q, partials ss,sy,yy,mm), mode 1 alpha0
-// (w = D^T U, partials g.g, g.w), mode 2 (g = D^T U + q, partial mm) ; chunks [c0,c1)
-int launch_dt(sc_ctx* ctx, int mode, const double* gam_new, const double* gam_old,
-              const double* g_old, double* g_out, int64_t c0, int64_t c1, bool fuse);
+// (partials g.g, g.M g), mode 2 warm g_0 = D^T U + q, mode 5 g_0 = q (both: partial mm) -- on the
+// packed state st[pp]; APGD: mode 3 (g_out = q), mode 4 (g_out = M x + q; x.Mx, q.x, mm); chunks [c0,c1)
+int launch_dt(sc_ctx* ctx, int mode, int pp, const double* x, double* g_out, int64_t c0, int64_t c1, bool fuse);
 int launch_dt_user(sc_ctx* ctx, const double* UW, double* out, const double* addq, double qscale);
 // q = gap/dt + D^T U_nc - n_k . V_k on the constraints with moving walls
 int launch_lcp_q(sc_ctx* ctx, const double* U_nc, double inv_dt, double* q);
