@@ -27,7 +27,8 @@
  *    scalars (n_c, stats) synchronise that stream.
  *  - Multi-GPU contexts (sc_create_dist) are collective: every rank makes
  *    the same sequence of calls with the same full inputs; results are
- *    bitwise identical to a 1-GPU context.
+ *    bitwise identical to a 1-GPU context (both RPY
+ *    kernels).  The fast summation (mobility model 2) is 1-GPU only.
  */
 #ifndef STOKESCOL_H
 #define STOKESCOL_H
@@ -314,13 +315,16 @@ int sc_sym_pair_table(int64_t nsb, int world, int rank, int32_t* pairs, int64_t*
 int sc_set_emulated_world(sc_ctx* ctx, int world);
 
 /* Choice of the RPY apply kernel: 0 = automatic (the
- * symmetric pair-tile kernel on a 1-GPU context with N >= 4096, else the
- * target-row kernel), 1 = target-row kernel (the multi-GPU sharding unit;
- * bitwise identical for any number of ranks), 2 = symmetric pair-tile kernel
- * (each unordered pair evaluated once).  Both compute the same sum; they differ
- * in rounding only.  Mode 0 on one GPU also runs the BBPGD loop of small sphere problems
- * (padded N <= 2048) as one persistent cooperative kernel; modes 1 and 2 keep
- * the kernel-per-step path.  Errors: SC_EINVAL for another mode. */
+ * symmetric pair-tile kernel for N >= 4096 -- on one GPU and on a multi-GPU
+ * context, where every rank evaluates its share of the super-block pairs and the
+ * exact fixed-point row sums are all-reduced as int64 -- else the target-row
+ * kernel), 1 = target-row kernel (rows sharded over the ranks), 2 = symmetric
+ * pair-tile kernel (each unordered pair evaluated once).  Both kernels give
+ * results that are bitwise independent of the number of ranks; they differ from
+ * each other in rounding only.  Mode 0 on one GPU also runs the BBPGD loop of small
+ * sphere problems (padded N <= 2048) as one persistent cooperative kernel
+ * (DESIGN.md); modes 1 and 2 keep the kernel-per-step path.  Errors: SC_EINVAL for
+ * another mode. */
 int sc_set_rpy_kernel(sc_ctx* ctx, int mode);
 
 #ifdef __cplusplus

@@ -528,7 +528,7 @@ int fmm_setup(sc_ctx* ctx) {
     }
   double ext = std::max(hi[0] - lo[0], std::max(hi[1] - lo[1], hi[2] - lo[2]));
   const double a = ctx->a_const;
-  ext = std::max(ext, 4.0 * a) * (1.0 + 1e-9) + 1e-9;
+  ext = std::max(ext, 8.0 * a) * (1.0 + 1e-9) + 1e-9;  // (>= 4 leaves of side >= 2a per dimension)
   // leaf level: largest useful L with leaf side >= 2a (far branch between well-separated boxes,
   // every overlapping pair in neighbouring leaves), chosen to balance the P2P and M2L work
   int L = ctx->fmm_leaf_level;

@@ -127,3 +127,21 @@ def test_fmm_rejects_polydisperse_and_bad_params(ctx):
     ctx.set_mobility_model("rpy")
     with pytest.raises(ScError):
         ctx.set_fmm_params(5, 0)
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 40])
+def test_fmm_tiny_problems_exact_near_field(ctx, n):
+    """Few bodies in a small cluster: the root cube is at least 4 leaves of side 2a per dimension,
+    every pair that can overlap is in the near field; the result matches the oracle."""
+    rng = np.random.default_rng(n)
+    pos = rng.uniform(0, 2.0 * max(1.0, n ** (1 / 3)), size=(n, 3))
+    if n == 2:
+        pos = np.array([[0.0, 0.0, 0.0], [1.2, 0.3, 0.0]])  # overlapping
+    FT = rng.normal(size=(n, 6))
+    ctx.build_contacts_spheres(_cuda(pos), None, 0.0, 0.1)
+    ctx.set_mobility_model("rpy_fmm")
+    ctx.set_fmm_params(6, 0)
+    U = ctx.mobility_apply(_cuda(FT)).cpu().numpy()
+    ctx.set_mobility_model("rpy")
+    Uo = oracle.rpy_apply(pos, np.ones(n), 1.0, FT)
+    assert _relL2(U, Uo) <= TOL[6]

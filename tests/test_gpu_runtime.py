@@ -185,3 +185,16 @@ def test_checked_build_flag_matches_the_loaded_library(ctx):
     import os
     want = 1 if "checked" in os.environ.get("SC_LIB", "") else 0
     assert ctx.lib.sc_build_flags() & 1 == want
+
+
+def test_residual_trace_truncated_and_off(ctx):
+    p = make_problem("C2", n=3000, fixed_iters=0)
+    ctx.set_residual_trace(10)
+    _setup(ctx, p)
+    r = ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=p.max_iter)
+    tr = ctx.residual_trace()
+    assert r["iters"] > 10 and tr.size == 10 and np.all(tr > 0)
+    ctx.set_residual_trace(0)
+    _setup(ctx, p)
+    ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=p.max_iter)
+    assert ctx.residual_trace().size == 0

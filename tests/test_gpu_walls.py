@@ -286,3 +286,15 @@ def test_moving_floor_closed_form_and_time_step(ctx):
         else:
             assert z1 == 1.05
     ctx.set_walls(None)
+
+
+def test_wall_velocity_errors(ctx):
+    ctx.set_walls([[0.0, 0.0, 1.0, 0.0], [0.0, 0.0, -1.0, -10.0]])
+    with pytest.raises(ScError):
+        ctx.set_wall_velocities([[0.0, 0.0, 1.0]])  # one velocity per wall
+    with pytest.raises(ScError):
+        ctx.set_wall_velocities([[0.0, 0.0, np.nan], [0.0, 0.0, 0.0]])
+    ctx.set_wall_velocities([[0.0, 0.0, 1.0], [0.0, 0.0, 0.0]])
+    ctx.set_walls([[0.0, 0.0, 1.0, 0.0]])  # new walls: velocities reset to 0
+    np.testing.assert_array_equal(ctx.get_walls(), [[0.0, 0.0, 1.0, 0.0]])
+    ctx.set_walls(None)
