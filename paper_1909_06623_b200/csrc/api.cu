@@ -1,11 +1,11 @@
 // api.cu -- the C ABI (include/stokescol.h): context, staging, NCCL, and the
 // BBPGD control loop (Alg. 1) around the device kernels.
 //
-// The loop runs on the host but never waits per iteration on small problems:
-// iterations are enqueued in batches and every kernel of an iteration starts by
-// reading the device flag `done` (set by K-FINALIZE on convergence, j_max or a
-// non-finite value) and returns at once if it is set.  The host reads the
-// solver scalars (one pinned copy) only between batches.
+// The loop runs on the device: one CUDA graph whose conditional WHILE node repeats the
+// two-iteration kernel sequence until K-FINALIZE sets the device flag `done` (convergence, j_max
+// or a non-finite value); every kernel of an iteration starts by reading `done` and returns at
+// once if it is set.  The host reads the solver scalars (one pinned copy) after the loop.
+// (Multi-GPU and timed runs: iterations enqueued from the host in batches, scalars read between.)
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -530,6 +530,7 @@ static int create_common(sc_ctx** out, int device, void* stream) {
     return SC_ECUDA;
   }
   if (const char* v = std::getenv("SC_SYM_VARIANT")) ctx->sym_variant = std::atoi(v);
+  if (const char* v = std::getenv("SC_BATCH")) ctx->batch_override = std::atoi(v);
   if (const char* v = std::getenv("SC_NO_GRAPHS")) ctx->use_graphs = std::atoi(v) == 0;
   if (const char* v = std::getenv("SC_NO_PERSIST")) ctx->use_persist = std::atoi(v) == 0;
   *ctx->herr = 0;
@@ -1056,7 +1057,8 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
                                   : 2e-5 + 1.2e-10 * static_cast<double>(nc + n);
     // (multi-GPU: the done flag is identical on every rank -- K-FINALIZE runs on every rank on the
     // all-reduced partials -- so every rank enqueues the same batches and the collectives match)
-    const int batch = std::max(1, std::min(32, static_cast<int>(1e-3 / t_iter)));
+    int batch = std::max(1, std::min(32, static_cast<int>(1e-3 / t_iter)));
+    if (ctx->batch_override > 0) batch = ctx->batch_override;  // tuning (env SC_BATCH)
     auto enqueue_iter = [&](int pp) -> int {
       if (dist) {  // Steps 8-9 on own constraints, then every rank needs the full gamma_j
         if (int rc = D.proj_own(pp)) return rc;
@@ -1071,56 +1073,73 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
       if (int rc = D.dt(0, pp, &fused)) return rc;  // Steps 10-15
       return reduce(0);
     };
-    // Small problems (several iterations per host read, one GPU, no per-launch timing): the
-    // two-iteration kernel sequence (even + odd buffer parity) is captured once into a CUDA
-    // graph and replayed, removing per-kernel launch gaps.
+    // One GPU, no per-launch timing: the loop runs on the device.  The two-iteration kernel
+    // sequence (even + odd buffer parity) is captured once as the body of a CUDA-graph
+    // conditional WHILE node; a last one-thread kernel sets the loop condition to !done (the
+    // flag K-FINALIZE sets on convergence, j_max or a non-finite value), so the whole Steps 7-16
+    // loop is one graph launch: no host round trip per batch of iterations and at most one
+    // no-op iteration after the last.  Multi-GPU (NCCL) or timed runs: iterations enqueued from
+    // the host in batches, the host reading the scalars between batches.
     cudaGraphExec_t gexec = nullptr;
-    int64_t graph_kernels = 0;
     const bool persist = !dist && persist_eligible(ctx) && opts->max_iter > 0;
     if (persist) {  // small problem: the whole loop in one cooperative launch (persist.cu)
       if (int rc = bbpgd_persistent(ctx, mu)) return rc;
       if (int rc = read_scalars(ctx)) return rc;
     }
-    if (!persist && batch >= 4 && !dist && !ctx->timer.enabled && ctx->use_graphs) {
+    if (!persist && !dist && !ctx->timer.enabled && ctx->use_graphs && opts->max_iter > 0) {
       cudaGraph_t graph = nullptr;
+      SC_CUDA(cudaGraphCreate(&graph, 0));
+      cudaGraphConditionalHandle cond;
+      cudaError_t ce = cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault);
+      cudaGraphNodeParams np = {};
+      np.type = cudaGraphNodeTypeConditional;
+      np.conditional.handle = cond;
+      np.conditional.type = cudaGraphCondTypeWhile;
+      np.conditional.size = 1;
+      cudaGraphNode_t node;
+      if (ce == cudaSuccess) ce = cudaGraphAddNode(&node, graph, nullptr, 0, &np);
+      if (ce != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        return cuda_fail(ctx, ce, "conditional graph node");
+      }
+      cudaGraph_t body = np.conditional.phGraph_out[0];
       const int64_t l0 = ctx->launch_count;
-      SC_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-      int rc0 = enqueue_iter(0);
+      ce = cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+      int rc0 = ce == cudaSuccess ? 0 : cuda_fail(ctx, ce, "cudaStreamBeginCaptureToGraph");
+      if (rc0 == 0) rc0 = enqueue_iter(0);
       if (rc0 == 0) rc0 = enqueue_iter(1);
-      cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
-      if (rc0 != 0) {
-        if (graph) cudaGraphDestroy(graph);
-        return rc0;
+      if (rc0 == 0) rc0 = launch_loop_continue(ctx, cond);
+      if (ce == cudaSuccess) {
+        cudaGraph_t captured = nullptr;
+        cudaError_t ce2 = cudaStreamEndCapture(ctx->stream, &captured);
+        if (rc0 == 0 && ce2 != cudaSuccess) rc0 = cuda_fail(ctx, ce2, "cudaStreamEndCapture");
       }
-      if (ce != cudaSuccess) return cuda_fail(ctx, ce, "cudaStreamEndCapture");
-      ce = cudaGraphInstantiate(&gexec, graph, 0);
+      if (rc0 == 0) {
+        ce = cudaGraphInstantiate(&gexec, graph, 0);
+        if (ce != cudaSuccess) rc0 = cuda_fail(ctx, ce, "cudaGraphInstantiate(conditional loop)");
+      }
       cudaGraphDestroy(graph);
-      if (ce != cudaSuccess) return cuda_fail(ctx, ce, "cudaGraphInstantiate");
-      graph_kernels = ctx->launch_count - l0;
+      const int64_t body_kernels = ctx->launch_count - l0;
       ctx->launch_count = l0;
-    }
-    int enq = persist ? opts->max_iter : 0;
-    while (enq < opts->max_iter) {
-      int nb = std::min(batch, opts->max_iter - enq);
-      if (gexec) {
-        nb = (nb + 1) & ~1;  // whole graph replays; iterations past j_max are no-ops (done flag)
-        for (int k = 0; k < nb; k += 2) {
-          cudaError_t ce = cudaGraphLaunch(gexec, ctx->stream);
-          if (ce != cudaSuccess) {
-            cudaGraphExecDestroy(gexec);
-            return cuda_fail(ctx, ce, "cudaGraphLaunch");
-          }
-          ctx->launch_count += graph_kernels;
-        }
-      } else {
-        for (int k = 0; k < nb; ++k)
-          if (int rc = enqueue_iter((enq + k) & 1)) return rc;
+      if (rc0 != 0) return rc0;
+      ce = cudaGraphLaunch(gexec, ctx->stream);
+      if (ce != cudaSuccess) {
+        cudaGraphExecDestroy(gexec);
+        return cuda_fail(ctx, ce, "cudaGraphLaunch(conditional loop)");
       }
-      enq += nb;
       if (int rc = read_scalars(ctx)) {
-        if (gexec) cudaGraphExecDestroy(gexec);
+        cudaGraphExecDestroy(gexec);
         return rc;
       }
+      ctx->launch_count += body_kernels * std::max(1, (ctx->hsc->iter + 1) / 2);  // bodies run
+    }
+    int enq = (persist || gexec) ? opts->max_iter : 0;
+    while (enq < opts->max_iter) {
+      const int nb = std::min(batch, opts->max_iter - enq);
+      for (int k = 0; k < nb; ++k)
+        if (int rc = enqueue_iter((enq + k) & 1)) return rc;
+      enq += nb;
+      if (int rc = read_scalars(ctx)) return rc;
       if (ctx->hsc->done) break;
     }
     if (gexec) cudaGraphExecDestroy(gexec);

@@ -317,6 +317,12 @@ __global__ void dt_user_kernel(const int32_t* __restrict__ ci, const int32_t* __
   out[l] = addgap ? nv.w * inv_dt + v : v;  // q = Phi/dt + D^T U_nc
 }
 
+// The loop condition of the device-side BBPGD loop (a CUDA-graph conditional WHILE node): run the
+// body again unless K-FINALIZE has set `done`.
+__global__ void loop_continue_kernel(cudaGraphConditionalHandle cond, const int32_t* __restrict__ done) {
+  cudaGraphSetConditional(cond, *done ? 0u : 1u);
+}
+
 __global__ void count_active_kernel(const double* __restrict__ gam, int64_t nc, int32_t* __restrict__ out) {
   __shared__ int32_t s;
   if (threadIdx.x == 0) s = 0;
@@ -535,6 +541,11 @@ int launch_minmap(sc_ctx* ctx, const double* gam, const double* g, int64_t nc, d
   minmap_kernel<<<1, 1024, 0, ctx->stream>>>(gam, g, nc, out);
   timer_end(ctx, SC_K_MISC);
   return check_launch(ctx, "minmap");
+}
+
+int launch_loop_continue(sc_ctx* ctx, cudaGraphConditionalHandle cond) {
+  loop_continue_kernel<<<1, 1, 0, ctx->stream>>>(cond, &ctx->dsc->done);
+  return check_launch(ctx, "loop_continue");
 }
 
 int launch_count_active(sc_ctx* ctx, const double* gam, int32_t* out) {

@@ -149,6 +149,7 @@ struct sc_ctx {
   int nsplit = 1;
   int rpy_mode = 0;             // 0 auto, 1 target-row kernel, 2 symmetric pair-tile kernel
   bool use_persist = true;      // persistent BBPGD loop for small sphere problems (env SC_NO_PERSIST=1: off)
+  int batch_override = 0;       // tuning: iterations enqueued between host reads (env SC_BATCH)
   bool use_graphs = true;       // CUDA-graph replay of small-problem iteration batches (env SC_NO_GRAPHS=1: off)
   int sym_variant = 0;          // tuning: (warps, targets/lane) of the symmetric kernel (env SC_SYM_VARIANT)
   int64_t sym_nsb = -1;         // super-blocks the pair tables were built for
@@ -271,6 +272,7 @@ int launch_unpack_uw_spheres(sc_ctx* ctx, const double4* u4, const double4* t4, 
 int launch_rod_drag_user(sc_ctx* ctx, const double* FT, double mu, double* UW);
 int launch_rod_unpack(sc_ctx* ctx, const double4* u4, double* UW);
 int launch_count_active(sc_ctx* ctx, const double* gam, int32_t* out);
+int launch_loop_continue(sc_ctx* ctx, cudaGraphConditionalHandle cond);  // device loop condition = !done
 int launch_minmap(sc_ctx* ctx, const double* gam, const double* g, int64_t nc, double* out);
 int launch_q(sc_ctx* ctx, double dt, const double* dtu, double* q);
 struct WallRates {
