@@ -63,7 +63,9 @@ int sc_build_flags(void);
 int sc_create(sc_ctx** out, int device, void* stream);
 /* Multi-GPU (one process per GPU, NCCL over NVLink): nccl_id is the 128-byte
  * ncclUniqueId that rank 0 obtained from sc_nccl_unique_id and broadcast to
- * every rank (e.g. via torch.distributed). */
+ * every rank (e.g. via torch.distributed).  world = 1 builds a one-rank
+ * communicator: the context runs the multi-GPU code path (partition, NCCL
+ * broadcast / all-reduce) with results bitwise equal to sc_create's. */
 int sc_nccl_unique_id(void* out128);
 int sc_create_dist(sc_ctx** out, int device, void* stream, const void* nccl_id, int rank, int world);
 void sc_destroy(sc_ctx* ctx);

@@ -78,7 +78,7 @@ class Context:
         s = None
         if stream is not None:
             s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
-        if world > 1:
+        if world > 1 or nccl_id is not None:  # (world 1 with an id: a one-rank communicator)
             idbuf = C.create_string_buffer(bytes(nccl_id), 128)
             rc = self.lib.sc_create_dist(C.byref(self._h), device, s, idbuf, rank, world)
         else:

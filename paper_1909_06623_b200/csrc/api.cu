@@ -219,9 +219,10 @@ struct Dist {
 
   explicit Dist(sc_ctx* c) : ctx(c) {
     const int ew = c->emul_world;
-    emul = c->world == 1 && ew > 1;
+    emul = c->world == 1 && ew > 1 && c->comm == nullptr;
     W = emul ? ew : c->world;
-    on = W > 1 && c->kind == kSpheres;
+    // a context with a communicator runs the NCCL path even with one rank (sc_create_dist, world 1)
+    on = (W > 1 || (c->comm != nullptr && !emul)) && c->kind == kSpheres;
     if (!on) W = 1;
     for (int r = 0; r < W; ++r) parts.push_back(partition(c, W, r));
     if (emul || !on)
@@ -254,7 +255,7 @@ struct Dist {
   // Target-row kernel: own rows, then all-gather of the rows.
   int rpy(double mu, const int32_t* done) {
     if (ctx->mobility_model == 2) {  // NEXT row f4(i): the fast summation (one GPU)
-      if (on && !emul) return fail(ctx, SC_EINVAL, "the fast RPY summation runs on a 1-GPU context");
+      if (on && !emul && W > 1) return fail(ctx, SC_EINVAL, "the fast RPY summation runs on a 1-GPU context");
       return fmm_apply(ctx, ctx->f4.p, mu, ctx->u4.p, done);
     }
     if (rpy_use_sym(ctx)) {
@@ -556,7 +557,7 @@ int sc_create_dist(sc_ctx** out, int device, void* stream, const void* nccl_id, 
   sc_ctx* ctx = *out;
   ctx->rank = rank;
   ctx->world = world;
-  if (world > 1) {
+  {  // (world 1 too: a one-rank communicator runs the same NCCL code path as world > 1)
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&ctx->comm, world, id, rank);
@@ -1516,7 +1517,8 @@ int sc_set_rpy_kernel(sc_ctx* ctx, int mode) {
 
 int sc_set_emulated_world(sc_ctx* ctx, int world) {
   if (ctx == nullptr) return SC_EINVAL;
-  if (world < 1 || ctx->world > 1) return fail(ctx, SC_EINVAL, "emulated world needs a 1-GPU context and world >= 1");
+  if (world < 1 || ctx->world > 1 || ctx->comm != nullptr)
+    return fail(ctx, SC_EINVAL, "emulated world needs a 1-GPU context without a communicator and world >= 1");
   ctx->emul_world = world;
   return SC_OK;
 }

@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kPT) bbpgd_persistent_kernel(PersistArgs a) {
 
 bool persist_eligible(const sc_ctx* ctx) {
   // (a forced RPY kernel choice, sc_set_rpy_kernel, keeps the launch-per-kernel path)
-  return ctx->use_persist && ctx->rpy_mode == 0 && ctx->kind == kSpheres && ctx->world == 1 &&
+  return ctx->use_persist && ctx->rpy_mode == 0 && ctx->kind == kSpheres && ctx->world == 1 && ctx->comm == nullptr &&
          ctx->mobility_model != 2 &&
          ctx->emul_world == 1 && ctx->npad <= kPersistMaxBodies && ctx->nc > 0 && ctx->persist_grid > 0;
 }

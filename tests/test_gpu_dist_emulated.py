@@ -91,3 +91,37 @@ def test_emulated_ranks_symmetric_kernel_bitwise(ctx, name, n, max_iter, fixed):
         assert r["iters"] == ref["iters"] and r["residual"] == ref["residual"], world
         for k in ("gamma", "g", "Fc", "Uc", "U_ext"):
             assert torch.equal(r[k], ref[k]), (world, k)
+
+
+@pytest.mark.parametrize("name,n,max_iter,fixed,kernel", [("C5", 9000, 25, True, 0), ("C2", 5000, 5000, False, 0),
+                                                           ("C3", 2500, 5000, False, 1), ("C1", None, 2000, False, 1)])
+def test_one_rank_nccl_path_bitwise_equals_plain_context(ctx, name, n, max_iter, fixed, kernel):
+    """sc_create_dist with world = 1 builds a one-rank NCCL communicator and runs the multi-GPU code
+    path for real on this GPU -- the partition, grouped ncclBroadcast of the owned (gamma, g)
+    slices, ncclAllReduce of the chunk partials (double) and of the RPY fixed-point limbs (int64),
+    the host-batched loop -- and must equal the plain 1-GPU context bitwise."""
+    from paper_1909_06623_b200 import nccl_unique_id
+    p = make_problem(name, n=n)
+
+    def solve(c):
+        c.set_rpy_kernel(kernel)
+        c.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+        c.assemble_D()
+        U = c.mobility_apply(_cuda(p.force), mu=p.mu)
+        c.lcp_q(p.dt, U)
+        r = c.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=max_iter, fixed_iters=fixed)
+        r["U_ext"] = U
+        return r
+
+    ref = solve(ctx)
+    ctx.set_rpy_kernel(0)
+    d = Context(0, nccl_id=nccl_unique_id(), rank=0, world=1)
+    try:
+        info = d.comm_info()
+        assert info["nranks"] == 1 and info["nccl_version"] > 0
+        r = solve(d)
+    finally:
+        d.close()
+    assert r["iters"] == ref["iters"] and r["residual"] == ref["residual"]
+    for k in ("gamma", "g", "Fc", "Uc", "U_ext"):
+        assert torch.equal(r[k], ref[k]), k
