@@ -13,8 +13,9 @@ from paper_1909_06623_b200 import Context  # noqa: E402
 from paper_1909_06623_b200.synthetic import make_problem  # noqa: E402
 
 PEAK = 148 * 64 * 2 * 1.965e9
-cases = [("C5", n) for n in (2048, 4096, 8192, 16384, 32768, 65536, 131072, 262144, 524288, 1048576)] + \
-    [("C2", 8192), ("C2", 65536)]
+cases = [("C5", int(x)) for x in os.environ.get("RPY_NS", "").split(",") if x] or (
+    [("C5", n) for n in (2048, 4096, 8192, 16384, 32768, 65536, 131072, 262144, 524288, 1048576)] +
+    [("C2", 8192), ("C2", 65536)])
 for name, n in cases:
     p = make_problem(name, n=n)
     ctx = Context(0)
