@@ -526,7 +526,7 @@ static int create_common(sc_ctx** out, int device, void* stream) {
   size_t free_b = 0;
   if (cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
       cudaMemGetInfo(&free_b, &ctx->total_mem) != cudaSuccess || rpy_init_device(ctx) != 0 ||
-      persist_init_device(ctx) != 0) {
+      persist_init_device(ctx) != 0 || fmm_init_device(ctx) != 0) {
     sc_destroy(ctx);
     return SC_ECUDA;
   }
@@ -991,6 +991,9 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
   const bool dist = D.on;
   const bool spheres = ctx->kind == kSpheres;
   const int32_t* done = &ctx->dsc->done;
+  if (spheres && ctx->mobility_model == 2 && !ctx->fmm_ready) {  // (the tree, before any graph capture)
+    if (int rc = fmm_setup(ctx)) return rc;
+  }
 
   DevScalars h;
   std::memset(&h, 0, sizeof(h));

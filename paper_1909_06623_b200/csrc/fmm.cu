@@ -31,10 +31,16 @@
 namespace sc {
 namespace {
 
-constexpr int kNmax = 10;
-__constant__ double c_xbar[kNmax];             // Chebyshev nodes
-__constant__ double c_T[kNmax * kNmax];        // T_q(xbar_k) at [k * n + q]
-__constant__ double c_P[2 * kNmax * kNmax];    // [sigma][m'][m] = S(xbar_m', (xbar_m + s)/2), s = -1, +1
+// Interpolation tables of the three orders, written once per device at context creation (they
+// depend on the order only, so every context writes the same bytes): for order n at offset
+// tab_off(n): the Chebyshev nodes xbar[n], T_q(xbar_k) at [k * n + q], and the child-parent
+// transfer matrices P[sigma][m'][m] = S(xbar_m', (xbar_m + s)/2), s = -1 (sigma 0), +1 (sigma 1).
+constexpr int tab_size(int n) { return n + 3 * n * n; }
+constexpr int tab_off(int n) { return n == 4 ? 0 : (n == 6 ? tab_size(4) : tab_size(4) + tab_size(6)); }
+__constant__ double c_tab[tab_size(4) + tab_size(6) + tab_size(8)];
+#define c_xbar (c_tab + tab_off(NN))
+#define c_T (c_tab + tab_off(NN) + NN)
+#define c_P (c_tab + tab_off(NN) + NN + NN * NN)
 
 struct Geom {
   double ox, oy, oz;  // root cube corner
@@ -485,33 +491,41 @@ double cheb_S(int n, double xk, double u) {  // host: S_n(xbar_k, u)
 
 }  // namespace
 
+// The interpolation tables of orders 4, 6, 8 into this device's constant memory (sc_create).
+int fmm_init_device(sc_ctx* ctx) {
+  double tab[tab_size(4) + tab_size(6) + tab_size(8)];
+  const double pi = 3.14159265358979323846;
+  for (int nn : {4, 6, 8}) {
+    double* xb = tab + tab_off(nn);
+    double* T = xb + nn;
+    double* P = T + nn * nn;
+    for (int k = 0; k < nn; ++k) xb[k] = std::cos((2 * k + 1) * pi / (2 * nn));
+    for (int k = 0; k < nn; ++k) {
+      double t0 = 1.0, t1 = xb[k];
+      T[k * nn] = 1.0;
+      if (nn > 1) T[k * nn + 1] = xb[k];
+      for (int q = 2; q < nn; ++q) {
+        const double t2 = 2.0 * xb[k] * t1 - t0;
+        T[k * nn + q] = t2;
+        t0 = t1;
+        t1 = t2;
+      }
+    }
+    for (int sg = 0; sg < 2; ++sg)
+      for (int mp = 0; mp < nn; ++mp)
+        for (int m = 0; m < nn; ++m) P[sg * nn * nn + mp * nn + m] = cheb_S(nn, xb[mp], 0.5 * (xb[m] + (sg ? 1.0 : -1.0)));
+  }
+  cudaError_t e = cudaMemcpyToSymbol(c_tab, tab, sizeof(tab));
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "fmm tables");
+  return 0;
+}
+
 // Tree of the current bodies (after build_contacts): root cube, leaf level, bodies sorted by leaf.
 int fmm_setup(sc_ctx* ctx) {
   const int nn = ctx->fmm_order;
   if (nn != 4 && nn != 6 && nn != 8) return fail(ctx, SC_EINVAL, "fmm order must be 4, 6 or 8");
   if (ctx->kind != kSpheres || ctx->poly) return fail(ctx, SC_EINVAL, "the fast RPY summation needs monodisperse spheres");
   const int64_t n = ctx->n;
-  // node tables
-  double xb[kNmax], T[kNmax * kNmax], P[2 * kNmax * kNmax];
-  const double pi = 3.14159265358979323846;
-  for (int k = 0; k < nn; ++k) xb[k] = std::cos((2 * k + 1) * pi / (2 * nn));
-  for (int k = 0; k < nn; ++k) {
-    double t0 = 1.0, t1 = xb[k];
-    T[k * nn] = 1.0;
-    if (nn > 1) T[k * nn + 1] = xb[k];
-    for (int q = 2; q < nn; ++q) {
-      const double t2 = 2.0 * xb[k] * t1 - t0;
-      T[k * nn + q] = t2;
-      t0 = t1;
-      t1 = t2;
-    }
-  }
-  for (int sg = 0; sg < 2; ++sg)
-    for (int mp = 0; mp < nn; ++mp)
-      for (int m = 0; m < nn; ++m) P[sg * nn * nn + mp * nn + m] = cheb_S(nn, xb[mp], 0.5 * (xb[m] + (sg ? 1.0 : -1.0)));
-  SC_CUDA(cudaMemcpyToSymbolAsync(c_xbar, xb, sizeof(double) * nn, 0, cudaMemcpyHostToDevice, ctx->stream));
-  SC_CUDA(cudaMemcpyToSymbolAsync(c_T, T, sizeof(double) * nn * nn, 0, cudaMemcpyHostToDevice, ctx->stream));
-  SC_CUDA(cudaMemcpyToSymbolAsync(c_P, P, sizeof(double) * 2 * nn * nn, 0, cudaMemcpyHostToDevice, ctx->stream));
   // bounding cube
   const int nbb = 64;
   if (int rc = ensure(ctx, ctx->bbox_part, 6 * nbb)) return rc;

@@ -237,6 +237,7 @@ int rpy_apply_rows(sc_ctx* ctx, const double4* f4, int64_t row0, int64_t nrows, 
                    double4* u4, const int32_t* done);
 int choose_nsplit(int64_t npad, int world);
 // NEXT row f4(i): u4 = RPY(f4) by the Chebyshev-interpolation FMM (builds the tree on first use)
+int fmm_init_device(sc_ctx* ctx);  // interpolation tables into constant memory (sc_create)
 int fmm_setup(sc_ctx* ctx);
 int fmm_apply(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done);
 // per-device kernel attributes (max dynamic shared memory); called by sc_create

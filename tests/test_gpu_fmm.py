@@ -145,3 +145,31 @@ def test_fmm_tiny_problems_exact_near_field(ctx, n):
     ctx.set_mobility_model("rpy")
     Uo = oracle.rpy_apply(pos, np.ones(n), 1.0, FT)
     assert _relL2(U, Uo) <= TOL[6]
+
+
+def test_fmm_two_contexts_different_orders():
+    """Two contexts with different orders interleaved in one process: the interpolation tables of
+    every order live in constant memory side by side, so neither context disturbs the other."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    p = make_problem("C5", n=15000)
+    FT = np.random.default_rng(9).normal(size=(p.n, 6))
+    ref = {}
+    for order in (4, 8):
+        c = Context(0)
+        c.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+        c.set_mobility_model("rpy_fmm")
+        c.set_fmm_params(order, 0)
+        ref[order] = c.mobility_apply(_cuda(FT)).clone()
+        c.close()
+    a, b = Context(0), Context(0)
+    for c, order in ((a, 4), (b, 8)):
+        c.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+        c.set_mobility_model("rpy_fmm")
+        c.set_fmm_params(order, 0)
+    for _ in range(2):
+        ua = a.mobility_apply(_cuda(FT))
+        ub = b.mobility_apply(_cuda(FT))
+        assert torch.equal(ua, ref[4]) and torch.equal(ub, ref[8])
+    a.close()
+    b.close()
