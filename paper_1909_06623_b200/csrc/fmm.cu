@@ -17,7 +17,8 @@
 //   L2P+P2P  U_i = sum_m S(m, u_i) L_B(m) + sum_{j in the 27 leaves around B} T_ij F_j
 // S(m, u) = prod_d (1/n + (2/n) sum_{q=1}^{n-1} T_q(xbar_{m_d}) T_q(u_d)) with the Chebyshev nodes
 // xbar_k = cos((2k+1) pi / (2n)); IL(T) = the children of the parent's neighbours that are not
-// adjacent to T (at most 189).  Every sum is in a fixed order (deterministic); monodisperse radii.
+// adjacent to T (at most 189).  Every sum is in a fixed order (deterministic).  Polydisperse radii:
+// the far branch is split into radius-free kernels (m2l_poly_kernel), 9 node components instead of 3.
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -45,7 +46,7 @@ __constant__ double c_tab[tab_size(4) + tab_size(6) + tab_size(8)];
 struct Geom {
   double ox, oy, oz;  // root cube corner
   double H;           // root cube side
-  double a;           // sphere radius (monodisperse)
+  double a;           // sphere radius (monodisperse kernels; the polydisperse ones read w = a_i/2)
   int L;              // leaf level
 };
 
@@ -117,8 +118,10 @@ __global__ void gather_sorted_kernel(const int32_t* __restrict__ sidx, int64_t n
   dst[k] = src[sidx[k]];
 }
 
-// P2M: one CTA per leaf, thread m = node (blockDim >= n^3)
-template <int NN>
+// P2M: one CTA per leaf, thread m = node (blockDim >= n^3).  C = 3 (monodisperse: the node
+// strengths of F) or 9 (polydisperse: of the three source densities F, w F, w^2 F, w = a/2; see
+// m2l_poly_kernel).
+template <int NN, int C>
 __global__ void p2m_kernel(const double4* __restrict__ spos, const double4* __restrict__ sf,
                            const int32_t* __restrict__ lstart, Geom g, double* __restrict__ M,
                            const int32_t* __restrict__ done) {
@@ -126,14 +129,16 @@ __global__ void p2m_kernel(const double4* __restrict__ spos, const double4* __re
   constexpr int NB = NN * NN * NN;
   constexpr int CH = 64;
   __shared__ double sw[CH][3][NN];
-  __shared__ double sfrc[CH][3];
+  __shared__ double sfrc[CH][C];
   const int64_t b = blockIdx.x;
   double cx, cy, cz, w;
   box_center(g, g.L, b, cx, cy, cz, w);
   const int32_t j0 = lstart[b], j1 = lstart[b + 1];
   const int m = threadIdx.x;
   const int mx = m % NN, my = (m / NN) % NN, mz = m / (NN * NN);
-  double ax = 0, ay = 0, az = 0;
+  double acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.0;
   for (int32_t c0 = j0; c0 < j1; c0 += CH) {
     const int cn = min(CH, j1 - c0);
     __syncthreads();
@@ -152,46 +157,55 @@ __global__ void p2m_kernel(const double4* __restrict__ spos, const double4* __re
         sfrc[jj][0] = f.x;
         sfrc[jj][1] = f.y;
         sfrc[jj][2] = f.z;
+        if constexpr (C == 9) {
+          const double hw = p.w, hw2 = p.w * p.w;
+          sfrc[jj][3] = hw * f.x;
+          sfrc[jj][4] = hw * f.y;
+          sfrc[jj][5] = hw * f.z;
+          sfrc[jj][6] = hw2 * f.x;
+          sfrc[jj][7] = hw2 * f.y;
+          sfrc[jj][8] = hw2 * f.z;
+        }
       }
     }
     __syncthreads();
     if (m < NB) {
       for (int jj = 0; jj < cn; ++jj) {
         const double s = sw[jj][0][mx] * sw[jj][1][my] * sw[jj][2][mz];
-        ax = fma(s, sfrc[jj][0], ax);
-        ay = fma(s, sfrc[jj][1], ay);
-        az = fma(s, sfrc[jj][2], az);
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[c] = fma(s, sfrc[jj][c], acc[c]);
       }
     }
   }
   if (m < NB) {
-    double* o = M + (b * NB + m) * 3;
-    o[0] = ax;
-    o[1] = ay;
-    o[2] = az;
+    double* o = M + (b * NB + m) * C;
+#pragma unroll
+    for (int c = 0; c < C; ++c) o[c] = acc[c];
   }
 }
 
 // M2M (child level l+1 -> parent level l) and L2L (parent l -> children l+1): the 1-D transfer
-// matrices c_P of the child's position sigma in its parent.
-template <int NN, bool UP>
+// matrices c_P of the child's position sigma in its parent; C components per node.
+template <int NN, bool UP, int C>
 __global__ void transfer_kernel(int l, double* __restrict__ Xp, double* __restrict__ Xc,
                                 const int32_t* __restrict__ done) {
   if (done != nullptr && *done) return;
   constexpr int NB = NN * NN * NN;
-  __shared__ double s[NB * 3];
+  __shared__ double s[NB * C];
   const int m = threadIdx.x;
   const int mx = m % NN, my = (m / NN) % NN, mz = m / (NN * NN);
+  double acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.0;
   if (UP) {  // parent box blockIdx.x at level l: sum over its 8 children
     const int D = 1 << l;
     const int64_t p = blockIdx.x;
     const int px = static_cast<int>(p % D), py = static_cast<int>((p / D) % D), pz = static_cast<int>(p / D / D);
-    double ax = 0, ay = 0, az = 0;
     for (int c = 0; c < 8; ++c) {
       const int sx = c & 1, sy = (c >> 1) & 1, sz = c >> 2;
       const int64_t ci = ((2 * pz + sz) * (2 * D) + (2 * py + sy)) * (2 * D) + (2 * px + sx);
       __syncthreads();
-      for (int t = threadIdx.x; t < 3 * NB; t += blockDim.x) s[t] = Xc[ci * NB * 3 + t];
+      for (int t = threadIdx.x; t < C * NB; t += blockDim.x) s[t] = Xc[ci * NB * C + t];
       __syncthreads();
       if (m < NB) {
         const double* Px = c_P + sx * NN * NN + mx * NN;
@@ -203,46 +217,41 @@ __global__ void transfer_kernel(int l, double* __restrict__ Xp, double* __restri
 #pragma unroll
             for (int kx = 0; kx < NN; ++kx) {
               const double wgt = Px[kx] * pyz;
-              const double* v = s + ((kz * NN + ky) * NN + kx) * 3;
-              ax = fma(wgt, v[0], ax);
-              ay = fma(wgt, v[1], ay);
-              az = fma(wgt, v[2], az);
+              const double* v = s + ((kz * NN + ky) * NN + kx) * C;
+#pragma unroll
+              for (int q = 0; q < C; ++q) acc[q] = fma(wgt, v[q], acc[q]);
             }
           }
       }
     }
     if (m < NB) {
-      double* o = Xp + (p * NB + m) * 3;
-      o[0] = ax;
-      o[1] = ay;
-      o[2] = az;
+      double* o = Xp + (p * NB + m) * C;
+#pragma unroll
+      for (int q = 0; q < C; ++q) o[q] = acc[q];
     }
   } else {  // child box blockIdx.x at level l+1: add its parent's local expansion at its nodes
     const int D = 2 << l;
     const int64_t c = blockIdx.x;
     const int cx = static_cast<int>(c % D), cy = static_cast<int>((c / D) % D), cz = static_cast<int>(c / D / D);
     const int64_t pi = ((cz / 2) * (D / 2) + cy / 2) * (D / 2) + cx / 2;
-    for (int t = threadIdx.x; t < 3 * NB; t += blockDim.x) s[t] = Xp[pi * NB * 3 + t];
+    for (int t = threadIdx.x; t < C * NB; t += blockDim.x) s[t] = Xp[pi * NB * C + t];
     __syncthreads();
     if (m < NB) {
       const int sx = cx & 1, sy = cy & 1, sz = cz & 1;
-      double ax = 0, ay = 0, az = 0;
       for (int kz = 0; kz < NN; ++kz)
         for (int ky = 0; ky < NN; ++ky) {
           const double pyz = c_P[sy * NN * NN + ky * NN + my] * c_P[sz * NN * NN + kz * NN + mz];
 #pragma unroll
           for (int kx = 0; kx < NN; ++kx) {
             const double wgt = c_P[sx * NN * NN + kx * NN + mx] * pyz;
-            const double* v = s + ((kz * NN + ky) * NN + kx) * 3;
-            ax = fma(wgt, v[0], ax);
-            ay = fma(wgt, v[1], ay);
-            az = fma(wgt, v[2], az);
+            const double* v = s + ((kz * NN + ky) * NN + kx) * C;
+#pragma unroll
+            for (int q = 0; q < C; ++q) acc[q] = fma(wgt, v[q], acc[q]);
           }
         }
-      double* o = Xc + (c * NB + m) * 3;
-      o[0] += ax;
-      o[1] += ay;
-      o[2] += az;
+      double* o = Xc + (c * NB + m) * C;
+#pragma unroll
+      for (int q = 0; q < C; ++q) o[q] += acc[q];
     }
   }
 }
@@ -306,9 +315,93 @@ __global__ void m2l_kernel(Geom g, const int64_t* __restrict__ lev_off /* box of
   }
 }
 
+// Polydisperse M2L.  The far branch with the pair radius abar = w_i + w_j (w = a/2) splits as
+//   T(r; abar) = O(r) + abar^2 D(r),  O = (1/r) I + (1/r^3) d d^T,  D = (2/3)(1/r^3) I - 2 (1/r^5) d d^T
+// (8 pi mu hoisted), and abar^2 = w_i^2 + 2 w_i w_j + w_j^2, so with the source densities
+// s0 = F, s1 = w F, s2 = w^2 F (the 9 node components of p2m_kernel<NN, 9>) every target field is
+//   U_i = L_A + 2 w_i L_B + w_i^2 L_C,  L_A = sum O s0 + D s2,  L_B = sum D s1,  L_C = sum D s0,
+// three fields of smooth kernels that the interpolation carries like the monodisperse one
+// (l2p_p2p_kernel<NN, true> forms U_i).  Source node positions from the nested loop (no table).
+template <int NN>
+__global__ void m2l_poly_kernel(Geom g, const int64_t* __restrict__ lev_off, const double* __restrict__ M,
+                                double* __restrict__ Lc, const int32_t* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  constexpr int NB = NN * NN * NN;
+  __shared__ double sm[NB * 9];
+  int64_t gb = blockIdx.x;
+  int l = 2;
+  while (l < g.L && gb >= lev_off[l + 1] - lev_off[2]) ++l;
+  const int64_t t = gb - (lev_off[l] - lev_off[2]);
+  const int D = 1 << l;
+  const int tx = static_cast<int>(t % D), ty = static_cast<int>((t / D) % D), tz = static_cast<int>(t / D / D);
+  double cx, cy, cz, w;
+  box_center(g, l, t, cx, cy, cz, w);
+  const int m = threadIdx.x;
+  const int mx = m % NN, my = (m / NN) % NN, mz = m / (NN * NN);
+  const double x = cx + w * c_xbar[mx], y = cy + w * c_xbar[my], z = cz + w * c_xbar[mz];
+  double A[3] = {0, 0, 0}, B[3] = {0, 0, 0}, Cc[3] = {0, 0, 0};
+  const int px = tx >> 1, py = ty >> 1, pz = tz >> 1, Dp = D >> 1;
+  for (int oz = -1; oz <= 1; ++oz)
+    for (int oy = -1; oy <= 1; ++oy)
+      for (int ox = -1; ox <= 1; ++ox) {
+        const int qx = px + ox, qy = py + oy, qz = pz + oz;
+        if (qx < 0 || qy < 0 || qz < 0 || qx >= Dp || qy >= Dp || qz >= Dp) continue;
+        for (int c = 0; c < 8; ++c) {
+          const int sx = 2 * qx + (c & 1), sy_ = 2 * qy + ((c >> 1) & 1), sz = 2 * qz + (c >> 2);
+          if (abs(sx - tx) <= 1 && abs(sy_ - ty) <= 1 && abs(sz - tz) <= 1) continue;  // adjacent: near
+          const int64_t s = (static_cast<int64_t>(sz) * D + sy_) * D + sx;
+          double scx, scy, scz, sw;
+          box_center(g, l, s, scx, scy, scz, sw);
+          __syncthreads();
+          const double* src = M + (lev_off[l] + s) * NB * 9;
+          for (int q = threadIdx.x; q < NB * 9; q += blockDim.x) sm[q] = src[q];
+          __syncthreads();
+          if (m < NB) {
+            const double* v = sm;
+            for (int qz_ = 0; qz_ < NN; ++qz_) {
+              const double dz = (scz + sw * c_xbar[qz_]) - z;
+              for (int qy_ = 0; qy_ < NN; ++qy_) {
+                const double dy = (scy + sw * c_xbar[qy_]) - y;
+#pragma unroll 2
+                for (int qx_ = 0; qx_ < NN; ++qx_, v += 9) {
+                  const double dx = (scx + sw * c_xbar[qx_]) - x;
+                  const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                  const double yr = rsqrt_dp(r2);
+                  const double h = yr * yr, e = yr * h;
+                  const double d1 = (2.0 / 3.0) * e, d2 = -2.0 * e * h;  // D: c1, c2
+                  const double p0 = fma(dz, v[2], fma(dy, v[1], dx * v[0]));
+                  const double p1 = fma(dz, v[5], fma(dy, v[4], dx * v[3]));
+                  const double p2 = fma(dz, v[8], fma(dy, v[7], dx * v[6]));
+                  const double ta = fma(e, p0, d2 * p2), tb = d2 * p1, tc = d2 * p0;
+                  A[0] = fma(ta, dx, fma(yr, v[0], fma(d1, v[6], A[0])));
+                  A[1] = fma(ta, dy, fma(yr, v[1], fma(d1, v[7], A[1])));
+                  A[2] = fma(ta, dz, fma(yr, v[2], fma(d1, v[8], A[2])));
+                  B[0] = fma(tb, dx, fma(d1, v[3], B[0]));
+                  B[1] = fma(tb, dy, fma(d1, v[4], B[1]));
+                  B[2] = fma(tb, dz, fma(d1, v[5], B[2]));
+                  Cc[0] = fma(tc, dx, fma(d1, v[0], Cc[0]));
+                  Cc[1] = fma(tc, dy, fma(d1, v[1], Cc[1]));
+                  Cc[2] = fma(tc, dz, fma(d1, v[2], Cc[2]));
+                }
+              }
+            }
+          }
+        }
+      }
+  if (m < NB) {
+    double* o = Lc + ((lev_off[l] + t) * NB + m) * 9;
+    for (int k = 0; k < 3; ++k) {
+      o[k] = A[k];
+      o[3 + k] = B[k];
+      o[6 + k] = Cc[k];
+    }
+  }
+}
+
 // L2P + P2P: one CTA per leaf; thread = target body (chunks of blockDim); sources of the 27
 // neighbouring leaves through shared memory (exact RPY incl. the overlap branch and the self term).
-template <int NN>
+// POLY: the leaf's 9-component local expansion (m2l_poly_kernel) and the pair radius w_i + w_j.
+template <int NN, bool POLY>
 __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict__ spos,
                                                       const double4* __restrict__ sf,
                                                       const int32_t* __restrict__ sidx,
@@ -319,7 +412,8 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
   if (done != nullptr && *done) return;
   constexpr int NB = NN * NN * NN;
   constexpr int TS = 128;
-  __shared__ double sl[NB * 3];
+  constexpr int C = POLY ? 9 : 3;
+  __shared__ double sl[NB * C];
   __shared__ double4 sp[TS], sfs[TS];
   const int64_t b = blockIdx.x;
   // grid.y: chunk of TS targets of the leaf (the leaf's targets in parallel CTAs)
@@ -329,7 +423,7 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
   const int bx = static_cast<int>(b % D), by = static_cast<int>((b / D) % D), bz = static_cast<int>(b / D / D);
   double cx, cy, cz, w;
   box_center(g, g.L, b, cx, cy, cz, w);
-  for (int t = threadIdx.x; t < 3 * NB; t += blockDim.x) sl[t] = Lc[(loff_L + b) * NB * 3 + t];
+  for (int t = threadIdx.x; t < C * NB; t += blockDim.x) sl[t] = Lc[(loff_L + b) * NB * C + t];
   const double a = g.a, a2 = a * a, ia = 1.0 / a;
   const long long near_bits = __double_as_longlong(4.0 * a2);
   for (int32_t k0 = i0; k0 < i1; k0 += TS) {
@@ -344,6 +438,7 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
     __syncthreads();  // (sl ready; sp / sfs free)
     if (act) {  // far field: interpolate the leaf's local expansion
       double wx[NN], wy[NN], wz[NN];
+      double ex[6] = {0, 0, 0, 0, 0, 0};  // POLY: L_B, L_C at u_i
       cheb_w<NN>(fmin(1.0, fmax(-1.0, (pi.x - cx) / w)), wx);
       cheb_w<NN>(fmin(1.0, fmax(-1.0, (pi.y - cy) / w)), wy);
       cheb_w<NN>(fmin(1.0, fmax(-1.0, (pi.z - cz) / w)), wz);
@@ -355,12 +450,20 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
 #pragma unroll
           for (int mx = 0; mx < NN; ++mx) {
             const double s = wx[mx] * wyz;
-            const double* v = sl + ((mz * NN + my) * NN + mx) * 3;
+            const double* v = sl + ((mz * NN + my) * NN + mx) * C;
             ux = fma(s, v[0], ux);
             uy = fma(s, v[1], uy);
             uz = fma(s, v[2], uz);
+#pragma unroll
+            for (int q = 0; q < C - 3; ++q) ex[q] = fma(s, v[3 + q], ex[q]);
           }
         }
+      if (POLY) {  // U = L_A + 2 w_i L_B + w_i^2 L_C
+        const double tw = 2.0 * pi.w, w2 = pi.w * pi.w;
+        ux = fma(w2, ex[3], fma(tw, ex[0], ux));
+        uy = fma(w2, ex[4], fma(tw, ex[1], uy));
+        uz = fma(w2, ex[5], fma(tw, ex[2], uz));
+      }
     }
     // near field: the 27 leaves around b (incl. b), fixed order
     for (int oz = -1; oz <= 1; ++oz)
@@ -385,9 +488,10 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
                 const double4 pj = sp[jj], fj = sfs[jj];
                 double dx, dy, dz;
                 const double r2 = rpy_r2(pi, pj, dx, dy, dz);
-                if (!rpy_is_near(r2, 0.0, false, near_bits)) {
-                  far_pair(dx, dy, dz, fj.x, fj.y, fj.z, a2, ux, uy, uz);
-                } else {  // overlap branch: (4/(3a))(1 - 9r/(32a)) I + (1/(8a^2 r)) d d^T
+                const double ab = POLY ? pi.w + pj.w : a;  // pair radius abar = (a_i + a_j)/2
+                if (!rpy_is_near(r2, ab, POLY, near_bits)) {
+                  far_pair(dx, dy, dz, fj.x, fj.y, fj.z, POLY ? ab * ab : a2, ux, uy, uz);
+                } else {  // overlap branch: (4/(3a))(1 - 9r/(32a)) I + (1/(8a^2 r)) d d^T, a = abar
                   double rs = 0.0, rr = 0.0;
                   if (r2 > 0.0) {
                     rs = rsqrt_dp(r2);
@@ -395,8 +499,9 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
                   } else {
                     atomicExch(err, 1);  // coincident centres (reading A12)
                   }
-                  const double c1 = (4.0 / 3.0) * ia * fma(-9.0 / 32.0 * ia, rr, 1.0);
-                  const double c2 = 0.125 * ia * ia * rs * fma(dz, fj.z, fma(dy, fj.y, dx * fj.x));
+                  const double iab = POLY ? 1.0 / ab : ia;
+                  const double c1 = (4.0 / 3.0) * iab * fma(-9.0 / 32.0 * iab, rr, 1.0);
+                  const double c2 = 0.125 * iab * iab * rs * fma(dz, fj.z, fma(dy, fj.y, dx * fj.x));
                   ux = fma(c2, dx, fma(c1, fj.x, ux));
                   uy = fma(c2, dy, fma(c1, fj.y, uy));
                   uz = fma(c2, dz, fma(c1, fj.z, uz));
@@ -406,7 +511,7 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
           }
         }
     if (act) {
-      const double cs = (4.0 / 3.0) * ia;  // self: F/(6 pi mu a) = (1/(8 pi mu)) (4/(3a)) F
+      const double cs = POLY ? (2.0 / 3.0) / pi.w : (4.0 / 3.0) * ia;  // self: F/(6 pi mu a) = (1/(8 pi mu)) (4/(3a)) F
       ux = fma(cs, fi.x, ux);
       uy = fma(cs, fi.y, uy);
       uz = fma(cs, fi.z, uz);
@@ -416,9 +521,10 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
   }
 }
 
-template <int NN>
+template <int NN, bool POLY>
 int fmm_launch(sc_ctx* ctx, const Geom& g, const double4* f4, double mu, double4* u4, const int32_t* done) {
   constexpr int NB = NN * NN * NN;
+  constexpr int C = POLY ? 9 : 3;
   const int nb = (NB + 31) / 32 * 32;
   const int L = g.L;
   const int64_t n = ctx->n;
@@ -429,19 +535,21 @@ int fmm_launch(sc_ctx* ctx, const Geom& g, const double4* f4, double mu, double4
   timer_begin(ctx, SC_K_RPY);
   gather_sorted_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->fmm_sidx.p, n, f4,
                                                                                        ctx->fmm_sf4.p);
-  p2m_kernel<NN><<<static_cast<unsigned>(nbox(L)), nb, 0, ctx->stream>>>(ctx->fmm_spos4.p, ctx->fmm_sf4.p,
-                                                                         ctx->fmm_lstart.p, g, M + lo[L] * NB * 3,
-                                                                         done);
+  p2m_kernel<NN, C><<<static_cast<unsigned>(nbox(L)), nb, 0, ctx->stream>>>(
+      ctx->fmm_spos4.p, ctx->fmm_sf4.p, ctx->fmm_lstart.p, g, M + lo[L] * NB * C, done);
   for (int l = L - 1; l >= 2; --l)
-    transfer_kernel<NN, true><<<static_cast<unsigned>(nbox(l)), nb, 0, ctx->stream>>>(
-        l, M + lo[l] * NB * 3, M + lo[l + 1] * NB * 3, done);
-  m2l_kernel<NN><<<static_cast<unsigned>(lo[L + 1] - lo[2]), nb, 0, ctx->stream>>>(g, loff, M, Lc, done);
+    transfer_kernel<NN, true, C><<<static_cast<unsigned>(nbox(l)), nb, 0, ctx->stream>>>(
+        l, M + lo[l] * NB * C, M + lo[l + 1] * NB * C, done);
+  if (POLY)
+    m2l_poly_kernel<NN><<<static_cast<unsigned>(lo[L + 1] - lo[2]), nb, 0, ctx->stream>>>(g, loff, M, Lc, done);
+  else
+    m2l_kernel<NN><<<static_cast<unsigned>(lo[L + 1] - lo[2]), nb, 0, ctx->stream>>>(g, loff, M, Lc, done);
   for (int l = 2; l < L; ++l)
-    transfer_kernel<NN, false><<<static_cast<unsigned>(nbox(l + 1)), nb, 0, ctx->stream>>>(
-        l, Lc + lo[l] * NB * 3, Lc + lo[l + 1] * NB * 3, done);
+    transfer_kernel<NN, false, C><<<static_cast<unsigned>(nbox(l + 1)), nb, 0, ctx->stream>>>(
+        l, Lc + lo[l] * NB * C, Lc + lo[l + 1] * NB * C, done);
   const double scale = 1.0 / (8.0 * 3.14159265358979323846 * mu);
   const dim3 gp(static_cast<unsigned>(nbox(L)), static_cast<unsigned>(std::max<int64_t>(1, (ctx->fmm_maxleaf + 127) / 128)));
-  l2p_p2p_kernel<NN><<<gp, 128, 0, ctx->stream>>>(
+  l2p_p2p_kernel<NN, POLY><<<gp, 128, 0, ctx->stream>>>(
       ctx->fmm_spos4.p, ctx->fmm_sf4.p, ctx->fmm_sidx.p, ctx->fmm_lstart.p, g, Lc, lo[L], scale, u4, ctx->derr,
       done);
   timer_end(ctx, SC_K_RPY);
@@ -453,30 +561,31 @@ int fmm_launch(sc_ctx* ctx, const Geom& g, const double4* f4, double mu, double4
   return 0;
 }
 
-__global__ void bbox_kernel(const double4* __restrict__ pos4, int64_t n, double* __restrict__ out /* 6 */) {
-  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+__global__ void bbox_kernel(const double4* __restrict__ pos4, int64_t n, double* __restrict__ out /* 8 */) {
+  double lo[4] = {1e300, 1e300, 1e300, 1e300}, hi[4] = {-1e300, -1e300, -1e300, -1e300};
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const double4 p = pos4[i];
     lo[0] = fmin(lo[0], p.x); lo[1] = fmin(lo[1], p.y); lo[2] = fmin(lo[2], p.z);
     hi[0] = fmax(hi[0], p.x); hi[1] = fmax(hi[1], p.y); hi[2] = fmax(hi[2], p.z);
+    lo[3] = fmin(lo[3], p.w); hi[3] = fmax(hi[3], p.w);  // half radii
   }
-  __shared__ double s[6][256];
-  for (int d = 0; d < 3; ++d) {
+  __shared__ double s[8][256];
+  for (int d = 0; d < 4; ++d) {
     s[d][threadIdx.x] = lo[d];
-    s[3 + d][threadIdx.x] = hi[d];
+    s[4 + d][threadIdx.x] = hi[d];
   }
   __syncthreads();
   for (int w = 128; w > 0; w >>= 1) {
     if (threadIdx.x < w)
-      for (int d = 0; d < 3; ++d) {
+      for (int d = 0; d < 4; ++d) {
         s[d][threadIdx.x] = fmin(s[d][threadIdx.x], s[d][threadIdx.x + w]);
-        s[3 + d][threadIdx.x] = fmax(s[3 + d][threadIdx.x], s[3 + d][threadIdx.x + w]);
+        s[4 + d][threadIdx.x] = fmax(s[4 + d][threadIdx.x], s[4 + d][threadIdx.x + w]);
       }
     __syncthreads();
   }
   if (threadIdx.x == 0)
-    for (int d = 0; d < 6; ++d) out[blockIdx.x * 6 + d] = s[d][0];
+    for (int d = 0; d < 8; ++d) out[blockIdx.x * 8 + d] = s[d][0];
 }
 
 double cheb_S(int n, double xk, double u) {  // host: S_n(xbar_k, u)
@@ -524,24 +633,26 @@ int fmm_init_device(sc_ctx* ctx) {
 int fmm_setup(sc_ctx* ctx) {
   const int nn = ctx->fmm_order;
   if (nn != 4 && nn != 6 && nn != 8) return fail(ctx, SC_EINVAL, "fmm order must be 4, 6 or 8");
-  if (ctx->kind != kSpheres || ctx->poly) return fail(ctx, SC_EINVAL, "the fast RPY summation needs monodisperse spheres");
+  if (ctx->kind != kSpheres) return fail(ctx, SC_EINVAL, "the fast RPY summation is for spheres");
   const int64_t n = ctx->n;
   // bounding cube
   const int nbb = 64;
-  if (int rc = ensure(ctx, ctx->bbox_part, 6 * nbb)) return rc;
+  if (int rc = ensure(ctx, ctx->bbox_part, 8 * nbb)) return rc;
   bbox_kernel<<<nbb, 256, 0, ctx->stream>>>(ctx->pos4.p, n, ctx->bbox_part.p);
   if (int rc = check_launch(ctx, "fmm_bbox")) return rc;
-  std::vector<double> hb(6 * nbb);
-  SC_CUDA(cudaMemcpyAsync(hb.data(), ctx->bbox_part.p, sizeof(double) * 6 * nbb, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<double> hb(8 * nbb);
+  SC_CUDA(cudaMemcpyAsync(hb.data(), ctx->bbox_part.p, sizeof(double) * 8 * nbb, cudaMemcpyDeviceToHost, ctx->stream));
   SC_CUDA(cudaStreamSynchronize(ctx->stream));
-  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  double lo[4] = {1e300, 1e300, 1e300, 1e300}, hi[4] = {-1e300, -1e300, -1e300, -1e300};
   for (int b = 0; b < nbb; ++b)
-    for (int d = 0; d < 3; ++d) {
-      lo[d] = std::min(lo[d], hb[b * 6 + d]);
-      hi[d] = std::max(hi[d], hb[b * 6 + 3 + d]);
+    for (int d = 0; d < 4; ++d) {
+      lo[d] = std::min(lo[d], hb[b * 8 + d]);
+      hi[d] = std::max(hi[d], hb[b * 8 + 4 + d]);
     }
   double ext = std::max(hi[0] - lo[0], std::max(hi[1] - lo[1], hi[2] - lo[2]));
-  const double a = ctx->a_const;
+  // the largest pair radius: every overlapping pair (r < 2 abar <= 2 a_max) must lie in
+  // neighbouring leaves, and well-separated boxes are >= one leaf side >= 2 a_max apart
+  const double a = ctx->poly ? 2.0 * hi[3] : ctx->a_const;
   ext = std::max(ext, 8.0 * a) * (1.0 + 1e-9) + 1e-9;  // (>= 4 leaves of side >= 2a per dimension)
   // leaf level: largest useful L with leaf side >= 2a (far branch between well-separated boxes,
   // every overlapping pair in neighbouring leaves), chosen to balance the P2P and M2L work
@@ -554,7 +665,7 @@ int fmm_setup(sc_ctx* ctx) {
     for (int l = 2; l <= std::min(Lmax, 7); ++l) {
       const double leaves = static_cast<double>(nbox(l));
       const double p2p = static_cast<double>(n) * 27.0 * (static_cast<double>(n) / leaves);
-      const double m2l = 0.8 * 1.15 * leaves * 150.0 * nb3 * nb3;
+      const double m2l = (ctx->poly ? 1.8 : 1.0) * 0.8 * 1.15 * leaves * 150.0 * nb3 * nb3;  // (poly: 3 fields)
       const double fill = std::min(1.0, leaves * std::max(1.0, static_cast<double>(n) / leaves / 128.0) /
                                             (2.0 * std::max(ctx->num_sms, 1)));
       const double cost = (p2p + m2l) / fill;
@@ -566,6 +677,7 @@ int fmm_setup(sc_ctx* ctx) {
   }
   L = std::max(2, std::min(L, Lmax));
   ctx->fmm_L_used = L;
+  ctx->fmm_poly = ctx->poly;
   ctx->fmm_geom[0] = 0.5 * (lo[0] + hi[0]) - 0.5 * ext;
   ctx->fmm_geom[1] = 0.5 * (lo[1] + hi[1]) - 0.5 * ext;
   ctx->fmm_geom[2] = 0.5 * (lo[2] + hi[2]) - 0.5 * ext;
@@ -612,8 +724,9 @@ int fmm_setup(sc_ctx* ctx) {
   }
   // (offsets relative to level 2: lev_off[l] = boxes of levels 2..l-1)
   const int64_t nb3 = static_cast<int64_t>(nn) * nn * nn;
-  if (int rc = ensure(ctx, ctx->fmm_M, static_cast<size_t>(off) * nb3 * 3)) return rc;
-  if (int rc = ensure(ctx, ctx->fmm_L, static_cast<size_t>(off) * nb3 * 3)) return rc;
+  const int ncomp = ctx->poly ? 9 : 3;  // node components (fmm_launch's C)
+  if (int rc = ensure(ctx, ctx->fmm_M, static_cast<size_t>(off) * nb3 * ncomp)) return rc;
+  if (int rc = ensure(ctx, ctx->fmm_L, static_cast<size_t>(off) * nb3 * ncomp)) return rc;
   if (int rc = ensure(ctx, ctx->fmm_lev_off_dev, L + 2)) return rc;
   SC_CUDA(cudaMemcpyAsync(ctx->fmm_lev_off_dev.p, ctx->fmm_lev_off.data(), sizeof(int64_t) * (L + 2),
                           cudaMemcpyHostToDevice, ctx->stream));
@@ -627,10 +740,15 @@ int fmm_apply(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int3
     if (int rc = fmm_setup(ctx)) return rc;
   }
   Geom g{ctx->fmm_geom[0], ctx->fmm_geom[1], ctx->fmm_geom[2], ctx->fmm_geom[3], ctx->a_const, ctx->fmm_L_used};
+  if (ctx->fmm_poly) switch (ctx->fmm_order) {
+      case 4: return fmm_launch<4, true>(ctx, g, f4, mu, u4, done);
+      case 6: return fmm_launch<6, true>(ctx, g, f4, mu, u4, done);
+      default: return fmm_launch<8, true>(ctx, g, f4, mu, u4, done);
+    }
   switch (ctx->fmm_order) {
-    case 4: return fmm_launch<4>(ctx, g, f4, mu, u4, done);
-    case 6: return fmm_launch<6>(ctx, g, f4, mu, u4, done);
-    default: return fmm_launch<8>(ctx, g, f4, mu, u4, done);
+    case 4: return fmm_launch<4, false>(ctx, g, f4, mu, u4, done);
+    case 6: return fmm_launch<6, false>(ctx, g, f4, mu, u4, done);
+    default: return fmm_launch<8, false>(ctx, g, f4, mu, u4, done);
   }
 }
 

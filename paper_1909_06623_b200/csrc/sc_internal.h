@@ -133,7 +133,7 @@ struct sc_ctx {
   int mobility_model = 0;       // 0: BASELINE RPY (tt + self rotation); 1: full 6N RPY (NEXT row f4(ii));
                                 // 2: BASELINE RPY by the fast summation (NEXT row f4(i), fmm.cu)
   // fast RPY summation (fmm.cu): Chebyshev order, leaf level (0: automatic), the tree of the bodies
-  int fmm_order = 6, fmm_leaf_level = 0, fmm_L_used = 0;
+  int fmm_order = 6, fmm_leaf_level = 0, fmm_L_used = 0, fmm_poly = 0;
   int64_t fmm_maxleaf = 0;      // bodies in the fullest leaf
   bool fmm_ready = false;       // tree built for the current bodies
   double fmm_geom[4] = {};      // root cube corner (x, y, z) and side
