@@ -577,7 +577,7 @@ void sc_destroy(sc_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   release(ctx->pos4); release(ctx->dir4); release(ctx->rodmob4);
   release(ctx->ci); release(ctx->cj); release(ctx->nrm4); release(ctx->lev4); release(ctx->rxn4);
-  release(ctx->rpy6_part); release(ctx->ft_tmp); release(ctx->row_ptr); release(ctx->inc); release(ctx->icol4); release(ctx->first_ptr); release(ctx->near_ptr); release(ctx->near_idx);
+  release(ctx->rpy6_part); release(ctx->ft_tmp); release(ctx->row_ptr); release(ctx->inc); release(ctx->icol4); release(ctx->einc); release(ctx->hinc); release(ctx->first_ptr); release(ctx->near_ptr); release(ctx->near_idx);
   release(ctx->q); release(ctx->gam[0]); release(ctx->gam[1]); release(ctx->g[0]); release(ctx->g[1]);
   release(ctx->w); release(ctx->gam_user); release(ctx->uc); release(ctx->prev_key); release(ctx->prev_gam); release(ctx->chunk_part); release(ctx->chunk_red);
   release(ctx->fmm_key); release(ctx->fmm_idx0); release(ctx->fmm_sidx); release(ctx->fmm_cnt); release(ctx->fmm_lstart); release(ctx->fmm_cubtmp); release(ctx->fmm_spos4); release(ctx->fmm_sf4); release(ctx->fmm_M); release(ctx->fmm_L); release(ctx->fmm_lev_off_dev);
@@ -1171,7 +1171,11 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     if (int rc = launch_gather_raw(ctx, gfin, 1, mu, dF)) return rc;
   }
   if (dU) {
-    if (stt.iters == 0 && stt.mvops >= 2) {  // j_max = 0: u4 holds the alpha_0 product, recompute
+    // j_max = 0: u4 holds the alpha_0 product; rods: the projected gathers of the loop write only
+    // the half rates -- recompute U = M D gamma from the final gamma
+    if (!spheres) {
+      if (int rc = launch_gather_raw(ctx, gfin, 1, mu, nullptr, false)) return rc;
+    } else if (stt.iters == 0 && stt.mvops >= 2) {
       if (int rc = mvop_raw(gfin, 1)) return rc;
     }
     if (spheres && ctx->mobility_model == 1) {  // U_c = M D gamma with the coupling blocks (Omega_c)

@@ -83,6 +83,15 @@ __global__ void rod_incidence_columns(const int32_t* __restrict__ inc, const int
   icolr[3 * e + 2] = make_double2(sg * r.y, sg * r.z);
 }
 
+// einc[l] = (e_i, e_j): where constraint l's two incidences sit in the body-sorted incidence
+// list (the rods D^T reads the per-incidence half rates h_e there); e_j = -1 for a wall.
+__global__ void rod_incidence_positions(const int32_t* __restrict__ inc, const int32_t* __restrict__ ninc_dev,
+                                        int64_t ninc, int32_t* __restrict__ epos) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= ninc || e >= *ninc_dev) return;
+  epos[inc[e]] = static_cast<int32_t>(e);  // inc[e] = 2 l + side
+}
+
 __global__ void rod_columns(const double4* __restrict__ nrm4, const double4* __restrict__ lev4, int64_t nc,
                             double4* __restrict__ rxn4) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -136,6 +145,14 @@ int assemble(sc_ctx* ctx) {
                                                                   reinterpret_cast<double2*>(ctx->icol4.p));
       timer_end(ctx, SC_K_ASSEMBLE);
       if (int rc = check_launch(ctx, "rod_incidence_columns")) return rc;
+      if (int rc = ensure(ctx, ctx->einc, nc)) return rc;
+      if (int rc = ensure(ctx, ctx->hinc, 2 * nc + 1)) return rc;
+      SC_CUDA(cudaMemsetAsync(ctx->einc.p, 0xFF, sizeof(int2) * nc, ctx->stream));  // -1: no incidence (wall)
+      timer_begin(ctx, SC_K_ASSEMBLE);
+      rod_incidence_positions<<<nblk(2 * nc), kT, 0, ctx->stream>>>(ctx->inc.p, ctx->row_ptr.p + n, 2 * nc,
+                                                                    reinterpret_cast<int32_t*>(ctx->einc.p));
+      timer_end(ctx, SC_K_ASSEMBLE);
+      if (int rc = check_launch(ctx, "rod_incidence_positions")) return rc;
 
     }
     if (ctx->kind == kSpheres) {  // (rods gather from the per-constraint columns)

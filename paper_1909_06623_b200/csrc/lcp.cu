@@ -22,6 +22,10 @@
 namespace sc {
 namespace {
 
+#ifndef SC_RODS_HSPLIT
+#define SC_RODS_HSPLIT 1  // rods D^T from per-incidence half rates (0: from the body velocities)
+#endif
+
 constexpr int kT = 256;
 inline unsigned nblk(int64_t n) { return static_cast<unsigned>((n + kT - 1) / kT); }
 
@@ -40,7 +44,7 @@ __global__ void __launch_bounds__(kT) gather_kernel(
     const double2* __restrict__ st_old, double2* __restrict__ st_new, const DevScalars* __restrict__ dsc, int64_t n,
     int64_t nout,
     const double4* __restrict__ dir4, const double4* __restrict__ mob4, double4* __restrict__ out4,
-    double* __restrict__ outFT, const int32_t* __restrict__ done, int64_t nc_chk) {
+    double* __restrict__ outFT, const int32_t* __restrict__ done, int64_t nc_chk, double* __restrict__ hout) {
   if (done != nullptr && *done) return;
   const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t b = gt / LPB;
@@ -95,6 +99,35 @@ __global__ void __launch_bounds__(kT) gather_kernel(
       tz += __shfl_xor_sync(0xffffffffu, tz, o);
     }
   }
+  if (KIND == kRods && OUT == kOutRodU && SC_RODS_HSPLIT) {
+    // the body's (U, W) from its lane 0 to every lane, then each lane writes the half rate
+    // h_e = (signed column of e) . (U, W) of its incidences: D_l^T (U, W) = h_{e_i(l)} + h_{e_j(l)}
+    // (the D^T pass reads 2 x 8 B per constraint instead of the columns and 2 body velocities)
+    double4 U = make_double4(0, 0, 0, 0), W = U;
+    if (k == 0 && real) {
+      const double f[6] = {fx, fy, fz, tx, ty, tz};
+      rods_drag(tb, mb, f, U, W);
+    }
+    const int src = static_cast<int>(threadIdx.x & 31) & ~(LPB - 1);
+    U.x = __shfl_sync(0xffffffffu, U.x, src);
+    U.y = __shfl_sync(0xffffffffu, U.y, src);
+    U.z = __shfl_sync(0xffffffffu, U.z, src);
+    W.x = __shfl_sync(0xffffffffu, W.x, src);
+    W.y = __shfl_sync(0xffffffffu, W.y, src);
+    W.z = __shfl_sync(0xffffffffu, W.z, src);
+    const double2* icr = reinterpret_cast<const double2*>(icol4);
+    for (int32_t e = e0 + k; e < e1; e += LPB) {
+      const double2 c0 = icr[3 * e], c1 = icr[3 * e + 1], c2 = icr[3 * e + 2];
+      const double un = fma(c1.x, U.z, fma(c0.y, U.y, c0.x * U.x));
+      const double wr = fma(c2.y, W.z, fma(c2.x, W.y, c1.y * W.x));
+      hout[e] = un + wr;
+    }
+    // (U, W) themselves only from the raw gathers (the solve recomputes U_c from the final gamma;
+    // the iteration's D^T needs only the half rates)
+    if (MODE == kProj || k != 0 || b >= nout) return;
+    rods_store_uw(out4, b, U, W);  // (zero for padded rows)
+    return;
+  }
   if (k != 0 || b >= nout) return;
   if (!real) {  // padded source rows: zero force
     if (OUT == kOutF4) out4[b] = make_double4(0, 0, 0, 0);
@@ -135,7 +168,7 @@ __global__ void __launch_bounds__(kR) dt_kernel(
     const double4* __restrict__ u4, const double* __restrict__ q, const double* __restrict__ gam_new,
     double* __restrict__ g_out, double2* __restrict__ st_old, double2* __restrict__ st_new,
     double* __restrict__ part, const int32_t* __restrict__ done, int64_t nchunks, DevScalars* __restrict__ sc,
-    unsigned int* __restrict__ counter) {
+    unsigned int* __restrict__ counter, const int2* __restrict__ einc, const double* __restrict__ hinc) {
   if (done != nullptr && *done) return;
   __shared__ double red[4 * kR];
   const int64_t c = c0 + blockIdx.x;
@@ -154,6 +187,11 @@ __global__ void __launch_bounds__(kR) dt_kernel(
         const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
         const double4 ui = u4[i], uj = wall ? z4 : u4[j];
         v = fma(nv.z, ui.z - uj.z, fma(nv.y, ui.y - uj.y, nv.x * (ui.x - uj.x)));
+      } else if (SC_RODS_HSPLIT) {  // the two half rates of the gather (e_j = -1: a wall at rest)
+        const int2 ep = einc[l];
+        SC_DCHECK(ep.x >= 0 && ep.x < 2 * nc && ep.y < 2 * nc);
+        const double hj = ep.y >= 0 ? hinc[ep.y] : 0.0;
+        v = hinc[ep.x] + hj;
       } else {
         v = rods_dt_value<false>(l, n, ci, cj, nrm4, rxn4, u4);
       }
@@ -368,38 +406,38 @@ int launch_gather_proj(sc_ctx* ctx, int pp, double mu) {
   if (ctx->kind == kSpheres)
     gather_kernel<kSpheres, kProj, kOutF4, kLpbS><<<nblk(ctx->npad * kLpbS), kT, 0, ctx->stream>>>(
         ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, nullptr, 1, so, sn, ctx->dsc, ctx->n,
-        ctx->npad, nullptr, nullptr, ctx->f4.p, nullptr, done, ctx->nc);
+        ctx->npad, nullptr, nullptr, ctx->f4.p, nullptr, done, ctx->nc, nullptr);
   else
     gather_kernel<kRods, kProj, kOutRodU, kLpbR><<<nblk(ctx->npad * kLpbR), kT, 0, ctx->stream>>>(
         ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, nullptr, 1, so, sn, ctx->dsc, ctx->n,
-        ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done, ctx->nc);
+        ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done, ctx->nc, ctx->hinc.p);
   timer_end(ctx, SC_K_GATHER);
   return check_launch(ctx, "gather_proj");
 }
 
 // F = D v for v[l * vstride] (vstride 2: a component of the packed state)
-int launch_gather_raw(sc_ctx* ctx, const double* v, int vstride, double mu, double* FT_user) {
+int launch_gather_raw(sc_ctx* ctx, const double* v, int vstride, double mu, double* FT_user, bool gated) {
   (void)mu;
   timer_begin(ctx, SC_K_GATHER);
   if (FT_user != nullptr) {
     if (ctx->kind == kSpheres)
       gather_kernel<kSpheres, kRaw, kOutFT, kLpbS><<<nblk(ctx->n * kLpbS), kT, 0, ctx->stream>>>(
           ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, vstride, nullptr, nullptr, ctx->dsc,
-          ctx->n, ctx->n, nullptr, nullptr, nullptr, FT_user, nullptr, ctx->nc);
+          ctx->n, ctx->n, nullptr, nullptr, nullptr, FT_user, nullptr, ctx->nc, nullptr);
     else
       gather_kernel<kRods, kRaw, kOutFT, kLpbR><<<nblk(ctx->n * kLpbR), kT, 0, ctx->stream>>>(
           ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, vstride, nullptr, nullptr, ctx->dsc,
-          ctx->n, ctx->n, nullptr, nullptr, nullptr, FT_user, nullptr, ctx->nc);
+          ctx->n, ctx->n, nullptr, nullptr, nullptr, FT_user, nullptr, ctx->nc, nullptr);
   } else {
-    const int32_t* done = &ctx->dsc->done;
+    const int32_t* done = gated ? &ctx->dsc->done : nullptr;
     if (ctx->kind == kSpheres)
       gather_kernel<kSpheres, kRaw, kOutF4, kLpbS><<<nblk(ctx->npad * kLpbS), kT, 0, ctx->stream>>>(
           ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, vstride, nullptr, nullptr, ctx->dsc,
-          ctx->n, ctx->npad, nullptr, nullptr, ctx->f4.p, nullptr, done, ctx->nc);
+          ctx->n, ctx->npad, nullptr, nullptr, ctx->f4.p, nullptr, done, ctx->nc, nullptr);
     else
       gather_kernel<kRods, kRaw, kOutRodU, kLpbR><<<nblk(ctx->npad * kLpbR), kT, 0, ctx->stream>>>(
           ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, vstride, nullptr, nullptr, ctx->dsc,
-          ctx->n, ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done, ctx->nc);
+          ctx->n, ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done, ctx->nc, ctx->hinc.p);
   }
   timer_end(ctx, SC_K_GATHER);
   return check_launch(ctx, "gather_raw");
@@ -447,12 +485,13 @@ int launch_dt(sc_ctx* ctx, int mode, int pp, const double* x, double* g_out, int
     if (fuse)                                                                                                   \
       dt_kernel<KIND, MODE, true><<<grid, kR, 0, ctx->stream>>>(fp, ctx->n, ctx->nc, c0, ctx->ci.p, ctx->cj.p,    \
                                                                 ctx->nrm4.p, ctx->rxn4.p, u4, q, x, g_out, so, sn, \
-                                                                part, done, ctx->nchunks, ctx->dsc, ctx->dcount);  \
+                                                                part, done, ctx->nchunks, ctx->dsc, ctx->dcount,   \
+                                                                ctx->einc.p, ctx->hinc.p);                         \
     else                                                                                                        \
       dt_kernel<KIND, MODE, false><<<grid, kR, 0, ctx->stream>>>(fp, ctx->n, ctx->nc, c0, ctx->ci.p, ctx->cj.p,   \
                                                                  ctx->nrm4.p, ctx->rxn4.p, u4, q, x, g_out, so,   \
                                                                  sn, part, done, ctx->nchunks, ctx->dsc,          \
-                                                                 ctx->dcount);                                    \
+                                                                 ctx->dcount, ctx->einc.p, ctx->hinc.p);          \
   } while (0)
 #define SC_DT_ALL(KIND)                                \
   switch (mode) {                                      \

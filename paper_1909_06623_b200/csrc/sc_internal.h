@@ -110,6 +110,8 @@ struct sc_ctx {
   sc::DBuf<int32_t> row_ptr;    // n+1
   sc::DBuf<int32_t> inc;        // 2*nc: (l << 1) | side
   sc::DBuf<double4> icol4;      // signed D columns per incidence (spheres: 1 double4; rods: 3 double2)
+  sc::DBuf<int2> einc;          // rods: incidence positions (e_i, e_j) of constraint l (e_j = -1: wall)
+  sc::DBuf<double> hinc;        // rods: h_e = (signed column of e) . (U, W) of its body, per incidence
   sc::DBuf<int32_t> first_ptr;  // n+1: constraints with first body < b start at first_ptr[b]
   sc::DBuf<int32_t> near_ptr, near_idx;  // spheres: RPY overlap-branch partners per body (CSR)
   int64_t nchunks = 0;
@@ -255,7 +257,9 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
 // or a user FT (n x 6).
 // The BBPGD state is packed per constraint: st[k][l] = (gamma_l, g_l), ping-pong k = 0, 1.
 int launch_gather_proj(sc_ctx* ctx, int pp, double mu);  // st[pp] -> st[pp ^ 1].x, F
-int launch_gather_raw(sc_ctx* ctx, const double* v, int vstride, double mu, double* FT_user /*nullable*/);
+// gated: skip when the solve's done flag is set (inside the BBPGD loop); false after the loop
+int launch_gather_raw(sc_ctx* ctx, const double* v, int vstride, double mu, double* FT_user /*nullable*/,
+                      bool gated = true);
 int launch_proj_own(sc_ctx* ctx, int pp, int64_t l0, int64_t l1);
 int launch_pack_gamma0(sc_ctx* ctx, const double* gam0);  // st[0] = (max(0, gamma_0), 0)
 int launch_unpack_state(sc_ctx* ctx, int pp, double* gam, double* g);
