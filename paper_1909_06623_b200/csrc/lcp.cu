@@ -22,6 +22,9 @@
 namespace sc {
 namespace {
 
+#ifndef SC_RODS_PEEL
+#define SC_RODS_PEEL 2  // rods half rates: a lane's first PEEL incidences issued straight-line (loads in flight)
+#endif
 #ifndef SC_RODS_HSPLIT
 #define SC_RODS_HSPLIT 1  // rods D^T from per-incidence half rates (0: from the body velocities)
 #endif
@@ -31,7 +34,10 @@ inline unsigned nblk(int64_t n) { return static_cast<unsigned>((n + kT - 1) / kT
 
 enum GatherMode { kProj = 0, kRaw = 1 };
 constexpr int kLpbS = 2;  // lanes per body in the D-gather: spheres (~2.7 incidences per body)
-constexpr int kLpbR = 4;  // rods (~4.5 incidences per body)
+#ifndef SC_RODS_LPB
+#define SC_RODS_LPB 4
+#endif
+constexpr int kLpbR = SC_RODS_LPB;  // rods (~4.5 incidences per body)
 enum GatherOut { kOutF4 = 0, kOutRodU = 1, kOutFT = 2 };
 
 // LPB lanes cooperate on one body (incidences e0+k, e0+k+LPB, ...), then an xor-butterfly
@@ -61,7 +67,41 @@ __global__ void __launch_bounds__(kT) gather_kernel(
     tb = dir4[b];
     mb = mob4[b];
   }
-  if (KIND == kRods) {  // the signed columns of the incidences, streamed (assemble.cu)
+  if (KIND == kRods && OUT == kOutRodU && SC_RODS_HSPLIT) {
+    // the lane's first SC_RODS_PEEL incidences straight-line: their loads in flight together
+    // (measured faster than an unrolled loop; keeping their columns in registers for the h pass
+    // below cost occupancy: 64 -> 70 / 90 registers, slower)
+    double f[6] = {0, 0, 0, 0, 0, 0};
+    const double2* icr = reinterpret_cast<const double2*>(icol4);
+    auto one = [&](int32_t e, double2* c) {
+      const int32_t v = inc[e];
+      const int32_t l = v >> 1;
+      double gm;
+      if (MODE == kProj) {
+        const double2 s = st_old[l];
+        const double x = __dsub_rn(s.x, __dmul_rn(alpha, s.y));  // Step 8
+        gm = x > 0.0 ? x : 0.0;                                  // Step 9
+        if ((v & 1) == 0) st_new[l].x = gm;                      // owner = first body
+      } else {
+        gm = a[static_cast<int64_t>(l) * astride];
+      }
+      c[0] = icr[3 * e];
+      c[1] = icr[3 * e + 1];
+      c[2] = icr[3 * e + 2];
+      f[0] = fma(gm, c[0].x, f[0]);
+      f[1] = fma(gm, c[0].y, f[1]);
+      f[2] = fma(gm, c[1].x, f[2]);
+      f[3] = fma(gm, c[1].y, f[3]);
+      f[4] = fma(gm, c[2].x, f[4]);
+      f[5] = fma(gm, c[2].y, f[5]);
+    };
+    double2 ct[3];
+#pragma unroll
+    for (int p = 0; p < SC_RODS_PEEL; ++p)
+      if (e0 + k + p * LPB < e1) one(e0 + k + p * LPB, ct);
+    for (int32_t e = e0 + k + SC_RODS_PEEL * LPB; e < e1; e += LPB) one(e, ct);
+    fx = f[0]; fy = f[1]; fz = f[2]; tx = f[3]; ty = f[4]; tz = f[5];
+  } else if (KIND == kRods) {  // the signed columns of the incidences, streamed (assemble.cu)
     double f[6] = {0, 0, 0, 0, 0, 0};
     rods_gather_lane<LPB, MODE == kProj>(e0, e1, k, alpha, inc, a, astride, st_old, st_new,
                                          reinterpret_cast<const double2*>(icol4), f);
@@ -116,11 +156,14 @@ __global__ void __launch_bounds__(kT) gather_kernel(
     W.y = __shfl_sync(0xffffffffu, W.y, src);
     W.z = __shfl_sync(0xffffffffu, W.z, src);
     const double2* icr = reinterpret_cast<const double2*>(icol4);
+    auto half_rate = [&](const double2* c) {
+      const double un = fma(c[1].x, U.z, fma(c[0].y, U.y, c[0].x * U.x));
+      const double wr = fma(c[2].y, W.z, fma(c[2].x, W.y, c[1].y * W.x));
+      return un + wr;
+    };
     for (int32_t e = e0 + k; e < e1; e += LPB) {
-      const double2 c0 = icr[3 * e], c1 = icr[3 * e + 1], c2 = icr[3 * e + 2];
-      const double un = fma(c1.x, U.z, fma(c0.y, U.y, c0.x * U.x));
-      const double wr = fma(c2.y, W.z, fma(c2.x, W.y, c1.y * W.x));
-      hout[e] = un + wr;
+      const double2 c[3] = {icr[3 * e], icr[3 * e + 1], icr[3 * e + 2]};
+      hout[e] = half_rate(c);
     }
     // (U, W) themselves only from the raw gathers (the solve recomputes U_c from the final gamma;
     // the iteration's D^T needs only the half rates)
