@@ -334,12 +334,14 @@ def _hbm_peak():
 def other_configs():
     """Time to solution (device-timed, CUDA events on the library stream around the solve, inputs
     resident) of the converged BASELINE configs: C1 (512 spheres, persistent loop), C2 (8,192
-    polydisperse spheres), C3 (65,536 spheres, phi = 0.5), C4 (200,000 rods, persistent loop) and
-    C5 converged (262,144 spheres).  Plus the HBM roofline of the D-gather (a3) and D^T (a5)
-    kernels from a second solve with CUDA events around every launch (algorithmic bytes of
-    SURVEY.md section 8(d): spheres 96 B/constraint + 28 B/body and 120 B/constraint, rods
-    144 B/constraint + 84 B/body and 216 B/constraint).  Context for the BBPGD-iterations/s half of
-    the metric; not part of `value`."""
+    polydisperse spheres), C3 (65,536 spheres, phi = 0.5), C4 (200,000 rods) and C5 converged
+    (262,144 spheres).  Plus the HBM roofline of the D-gather (a3) and D^T (a5) kernels from a
+    second solve with CUDA events around every launch (algorithmic bytes of SURVEY.md section 8(d):
+    spheres 96 B/constraint + 28 B/body and 120 B/constraint, rods 144 B/constraint + 84 B/body and
+    216 B/constraint).  Rods: the gather also forms the per-incidence half rates that the D^T pass
+    sums, so the column work of D^T runs in the gather -- the per-kernel split
+    of the section 8(d) bytes is nominal there and `iteration_frac` is the figure.  Context for the
+    BBPGD-iterations/s half of the metric; not part of `value`."""
     import torch
 
     from paper_1909_06623_b200 import Context
@@ -391,7 +393,9 @@ def other_configs():
                        "frac": db / dus / 1e3 / peak, "launches": tim["dt"][1]},
                 "iteration_frac": (gb + db) / (d["us_per_iter"] * 1e3) / peak,
                 "note": "iteration_frac: algorithmic bytes of gather + D^T per iteration / time to solution "
-                        "per iteration (the persistent rods loop has no per-kernel events)"}
+                        "per iteration (device-side graph loop, no per-launch events)" + (
+                            "; rods: D^T sums the gather's per-incidence half rates, so the per-kernel "
+                            "fractions split the section 8(d) bytes nominally" if rods else "")}
         res[name] = d
         ctx.close()
     # C5 with the fast O(N) RPY summation (NEXT row f4(i), order 8, approximate operator: rel. L2
