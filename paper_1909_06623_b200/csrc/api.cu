@@ -531,6 +531,7 @@ static int create_common(sc_ctx** out, int device, void* stream) {
     return SC_ECUDA;
   }
   if (const char* v = std::getenv("SC_SYM_VARIANT")) ctx->sym_variant = std::atoi(v);
+  if (const char* v = std::getenv("SC_SYM_HS")) ctx->sym_hs = std::atoi(v);
   if (const char* v = std::getenv("SC_BATCH")) ctx->batch_override = std::atoi(v);
   if (const char* v = std::getenv("SC_NO_GRAPHS")) ctx->use_graphs = std::atoi(v) == 0;
   if (const char* v = std::getenv("SC_NO_PERSIST")) ctx->use_persist = std::atoi(v) == 0;

@@ -803,7 +803,9 @@ int rpy_apply_sym(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const 
   // prologue cost per halving (C2: 136 pairs -> hs = 8); large N keeps hs = 1.  hs depends on N
   // only (all pairs, not this rank's), so every partial sum -- and U -- is the same for any P.
   int hs = 1;
-  if (ctx->sym_variant == 0) {
+  if (ctx->sym_hs == 1 || ctx->sym_hs == 2 || ctx->sym_hs == 4 || ctx->sym_hs == 8) {
+    hs = ctx->sym_hs;
+  } else if (ctx->sym_variant == 0) {
     const double units = 0.5 * static_cast<double>(NS) * static_cast<double>(NS + 1);
     const double slots = 3.0 * (ctx->num_sms > 0 ? ctx->num_sms : 148);
     double best = 1e300;
