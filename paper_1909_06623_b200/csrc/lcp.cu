@@ -5,8 +5,11 @@
 //   gamma_l = max(0, gamma_l^old - alpha g_l^old)   (Steps 8-9)
 // recomputed identically by both incident bodies; the first body (owner)
 // writes gamma_l.  For rods the 6x6 drag mobility is applied in the same
-// thread (U = M_b F_b), so the rods MVOP is one gather + one D^T pass.
-// K-DT (a5): per constraint g_l = n.(U_i - U_j) [+ (r_i x n).W_i - (r_j x n).W_j] + q_l
+// thread (U = M_b F_b), so the rods MVOP is one gather + one D^T pass; the
+// gather also writes the half rates h_e = (sigma n, sigma r x n)_e . (U, W)_b of
+// the body's incidences.
+// K-DT (a5): per constraint g_l = n.(U_i - U_j) + q_l (spheres) or
+//   h_{e_i(l)} + h_{e_j(l)} + q_l (rods: n.(U_i - U_j) + (r_i x n).W_i - (r_j x n).W_j)
 //   (Step 10), fused with the partial sums of s.s, s.y, y.y and min(gamma, g)^2
 //   (Steps 11, 14-15) over a FIXED chunking: spheres, chunk c = constraints
 //   whose first body lies in [256c, 256c+256); rods, 256 consecutive constraints
@@ -24,9 +27,6 @@ namespace {
 
 #ifndef SC_RODS_PEEL
 #define SC_RODS_PEEL 2  // rods half rates: a lane's first PEEL incidences issued straight-line (loads in flight)
-#endif
-#ifndef SC_RODS_HSPLIT
-#define SC_RODS_HSPLIT 1  // rods D^T from per-incidence half rates (0: from the body velocities)
 #endif
 
 constexpr int kT = 256;
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kT) gather_kernel(
     tb = dir4[b];
     mb = mob4[b];
   }
-  if (KIND == kRods && OUT == kOutRodU && SC_RODS_HSPLIT) {
+  if (KIND == kRods && OUT == kOutRodU) {
     // the lane's first SC_RODS_PEEL incidences straight-line: their loads in flight together
     // (measured faster than an unrolled loop; keeping their columns in registers for the h pass
     // below cost occupancy: 64 -> 70 / 90 registers, slower)
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kT) gather_kernel(
       if (e0 + k + p * LPB < e1) one(e0 + k + p * LPB, ct);
     for (int32_t e = e0 + k + SC_RODS_PEEL * LPB; e < e1; e += LPB) one(e, ct);
     fx = f[0]; fy = f[1]; fz = f[2]; tx = f[3]; ty = f[4]; tz = f[5];
-  } else if (KIND == kRods) {  // the signed columns of the incidences, streamed (assemble.cu)
+  } else if (KIND == kRods) {  // (F, T) out: the signed columns of the incidences, streamed (assemble.cu)
     double f[6] = {0, 0, 0, 0, 0, 0};
     rods_gather_lane<LPB, MODE == kProj>(e0, e1, k, alpha, inc, a, astride, st_old, st_new,
                                          reinterpret_cast<const double2*>(icol4), f);
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kT) gather_kernel(
       tz += __shfl_xor_sync(0xffffffffu, tz, o);
     }
   }
-  if (KIND == kRods && OUT == kOutRodU && SC_RODS_HSPLIT) {
+  if (KIND == kRods && OUT == kOutRodU) {
     // the body's (U, W) from its lane 0 to every lane, then each lane writes the half rate
     // h_e = (signed column of e) . (U, W) of its incidences: D_l^T (U, W) = h_{e_i(l)} + h_{e_j(l)}
     // (the D^T pass reads 2 x 8 B per constraint instead of the columns and 2 body velocities)
@@ -174,7 +174,6 @@ __global__ void __launch_bounds__(kT) gather_kernel(
   if (k != 0 || b >= nout) return;
   if (!real) {  // padded source rows: zero force
     if (OUT == kOutF4) out4[b] = make_double4(0, 0, 0, 0);
-    if (OUT == kOutRodU) rods_store_uw(out4, b, make_double4(0, 0, 0, 0), make_double4(0, 0, 0, 0));
     return;
   }
   if (OUT == kOutF4) {
@@ -182,11 +181,6 @@ __global__ void __launch_bounds__(kT) gather_kernel(
   } else if (OUT == kOutFT) {
     double* o = outFT + 6 * b;
     o[0] = fx; o[1] = fy; o[2] = fz; o[3] = tx; o[4] = ty; o[5] = tz;
-  } else {
-    const double f[6] = {fx, fy, fz, tx, ty, tz};
-    double4 U, W;
-    rods_drag(tb, mb, f, U, W);
-    rods_store_uw(out4, b, U, W);
   }
 }
 
@@ -230,13 +224,11 @@ __global__ void __launch_bounds__(kR) dt_kernel(
         const double4 z4 = make_double4(0.0, 0.0, 0.0, 0.0);
         const double4 ui = u4[i], uj = wall ? z4 : u4[j];
         v = fma(nv.z, ui.z - uj.z, fma(nv.y, ui.y - uj.y, nv.x * (ui.x - uj.x)));
-      } else if (SC_RODS_HSPLIT) {  // the two half rates of the gather (e_j = -1: a wall at rest)
+      } else {  // rods: the two half rates of the gather (e_j = -1: a wall at rest)
         const int2 ep = einc[l];
         SC_DCHECK(ep.x >= 0 && ep.x < 2 * nc && ep.y < 2 * nc);
         const double hj = ep.y >= 0 ? hinc[ep.y] : 0.0;
         v = hinc[ep.x] + hj;
-      } else {
-        v = rods_dt_value<false>(l, n, ci, cj, nrm4, rxn4, u4);
       }
     }
     if (MODE == kDtIter) {

@@ -118,25 +118,6 @@ __device__ __forceinline__ void rods_drag(const double4& t, const double4& m, co
   U = make_double4(fma(m.y, f[0], cpar * t.x), fma(m.y, f[1], cpar * t.y), fma(m.y, f[2], cpar * t.z), 0.0);
   W = make_double4(m.z * f[3], m.z * f[4], m.z * f[5], 0.0);
 }
-// Rods, D_l^T (U, W) for constraint l (Step 10 without q): n.(U_i - U_j) + (r_i x n).W_i
-// - (r_j x n).W_j; a wall (j >= n) is at rest.
-template <bool CG>
-__device__ __forceinline__ double rods_dt_value(int64_t l, int64_t n, const int32_t* __restrict__ ci,
-                                                const int32_t* __restrict__ cj, const double4* __restrict__ nrm4,
-                                                const double4* __restrict__ rxn4, const double4* u4) {
-  const int32_t i = ci[l], j = cj[l];
-  SC_DCHECK(i >= 0 && i < n && j > i && j < n + SC_MAX_WALLS);
-  const bool wall = j >= n;
-  const double4 nv = nrm4[l];
-  double4 ui, wi, uj = make_double4(0.0, 0.0, 0.0, 0.0), wj = uj;
-  rods_load_uw<CG>(u4, i, ui, wi);
-  if (!wall) rods_load_uw<CG>(u4, j, uj, wj);
-  const double4 ra = rxn4[2 * l], rb = rxn4[2 * l + 1];
-  double v = fma(nv.z, ui.z - uj.z, fma(nv.y, ui.y - uj.y, nv.x * (ui.x - uj.x)));
-  v += fma(ra.z, wi.z, fma(ra.y, wi.y, ra.x * wi.x)) - fma(rb.z, wj.z, fma(rb.y, wj.y, rb.x * wj.x));
-  return v;
-}
-
 // Step 10 (g = D^T U + q, written) and the partial sums of Steps 11, 14-15 for constraint l:
 // s.s, s.y, y.y, min(gamma, g)^2 with s = gamma_new - gamma_old, y = g - g_old.  The BBPGD state
 // is packed per constraint, st = (gamma_l, g_l) (one 16-B access in the gathers).
