@@ -404,7 +404,7 @@ constexpr size_t kRpySmem = 4 * kRpyTile * sizeof(double4) + 2 * sizeof(uint64_t
 // SI == SJ: forward contributions only (every ordered pair of the super-block once).
 // Near pairs (r < 2 abar) and the self pair are NOT tested in the loop: r^2 is clamped on its
 // high word (one integer max, rpy_common.cuh) so they get a bounded far-formula value, which
-// the combine swaps for the overlap branch (tools/sym_tune.cu: 82.9% vs 81.3% of the FP64
+// the combine swaps for the overlap branch (round-1 tuning harness: 82.9% vs 81.3% of the FP64
 // peak for the compare + select form).
 //
 // Output: part[slot][row][3] with slot = the partner super-block: rows of SI get slot SJ
