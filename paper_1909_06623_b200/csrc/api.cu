@@ -535,6 +535,7 @@ static int create_common(sc_ctx** out, int device, void* stream) {
   if (const char* v = std::getenv("SC_BATCH")) ctx->batch_override = std::atoi(v);
   if (const char* v = std::getenv("SC_NO_GRAPHS")) ctx->use_graphs = std::atoi(v) == 0;
   if (const char* v = std::getenv("SC_NO_PERSIST")) ctx->use_persist = std::atoi(v) == 0;
+  if (const char* v = std::getenv("SC_PERSIST_GRID")) ctx->persist_grid_cap = std::atoi(v);
   *ctx->herr = 0;
   *out = ctx;
   return SC_OK;

@@ -236,8 +236,9 @@ int persist_init_device(sc_ctx* ctx) {
 
 // Steps 7-16 of Alg. 1 in one cooperative launch (the scalars in ctx->dsc after Step 6).
 int bbpgd_persistent(sc_ctx* ctx, double mu) {
-  const int grid = ctx->persist_grid;
+  int grid = ctx->persist_grid;
   if (grid <= 0) return fail(ctx, SC_ECUDA, "persistent BBPGD kernel cannot be resident");
+  if (ctx->persist_grid_cap > 0 && ctx->persist_grid_cap < grid) grid = ctx->persist_grid_cap;
   PersistArgs a;
   a.n = ctx->n;
   a.npad = ctx->npad;

@@ -154,7 +154,8 @@ struct sc_ctx {
   int batch_override = 0;       // tuning: iterations enqueued between host reads (env SC_BATCH)
   bool use_graphs = true;       // CUDA-graph replay of small-problem iteration batches (env SC_NO_GRAPHS=1: off)
   int sym_variant = 0;          // tuning: (warps, targets/lane) of the symmetric kernel (env SC_SYM_VARIANT)
-  int sym_hs = 0;               // tuning: source parts per super-block pair (env SC_SYM_HS; 0 = cost model)
+  int sym_hs = 0;
+  int persist_grid_cap = 0;     // tuning: CTAs of the persistent loop (env SC_PERSIST_GRID; 0 = one per SM)               // tuning: source parts per super-block pair (env SC_SYM_HS; 0 = cost model)
   int64_t sym_nsb = -1;         // super-blocks the pair tables were built for
   int sym_world = -1;           // ... and the number of ranks
   sc::DBuf<int2> sym_pairs;     // (SI, SJ) of every rank, concatenated (cyclic-half assignment)
