@@ -46,7 +46,7 @@ enum GatherOut { kOutF4 = 0, kOutRodU = 1, kOutFT = 2 };
 template <int KIND, int MODE, int OUT, int LPB>
 __global__ void __launch_bounds__(kT) gather_kernel(
     const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ inc, const double4* __restrict__ icol4,
-    const double4* __restrict__ nrm4, const double4* __restrict__ rxn4, const double* __restrict__ a, int astride,
+    const double* __restrict__ a, int astride,
     const double2* __restrict__ st_old, double2* __restrict__ st_new, const DevScalars* __restrict__ dsc, int64_t n,
     int64_t nout,
     const double4* __restrict__ dir4, const double4* __restrict__ mob4, double4* __restrict__ out4,
@@ -201,9 +201,8 @@ enum DtMode { kDtIter = 0, kDtAlpha0 = 1, kDtG0 = 2, kDtInitQ = 3, kDtGrad = 4, 
 template <int KIND, int MODE, bool FUSE>
 __global__ void __launch_bounds__(kR) dt_kernel(
     const int32_t* __restrict__ first_ptr, int64_t n, int64_t nc, int64_t c0, const int32_t* __restrict__ ci,
-    const int32_t* __restrict__ cj, const double4* __restrict__ nrm4, const double4* __restrict__ rxn4,
-    const double4* __restrict__ u4, const double* __restrict__ q, const double* __restrict__ gam_new,
-    double* __restrict__ g_out, double2* __restrict__ st_old, double2* __restrict__ st_new,
+    const int32_t* __restrict__ cj, const double4* __restrict__ nrm4, const double4* __restrict__ u4,
+    const double* __restrict__ q, const double* __restrict__ gam_new, double* __restrict__ g_out, double2* __restrict__ st_old, double2* __restrict__ st_new,
     double* __restrict__ part, const int32_t* __restrict__ done, int64_t nchunks, DevScalars* __restrict__ sc,
     unsigned int* __restrict__ counter, const int2* __restrict__ einc, const double* __restrict__ hinc) {
   if (done != nullptr && *done) return;
@@ -440,11 +439,11 @@ int launch_gather_proj(sc_ctx* ctx, int pp, double mu) {
   timer_begin(ctx, SC_K_GATHER);
   if (ctx->kind == kSpheres)
     gather_kernel<kSpheres, kProj, kOutF4, kLpbS><<<nblk(ctx->npad * kLpbS), kT, 0, ctx->stream>>>(
-        ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, nullptr, 1, so, sn, ctx->dsc, ctx->n,
+        ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, nullptr, 1, so, sn, ctx->dsc, ctx->n,
         ctx->npad, nullptr, nullptr, ctx->f4.p, nullptr, done, ctx->nc, nullptr);
   else
     gather_kernel<kRods, kProj, kOutRodU, kLpbR><<<nblk(ctx->npad * kLpbR), kT, 0, ctx->stream>>>(
-        ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, nullptr, 1, so, sn, ctx->dsc, ctx->n,
+        ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, nullptr, 1, so, sn, ctx->dsc, ctx->n,
         ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done, ctx->nc, ctx->hinc.p);
   timer_end(ctx, SC_K_GATHER);
   return check_launch(ctx, "gather_proj");
@@ -457,21 +456,21 @@ int launch_gather_raw(sc_ctx* ctx, const double* v, int vstride, double mu, doub
   if (FT_user != nullptr) {
     if (ctx->kind == kSpheres)
       gather_kernel<kSpheres, kRaw, kOutFT, kLpbS><<<nblk(ctx->n * kLpbS), kT, 0, ctx->stream>>>(
-          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, vstride, nullptr, nullptr, ctx->dsc,
+          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, v, vstride, nullptr, nullptr, ctx->dsc,
           ctx->n, ctx->n, nullptr, nullptr, nullptr, FT_user, nullptr, ctx->nc, nullptr);
     else
       gather_kernel<kRods, kRaw, kOutFT, kLpbR><<<nblk(ctx->n * kLpbR), kT, 0, ctx->stream>>>(
-          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, vstride, nullptr, nullptr, ctx->dsc,
+          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, v, vstride, nullptr, nullptr, ctx->dsc,
           ctx->n, ctx->n, nullptr, nullptr, nullptr, FT_user, nullptr, ctx->nc, nullptr);
   } else {
     const int32_t* done = gated ? &ctx->dsc->done : nullptr;
     if (ctx->kind == kSpheres)
       gather_kernel<kSpheres, kRaw, kOutF4, kLpbS><<<nblk(ctx->npad * kLpbS), kT, 0, ctx->stream>>>(
-          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, vstride, nullptr, nullptr, ctx->dsc,
+          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, v, vstride, nullptr, nullptr, ctx->dsc,
           ctx->n, ctx->npad, nullptr, nullptr, ctx->f4.p, nullptr, done, ctx->nc, nullptr);
     else
       gather_kernel<kRods, kRaw, kOutRodU, kLpbR><<<nblk(ctx->npad * kLpbR), kT, 0, ctx->stream>>>(
-          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, ctx->nrm4.p, ctx->rxn4.p, v, vstride, nullptr, nullptr, ctx->dsc,
+          ctx->row_ptr.p, ctx->inc.p, ctx->icol4.p, v, vstride, nullptr, nullptr, ctx->dsc,
           ctx->n, ctx->npad, ctx->dir4.p, ctx->rodmob4.p, ctx->u4.p, nullptr, done, ctx->nc, ctx->hinc.p);
   }
   timer_end(ctx, SC_K_GATHER);
@@ -519,12 +518,12 @@ int launch_dt(sc_ctx* ctx, int mode, int pp, const double* x, double* g_out, int
   do {                                                                                                          \
     if (fuse)                                                                                                   \
       dt_kernel<KIND, MODE, true><<<grid, kR, 0, ctx->stream>>>(fp, ctx->n, ctx->nc, c0, ctx->ci.p, ctx->cj.p,    \
-                                                                ctx->nrm4.p, ctx->rxn4.p, u4, q, x, g_out, so, sn, \
+                                                                ctx->nrm4.p, u4, q, x, g_out, so, sn, \
                                                                 part, done, ctx->nchunks, ctx->dsc, ctx->dcount,   \
                                                                 ctx->einc.p, ctx->hinc.p);                         \
     else                                                                                                        \
       dt_kernel<KIND, MODE, false><<<grid, kR, 0, ctx->stream>>>(fp, ctx->n, ctx->nc, c0, ctx->ci.p, ctx->cj.p,   \
-                                                                 ctx->nrm4.p, ctx->rxn4.p, u4, q, x, g_out, so,   \
+                                                                 ctx->nrm4.p, u4, q, x, g_out, so,   \
                                                                  sn, part, done, ctx->nchunks, ctx->dsc,          \
                                                                  ctx->dcount, ctx->einc.p, ctx->hinc.p);          \
   } while (0)
