@@ -176,7 +176,7 @@ int sc_set_mobility_model(sc_ctx* ctx, int model);
  * apply falls with the order (measured rel. L2 errors); every sum is in a
  * fixed order (deterministic).  Mono- or polydisperse spheres (polydisperse: the far branch is split
  * into radius-free kernels of the densities F, (a/2) F, (a/2)^2 F, reading A29) on a 1-GPU context
- * (SC_EINVAL for rods); used
+ * (rods keep their drag mobility under every model); used
  * by sc_mobility_apply, sc_lcp_q's U_ext and every BBPGD MVOP.  leaf_level 0 = chosen from N and the
  * order (leaf side >= 2a).  Errors: SC_EINVAL (order not 4/6/8, leaf_level outside 0..8). */
 int sc_set_fmm_params(sc_ctx* ctx, int order, int leaf_level);
