@@ -178,7 +178,8 @@ int sc_set_mobility_model(sc_ctx* ctx, int model);
  * into radius-free kernels of the densities F, (a/2) F, (a/2)^2 F, reading A29) on a 1-GPU context
  * (rods keep their drag mobility under every model); used
  * by sc_mobility_apply, sc_lcp_q's U_ext and every BBPGD MVOP.  leaf_level 0 = chosen from N and the
- * order (leaf side >= 2a).  Errors: SC_EINVAL (order not 4/6/8, leaf_level outside 0..8). */
+ * order (leaf side >= 2 a_max).  Errors: SC_EINVAL (order not 4/6/8, leaf_level outside 0..8; model 2 on
+ * a multi-GPU context, at the first apply). */
 int sc_set_fmm_params(sc_ctx* ctx, int order, int leaf_level);
 /* out3 = {order, leaf level of the current tree (0: not built yet), tree built (0/1)} */
 int sc_get_fmm_info(const sc_ctx* ctx, int32_t* out3);
