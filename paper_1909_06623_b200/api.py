@@ -178,6 +178,13 @@ class Context:
         fast RPY summation used with set_mobility_model("rpy_fmm")."""
         self._rc(self.lib.sc_set_fmm_params(self._h, int(order), int(leaf_level)))
 
+    def set_fmm_compression(self, mode=1):
+        """Compressed M2L of the fast summation (one orthonormal basis per level for its M2L
+        operators, include/stokescol.h sc_set_fmm_compression): 0 / False off, 1 / True on,
+        2 / "auto" (the default: on at orders 6 and 8)."""
+        m = 2 if mode == "auto" else int(mode)
+        self._rc(self.lib.sc_set_fmm_compression(self._h, m))
+
     def fmm_info(self) -> dict:
         out = (C.c_int32 * 3)()
         self._rc(self.lib.sc_get_fmm_info(self._h, out))

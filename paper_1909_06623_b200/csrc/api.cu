@@ -583,6 +583,9 @@ void sc_destroy(sc_ctx* ctx) {
   release(ctx->q); release(ctx->gam[0]); release(ctx->gam[1]); release(ctx->g[0]); release(ctx->g[1]);
   release(ctx->w); release(ctx->gam_user); release(ctx->uc); release(ctx->prev_key); release(ctx->prev_gam); release(ctx->chunk_part); release(ctx->chunk_red);
   release(ctx->fmm_key); release(ctx->fmm_idx0); release(ctx->fmm_sidx); release(ctx->fmm_cnt); release(ctx->fmm_lstart); release(ctx->fmm_cubtmp); release(ctx->fmm_spos4); release(ctx->fmm_sf4); release(ctx->fmm_M); release(ctx->fmm_L); release(ctx->fmm_lev_off_dev);
+  release(ctx->fmm_svd_U); release(ctx->fmm_svd_C); release(ctx->fmm_Mc); release(ctx->fmm_Lc); release(ctx->fmm_svd_work);
+  release(ctx->fmm_svd_li); release(ctx->fmm_svd_ptrs);
+  fmm_destroy_handles(ctx);
   release(ctx->sym_pairs); release(ctx->sym_acc); release(ctx->fx_scale); release(ctx->trace); release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);
   release(ctx->bbox_part); release(ctx->cell_of); release(ctx->cell_cnt); release(ctx->cell_start);
   release(ctx->sorted_idx); release(ctx->pair_cnt); release(ctx->pair_off); release(ctx->scan_tmp);
@@ -657,6 +660,14 @@ int sc_set_fmm_params(sc_ctx* ctx, int order, int leaf_level) {
   ctx->fmm_order = order;
   ctx->fmm_leaf_level = leaf_level;
   ctx->fmm_ready = false;
+  return SC_OK;
+}
+
+int sc_set_fmm_compression(sc_ctx* ctx, int mode) {
+  if (ctx == nullptr) return SC_EINVAL;
+  if (mode < 0 || mode > 2) return fail(ctx, SC_EINVAL, "set_fmm_compression: 0 (off), 1 (on) or 2 (auto)");
+  ctx->fmm_compress = mode;
+  ctx->fmm_ready = false;  // (the root side follows the mode)
   return SC_OK;
 }
 
@@ -1092,7 +1103,9 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
       if (int rc = bbpgd_persistent(ctx, mu)) return rc;
       if (int rc = read_scalars(ctx)) return rc;
     }
-    if (!persist && !dist && !ctx->timer.enabled && ctx->use_graphs && opts->max_iter > 0) {
+    // (the compressed fast summation calls cuBLAS: host-enqueued iterations, no graph capture)
+    const bool lib_calls = spheres && ctx->mobility_model == 2 && fmm_uses_library_calls(ctx);
+    if (!persist && !dist && !ctx->timer.enabled && ctx->use_graphs && opts->max_iter > 0 && !lib_calls) {
       cudaGraph_t graph = nullptr;
       SC_CUDA(cudaGraphCreate(&graph, 0));
       cudaGraphConditionalHandle cond;

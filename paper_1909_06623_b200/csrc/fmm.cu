@@ -19,11 +19,14 @@
 // xbar_k = cos((2k+1) pi / (2n)); IL(T) = the children of the parent's neighbours that are not
 // adjacent to T (at most 189).  Every sum is in a fixed order (deterministic).  Polydisperse radii:
 // the far branch is split into radius-free kernels (m2l_poly_kernel), 9 node components instead of 3.
+#include <cublas_v2.h>
 #include <cub/device/device_radix_sort.cuh>
+#include <cusolverDn.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "rpy_common.cuh"
@@ -51,6 +54,12 @@ struct Geom {
 };
 
 __host__ __device__ inline int64_t nbox(int l) { return int64_t(1) << (3 * l); }
+
+// compressed M2L for this context: mode 1 (on), or mode 2 (auto, the default) at orders 6 and 8;
+// monodisperse only (the polydisperse far field keeps the direct M2L)
+inline bool fmm_use_svd(const sc_ctx* ctx) {
+  return !ctx->poly && (ctx->fmm_compress == 1 || (ctx->fmm_compress == 2 && ctx->fmm_order >= 6));
+}
 
 // 1-D interpolation weights w[k] = S_n(xbar_k, u), u in [-1, 1]
 template <int NN>
@@ -398,6 +407,156 @@ __global__ void m2l_poly_kernel(Geom g, const int64_t* __restrict__ lev_off, con
   }
 }
 
+// ---- compressed M2L (sc_set_fmm_compression; monodisperse) ---------------------------------
+// Offsets o of a source box relative to its target box at one level: o in [-3, 3]^3 with
+// max |o_d| >= 2 (316 of the 7^3 grid; index oi = ((oz+3) 7 + oy+3) 7 + ox+3).  K_o is the
+// 3n^3 x 3n^3 matrix of the RPY far branch (8 pi mu hoisted) between the target nodes w xi_m and
+// the source nodes 2 w o + w xi_n, row (m, alpha) = 3m + alpha, column (n, beta) = 3n + beta --
+// the layout of one box's node strengths / local expansion in M and L.
+constexpr int kOffGrid = 343, kOffCount = 316;
+
+// K for q offsets (oi list), column-major with leading dimension R = 3 n^3:
+// K[(c R + col) R + row], c = 0..q-1.
+template <int NN>
+__global__ void svd_build_k_kernel(double* __restrict__ K, const int32_t* __restrict__ ois, int q, double w,
+                                   double a2) {
+  constexpr int NB = NN * NN * NN, R = 3 * NB;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<int64_t>(R) * R * q) return;
+  const int row = static_cast<int>(t % R);
+  const int64_t cc = t / R;  // c R + col
+  const int col = static_cast<int>(cc % R), c = static_cast<int>(cc / R);
+  const int oi = ois[c];
+  const int ox = oi % 7 - 3, oy = (oi / 7) % 7 - 3, oz = oi / 49 - 3;
+  const int m = row / 3, al = row % 3, nn = col / 3, be = col % 3;
+  const int mx = m % NN, my = (m / NN) % NN, mz = m / (NN * NN);
+  const int nx = nn % NN, ny = (nn / NN) % NN, nz = nn / (NN * NN);
+  const double d[3] = {w * (2.0 * ox + c_xbar[nx] - c_xbar[mx]), w * (2.0 * oy + c_xbar[ny] - c_xbar[my]),
+                       w * (2.0 * oz + c_xbar[nz] - c_xbar[mz])};
+  const double r2 = fma(d[2], d[2], fma(d[1], d[1], d[0] * d[0]));
+  const double y = 1.0 / sqrt(r2), h = y * y, e = y * h;
+  const double c1 = fma(2.0 / 3.0 * a2, e, y);
+  const double c2 = e * fma(-2.0 * a2, h, 1.0);
+  K[t] = (al == be ? c1 : 0.0) + c2 * d[al] * d[be];
+}
+
+// L^c_T = sum_{o in IL(T)} C_o M^c_{T+o} at one level as one GEMM per parity class.  Boxes
+// T = 2P + p of class p (parent P in [0, Dp)^3) see the offsets o_d in [-2 - p_d, 3 - p_d], not
+// all |o_d| <= 1; the source S = T + o has class p' = (p + o) mod 2 and parent P + delta,
+// delta = floor((p + o) / 2) in {-1, 0, 1}^3.  With every class's M^c stored over its parents
+// padded by one zero parent on each side ((Dp+2)^3 columns of k values: McP), the sources of all
+// targets of a class for one o are the target columns shifted by the constant delta_lin -- so the
+// class's L^c is a plain GEMM [k x k] x [k x columns] accumulated over its 189 offsets (K dimension
+// 189 k), computed here by a register-tiled FP64 kernel (64 x 64 tile, 4 x 4 per thread, K steps
+// of 16 through shared memory).  Columns = the span of interior parents in the padded numbering;
+// halo columns are computed and dropped.  Fixed order over o and k -> deterministic.
+constexpr int kGbm = 64, kGbn = 64, kGbk = 16;
+__global__ void __launch_bounds__(256) m2l_svd_gemm_kernel(int Dp, int k, const double* __restrict__ Cops,
+                                                           const int32_t* __restrict__ li_of_oi,
+                                                           const double* __restrict__ McP,
+                                                           double* __restrict__ LcP, const int32_t* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  __shared__ double sA[kGbk][kGbm];
+  __shared__ double sB[kGbk][kGbn];
+  const int pc = static_cast<int>(blockIdx.z);
+  const int pxb = pc & 1, pyb = (pc >> 1) & 1, pzb = pc >> 2;
+  const int Dq = Dp + 2;
+  const int64_t npad = static_cast<int64_t>(Dq) * Dq * Dq;
+  const int64_t cbeg = (static_cast<int64_t>(1) * Dq + 1) * Dq + 1;  // parent (1,1,1)
+  const int64_t cend = (static_cast<int64_t>(Dp) * Dq + Dp) * Dq + Dp + 1;
+  const int64_t col0 = cbeg + static_cast<int64_t>(blockIdx.x) * kGbn;
+  const int row0 = static_cast<int>(blockIdx.y) * kGbm;
+  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int oz = -2 - pzb; oz <= 3 - pzb; ++oz)
+    for (int oy = -2 - pyb; oy <= 3 - pyb; ++oy)
+      for (int ox = -2 - pxb; ox <= 3 - pxb; ++ox) {
+        if (abs(ox) <= 1 && abs(oy) <= 1 && abs(oz) <= 1) continue;
+        const int li = li_of_oi[((oz + 3) * 7 + oy + 3) * 7 + ox + 3];
+        const int qx = pxb + ox, qy = pyb + oy, qz = pzb + oz;  // in [-2, 3]
+        const int spc = (qx & 1) | ((qy & 1) << 1) | ((qz & 1) << 2);
+        const int dx = (qx - (qx & 1)) / 2, dy = (qy - (qy & 1)) / 2, dz = (qz - (qz & 1)) / 2;
+        const int64_t dl = (static_cast<int64_t>(dz) * Dq + dy) * Dq + dx;
+        const double* A = Cops + static_cast<int64_t>(li) * k * k;
+        const double* B = McP + static_cast<int64_t>(spc) * npad * k;
+        for (int j0 = 0; j0 < k; j0 += kGbk) {
+          __syncthreads();
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {  // A tile: (row, j) = C[j k + row], row fastest
+            const int e = tid + t * 256;
+            const int r = e % kGbm, jj = e / kGbm;
+            const int gr = row0 + r, gj = j0 + jj;
+            sA[jj][r] = (gr < k && gj < k) ? __ldg(A + static_cast<int64_t>(gj) * k + gr) : 0.0;
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {  // B tile: (j, col) = McP[(col + dl) k + j], j fastest
+            const int e = tid + t * 256;
+            const int jj = e % kGbk, c = e / kGbk;
+            const int gj = j0 + jj;
+            const int64_t gc = col0 + c;
+            sB[jj][c] = (gj < k && gc < cend) ? __ldg(B + (gc + dl) * k + gj) : 0.0;
+          }
+          __syncthreads();
+#pragma unroll
+          for (int jj = 0; jj < kGbk; ++jj) {
+            double a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              a[u] = sA[jj][tr * 4 + u];
+              b[u] = sB[jj][tc * 4 + u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+          }
+        }
+      }
+  // interior columns only
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int64_t gc = col0 + tc * 4 + v;
+    if (gc >= cend) continue;
+    const int px = static_cast<int>(gc % Dq), py = static_cast<int>((gc / Dq) % Dq), pz = static_cast<int>(gc / Dq / Dq);
+    if (px < 1 || py < 1 || pz < 1 || px > Dp || py > Dp || pz > Dp) continue;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = row0 + tr * 4 + u;
+      if (r < k) LcP[(static_cast<int64_t>(pc) * npad + gc) * k + r] = acc[u][v];
+    }
+  }
+}
+
+// natural box order (k x nbox, box T = (z D + y) D + x) <-> class-padded order (McP layout)
+__global__ void svd_to_classes_kernel(int D, int k, const double* __restrict__ src, double* __restrict__ dst) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nb = static_cast<int64_t>(D) * D * D;
+  if (t >= nb * k) return;
+  const int j = static_cast<int>(t % k);
+  const int64_t T = t / k;
+  const int x = static_cast<int>(T % D), y = static_cast<int>((T / D) % D), z = static_cast<int>(T / D / D);
+  const int Dp = D / 2, Dq = Dp + 2;
+  const int pc = (x & 1) | ((y & 1) << 1) | ((z & 1) << 2);
+  const int64_t col = ((static_cast<int64_t>(z / 2 + 1)) * Dq + (y / 2 + 1)) * Dq + (x / 2 + 1);
+  dst[(static_cast<int64_t>(pc) * Dq * Dq * Dq + col) * k + j] = src[T * k + j];
+}
+__global__ void svd_from_classes_kernel(int D, int k, const double* __restrict__ src, double* __restrict__ dst) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nb = static_cast<int64_t>(D) * D * D;
+  if (t >= nb * k) return;
+  const int j = static_cast<int>(t % k);
+  const int64_t T = t / k;
+  const int x = static_cast<int>(T % D), y = static_cast<int>((T / D) % D), z = static_cast<int>(T / D / D);
+  const int Dp = D / 2, Dq = Dp + 2;
+  const int pc = (x & 1) | ((y & 1) << 1) | ((z & 1) << 2);
+  const int64_t col = ((static_cast<int64_t>(z / 2 + 1)) * Dq + (y / 2 + 1)) * Dq + (x / 2 + 1);
+  dst[T * k + j] = src[(static_cast<int64_t>(pc) * Dq * Dq * Dq + col) * k + j];
+}
+
 // L2P + P2P: one CTA per leaf; thread = target body (chunks of blockDim); sources of the 27
 // neighbouring leaves through shared memory (exact RPY incl. the overlap branch and the self term).
 // POLY: the leaf's 9-component local expansion (m2l_poly_kernel) and the pair radius w_i + w_j.
@@ -521,6 +680,224 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
   }
 }
 
+#define SC_CUBLAS(call)                                                                  \
+  do {                                                                                   \
+    cublasStatus_t s_ = (call);                                                          \
+    if (s_ != CUBLAS_STATUS_SUCCESS) return fail(ctx, SC_ECUDA, std::string(#call) + " failed"); \
+  } while (0)
+#define SC_CUSOLVER(call)                                                                \
+  do {                                                                                   \
+    cusolverStatus_t s_ = (call);                                                        \
+    if (s_ != CUSOLVER_STATUS_SUCCESS) return fail(ctx, SC_ECUDA, std::string(#call) + " failed"); \
+  } while (0)
+
+int svd_handles(sc_ctx* ctx) {
+  if (ctx->cublas == nullptr) {
+    cublasHandle_t h = nullptr;
+    SC_CUBLAS(cublasCreate(&h));
+    ctx->cublas = h;
+  }
+  if (ctx->cusolver == nullptr) {
+    cusolverDnHandle_t h = nullptr;
+    SC_CUSOLVER(cusolverDnCreate(&h));
+    ctx->cusolver = h;
+  }
+  SC_CUBLAS(cublasSetStream(static_cast<cublasHandle_t>(ctx->cublas), ctx->stream));
+  SC_CUSOLVER(cusolverDnSetStream(static_cast<cusolverDnHandle_t>(ctx->cusolver), ctx->stream));
+  return 0;
+}
+
+// Bases and compressed operators of every level for the current tree (cached by geometry key).
+template <int NN>
+int fmm_svd_prepare(sc_ctx* ctx, const Geom& g) {
+  double escale = 1.0;
+  if (const char* v = std::getenv("SC_FMM_SVD_EPS_SCALE")) escale = std::atof(v);
+  const double key[5] = {g.H, static_cast<double>(g.L), static_cast<double>(NN), g.a, escale};
+  bool same = true;
+  for (int i = 0; i < 5; ++i) same = same && ctx->fmm_svd_key[i] == key[i];
+  if (same) return 0;
+  if (int rc = svd_handles(ctx)) return rc;
+  cublasHandle_t cb = static_cast<cublasHandle_t>(ctx->cublas);
+  cusolverDnHandle_t cs = static_cast<cusolverDnHandle_t>(ctx->cusolver);
+  constexpr int NB = NN * NN * NN, R = 3 * NB;
+  // kept singular directions: sigma >= eps sigma_max
+  double eps = NN == 4 ? 6e-5 : (NN == 6 ? 1.8e-6 : 9e-8);  // 3% of the order's stated error bar
+  if (const char* v = std::getenv("SC_FMM_SVD_EPS_SCALE")) eps *= std::atof(v);  // (tuning)
+  const int L = g.L;
+  std::vector<int32_t> tab(kOffGrid + kOffCount, -1);  // [li_of_oi (343) | oi of li (316)]
+  int nl = 0;
+  for (int oi = 0; oi < kOffGrid; ++oi) {
+    const int ox = oi % 7 - 3, oy = (oi / 7) % 7 - 3, oz = oi / 49 - 3;
+    if (std::abs(ox) <= 1 && std::abs(oy) <= 1 && std::abs(oz) <= 1) continue;
+    tab[oi] = nl;
+    tab[kOffGrid + nl] = oi;
+    ++nl;
+  }
+  if (nl != kOffCount) return fail(ctx, SC_EINVAL, "fmm compression: offset table");
+  ctx->fmm_svd_lih.assign(tab.begin(), tab.begin() + kOffGrid);
+  if (int rc = ensure(ctx, ctx->fmm_svd_li, tab.size())) return rc;
+  SC_CUDA(cudaMemcpyAsync(ctx->fmm_svd_li.p, tab.data(), sizeof(int32_t) * tab.size(), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  const int32_t* ois = ctx->fmm_svd_li.p + kOffGrid;
+  const int Q = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kOffCount, (int64_t(256) << 20) /
+                                                                                        (int64_t(R) * R * 8))));
+  int lwork = 0;
+  SC_CUSOLVER(cusolverDnDsyevd_bufferSize(cs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, R, nullptr, R,
+                                          nullptr, &lwork));
+  // work: K chunk (Q R R) | G (R R) | eigenvalues (R) | syevd work (lwork) | info | eigvecs per level
+  const size_t nK = size_t(Q) * R * R, nG = size_t(R) * R;
+  const size_t nwork = nK + nG + R + size_t(lwork) + 2 + size_t(L + 1) * R * R;
+  if (int rc = ensure(ctx, ctx->fmm_svd_work, nwork)) return rc;
+  double* K = ctx->fmm_svd_work.p;
+  double* G = K + nK;
+  double* W = G + nG;
+  double* wk = W + R;
+  int* info = reinterpret_cast<int*>(wk + lwork);
+  double* Uall = wk + lwork + 2;  // level l: R x R eigenvectors at Uall + l R R
+  const double one = 1.0, zero = 0.0;
+  const unsigned kb = 256;
+  ctx->fmm_svd_k.assign(L + 1, 0);
+  std::vector<double> hW(R);
+  for (int l = 2; l <= L; ++l) {
+    const double w = g.H / static_cast<double>(int64_t(1) << (l + 1));
+    SC_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * nG, ctx->stream));
+    for (int c0 = 0; c0 < kOffCount; c0 += Q) {
+      const int q = std::min(Q, kOffCount - c0);
+      const int64_t tot = int64_t(R) * R * q;
+      svd_build_k_kernel<NN><<<static_cast<unsigned>((tot + kb - 1) / kb), kb, 0, ctx->stream>>>(K, ois + c0, q, w,
+                                                                                               g.a * g.a);
+      if (int rc = check_launch(ctx, "fmm_svd_build_k")) return rc;
+      SC_CUBLAS(cublasDsyrk(cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, R, R * q, &one, K, R, &one, G, R));
+    }
+    SC_CUSOLVER(cusolverDnDsyevd(cs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, R, G, R, W, wk, lwork, info));
+    SC_CUDA(cudaMemcpyAsync(hW.data(), W, sizeof(double) * R, cudaMemcpyDeviceToHost, ctx->stream));
+    int hinfo = 0;
+    SC_CUDA(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SC_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hinfo != 0) return fail(ctx, SC_ECUDA, "fmm compression: eigensolver did not converge");
+    const double lmax = hW[R - 1];  // ascending; G = sum K K^T: lambda = sigma^2
+    int k = 0;
+    for (int i = R - 1; i >= 0 && hW[i] >= eps * eps * lmax; --i) ++k;
+    k = std::max(1, k);
+    ctx->fmm_svd_k[l] = k;
+    SC_CUDA(cudaMemcpyAsync(Uall + size_t(l) * R * R, G + size_t(R - k) * R, sizeof(double) * R * k,
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  // U_l and C_l (316 k_l x k_l, column-major, operator index li) into their buffers
+  ctx->fmm_svd_uoff.assign(L + 2, 0);
+  ctx->fmm_svd_coff.assign(L + 2, 0);
+  int64_t nu = 0, ncop = 0, kmax = 1;
+  for (int l = 2; l <= L; ++l) {
+    ctx->fmm_svd_uoff[l] = nu;
+    ctx->fmm_svd_coff[l] = ncop;
+    nu += int64_t(R) * ctx->fmm_svd_k[l];
+    ncop += int64_t(kOffCount) * ctx->fmm_svd_k[l] * ctx->fmm_svd_k[l];
+    kmax = std::max<int64_t>(kmax, ctx->fmm_svd_k[l]);
+  }
+  if (int rc = ensure(ctx, ctx->fmm_svd_U, nu)) return rc;
+  if (int rc = ensure(ctx, ctx->fmm_svd_C, ncop)) return rc;
+  // T1 = K_o U reuses G's and the K chunk's space when it fits, else a fresh chunk size
+  const int Q2 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(Q, int64_t(nG) / (int64_t(R) * kmax))));
+  for (int l = 2; l <= L; ++l) {
+    const int k = ctx->fmm_svd_k[l];
+    const double w = g.H / static_cast<double>(int64_t(1) << (l + 1));
+    double* U = ctx->fmm_svd_U.p + ctx->fmm_svd_uoff[l];
+    SC_CUDA(cudaMemcpyAsync(U, Uall + size_t(l) * R * R, sizeof(double) * R * k, cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    double* Cl = ctx->fmm_svd_C.p + ctx->fmm_svd_coff[l];
+    for (int c0 = 0; c0 < kOffCount; c0 += Q2) {
+      const int q = std::min(Q2, kOffCount - c0);
+      const int64_t tot = int64_t(R) * R * q;
+      svd_build_k_kernel<NN><<<static_cast<unsigned>((tot + kb - 1) / kb), kb, 0, ctx->stream>>>(K, ois + c0, q, w,
+                                                                                               g.a * g.a);
+      if (int rc = check_launch(ctx, "fmm_svd_build_k")) return rc;
+      // T1_c = K_c U (R x k) into G's space; C_c = U^T T1_c (k x k)
+      SC_CUBLAS(cublasDgemmStridedBatched(cb, CUBLAS_OP_N, CUBLAS_OP_N, R, k, R, &one, K, R, int64_t(R) * R, U, R,
+                                          0, &zero, G, R, int64_t(R) * k, q));
+      SC_CUBLAS(cublasDgemmStridedBatched(cb, CUBLAS_OP_T, CUBLAS_OP_N, k, k, R, &one, U, R, 0, G, R,
+                                          int64_t(R) * k, &zero, Cl + int64_t(c0) * k * k, k, int64_t(k) * k, q));
+    }
+  }
+  SC_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < 5; ++i) ctx->fmm_svd_key[i] = key[i];
+  if (std::getenv("SC_FMM_DEBUG"))
+    for (int l = 2; l <= L; ++l) std::fprintf(stderr, "fmm svd: order %d level %d rank %d of %d\n", NN, l, ctx->fmm_svd_k[l], R);
+  return 0;
+}
+
+// The compressed M2L of every level: M^c = U^T M, L^c = sum_o C_o M^c, L = U L^c (writes L).
+template <int NN>
+int fmm_m2l_compressed(sc_ctx* ctx, const Geom& g, const double* M, double* Lx, const int32_t* done) {
+  constexpr int NB = NN * NN * NN, R = 3 * NB;
+  cublasHandle_t cb = static_cast<cublasHandle_t>(ctx->cublas);
+  SC_CUBLAS(cublasSetStream(cb, ctx->stream));
+  const std::vector<int64_t>& lo = ctx->fmm_lev_off;
+  int64_t need = 1;
+  for (int l = 2; l <= g.L; ++l) {
+    const int64_t Dq = (int64_t(1) << (l - 1)) + 2;
+    need = std::max<int64_t>(need, 8 * Dq * Dq * Dq * ctx->fmm_svd_k[l]);
+  }
+  // Mc / Lc: [natural k x nbox | class-padded 8 (Dp+2)^3 k]
+  const int64_t nat = nbox(g.L) * *std::max_element(ctx->fmm_svd_k.begin(), ctx->fmm_svd_k.end());
+  if (int rc = ensure(ctx, ctx->fmm_Mc, nat + need)) return rc;
+  if (int rc = ensure(ctx, ctx->fmm_Lc, nat + need)) return rc;
+  const double one = 1.0, zero = 0.0;
+  for (int l = 2; l <= g.L; ++l) {
+    const int k = ctx->fmm_svd_k[l];
+    const int nb = static_cast<int>(nbox(l));
+    const int D = 1 << l, Dp = D / 2, Dq = Dp + 2;
+    const int64_t npad = int64_t(Dq) * Dq * Dq;
+    const double* U = ctx->fmm_svd_U.p + ctx->fmm_svd_uoff[l];
+    double* mcn = ctx->fmm_Mc.p;
+    double* mcp = ctx->fmm_Mc.p + nat;
+    double* lcn = ctx->fmm_Lc.p;
+    double* lcp = ctx->fmm_Lc.p + nat;
+    SC_CUBLAS(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, k, nb, R, &one, U, R, M + lo[l] * R, R, &zero, mcn, k));
+    SC_CUDA(cudaMemsetAsync(mcp, 0, sizeof(double) * 8 * npad * k, ctx->stream));  // zero halo
+    const int64_t tot = int64_t(nb) * k;
+    svd_to_classes_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(D, k, mcn, mcp);
+    const int64_t cbeg = (int64_t(1) * Dq + 1) * Dq + 1, cend = (int64_t(Dp) * Dq + Dp) * Dq + Dp + 1;
+    const int ncol = static_cast<int>(cend - cbeg);
+    // 189 batched GEMMs: batch entry pc = the i-th offset of class pc (distinct outputs), the
+    // calls accumulate in offset order (beta 0, then 1) -> fixed order
+    const double* Cl = ctx->fmm_svd_C.p + ctx->fmm_svd_coff[l];
+    std::vector<const double*> hA(189 * 8), hB(189 * 8);
+    std::vector<double*> hC(189 * 8);
+    for (int pc = 0; pc < 8; ++pc) {
+      const int pxb = pc & 1, pyb = (pc >> 1) & 1, pzb = pc >> 2;
+      int i = 0;
+      for (int oz = -2 - pzb; oz <= 3 - pzb; ++oz)
+        for (int oy = -2 - pyb; oy <= 3 - pyb; ++oy)
+          for (int ox = -2 - pxb; ox <= 3 - pxb; ++ox) {
+            if (std::abs(ox) <= 1 && std::abs(oy) <= 1 && std::abs(oz) <= 1) continue;
+            const int oi = ((oz + 3) * 7 + oy + 3) * 7 + ox + 3;
+            const int qx = pxb + ox, qy = pyb + oy, qz = pzb + oz;
+            const int spc = (qx & 1) | ((qy & 1) << 1) | ((qz & 1) << 2);
+            const int64_t dl = ((int64_t((qz - (qz & 1)) / 2)) * Dq + (qy - (qy & 1)) / 2) * Dq + (qx - (qx & 1)) / 2;
+            hA[i * 8 + pc] = Cl + int64_t(ctx->fmm_svd_lih[oi]) * k * k;
+            hB[i * 8 + pc] = mcp + (int64_t(spc) * npad + cbeg + dl) * k;
+            hC[i * 8 + pc] = lcp + (int64_t(pc) * npad + cbeg) * k;
+            ++i;
+          }
+    }
+    if (int rc = ensure(ctx, ctx->fmm_svd_ptrs, 3 * 189 * 8)) return rc;
+    const double** dA = reinterpret_cast<const double**>(ctx->fmm_svd_ptrs.p);
+    const double** dB = dA + 189 * 8;
+    double** dC = reinterpret_cast<double**>(ctx->fmm_svd_ptrs.p + 2 * 189 * 8);
+    SC_CUDA(cudaMemcpyAsync(dA, hA.data(), sizeof(void*) * 189 * 8, cudaMemcpyHostToDevice, ctx->stream));
+    SC_CUDA(cudaMemcpyAsync(dB, hB.data(), sizeof(void*) * 189 * 8, cudaMemcpyHostToDevice, ctx->stream));
+    SC_CUDA(cudaMemcpyAsync(dC, hC.data(), sizeof(void*) * 189 * 8, cudaMemcpyHostToDevice, ctx->stream));
+    for (int i = 0; i < 189; ++i)
+      SC_CUBLAS(cublasDgemmBatched(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, ncol, k, &one, dA + i * 8, k, dB + i * 8, k,
+                                   i == 0 ? &zero : &one, dC + i * 8, k, 8));
+    SC_CUDA(cudaStreamSynchronize(ctx->stream));  // (the host pointer tables are reused next level)
+    svd_from_classes_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(D, k, lcp, lcn);
+    SC_CUBLAS(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, R, nb, k, &one, U, R, lcn, k, &zero, Lx + lo[l] * R, R));
+  }
+  ctx->launch_count += 5 * (g.L - 1);
+  return 0;
+}
+
 template <int NN, bool POLY>
 int fmm_launch(sc_ctx* ctx, const Geom& g, const double4* f4, double mu, double4* u4, const int32_t* done) {
   constexpr int NB = NN * NN * NN;
@@ -542,7 +919,9 @@ int fmm_launch(sc_ctx* ctx, const Geom& g, const double4* f4, double mu, double4
         l, M + lo[l] * NB * C, M + lo[l + 1] * NB * C, done);
   if (POLY)
     m2l_poly_kernel<NN><<<static_cast<unsigned>(lo[L + 1] - lo[2]), nb, 0, ctx->stream>>>(g, loff, M, Lc, done);
-  else
+  else if (fmm_use_svd(ctx)) {
+    if (int rc = fmm_m2l_compressed<NN>(ctx, g, M, Lc, done)) return rc;
+  } else
     m2l_kernel<NN><<<static_cast<unsigned>(lo[L + 1] - lo[2]), nb, 0, ctx->stream>>>(g, loff, M, Lc, done);
   for (int l = 2; l < L; ++l)
     transfer_kernel<NN, false, C><<<static_cast<unsigned>(nbox(l + 1)), nb, 0, ctx->stream>>>(
@@ -654,6 +1033,11 @@ int fmm_setup(sc_ctx* ctx) {
   // neighbouring leaves, and well-separated boxes are >= one leaf side >= 2 a_max apart
   const double a = ctx->poly ? 2.0 * hi[3] : ctx->a_const;
   ext = std::max(ext, 8.0 * a) * (1.0 + 1e-9) + 1e-9;  // (>= 4 leaves of side >= 2a per dimension)
+  if (fmm_use_svd(ctx)) {  // root side on a ladder 8a 2^(i/8): the cached M2L bases survive small
+                           // changes of the bounding box (time stepping)
+    const double i = std::ceil(8.0 * std::log2(ext / (8.0 * a)) - 1e-9);
+    ext = 8.0 * a * std::exp2(std::max(0.0, i) / 8.0);
+  }
   // leaf level: largest useful L with leaf side >= 2a (far branch between well-separated boxes,
   // every overlapping pair in neighbouring leaves), chosen to balance the P2P and M2L work
   int L = ctx->fmm_leaf_level;
@@ -665,7 +1049,11 @@ int fmm_setup(sc_ctx* ctx) {
     for (int l = 2; l <= std::min(Lmax, 7); ++l) {
       const double leaves = static_cast<double>(nbox(l));
       const double p2p = static_cast<double>(n) * 27.0 * (static_cast<double>(n) / leaves);
-      const double m2l = (ctx->poly ? 1.8 : 1.0) * 0.8 * 1.15 * leaves * 150.0 * nb3 * nb3;  // (poly: 3 fields)
+      double m2l = (ctx->poly ? 1.8 : 1.0) * 0.8 * 1.15 * leaves * 150.0 * nb3 * nb3;  // (poly: 3 fields)
+      if (fmm_use_svd(ctx)) {  // compressed: 189 k^2 FMA per box on the GEMM path, ~7.8 FMA per P2P pair
+        const double kest = nn == 4 ? 132.0 : (nn == 6 ? 286.0 : 454.0);
+        m2l = leaves * 189.0 * kest * kest / 7.8;
+      }
       const double fill = std::min(1.0, leaves * std::max(1.0, static_cast<double>(n) / leaves / 128.0) /
                                             (2.0 * std::max(ctx->num_sms, 1)));
       const double cost = (p2p + m2l) / fill;
@@ -735,11 +1123,29 @@ int fmm_setup(sc_ctx* ctx) {
   return 0;
 }
 
+bool fmm_uses_library_calls(const sc_ctx* ctx) { return fmm_use_svd(ctx); }
+
+void fmm_destroy_handles(sc_ctx* ctx) {
+  if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
+  if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
+  ctx->cublas = nullptr;
+  ctx->cusolver = nullptr;
+}
+
 int fmm_apply(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done) {
   if (!ctx->fmm_ready) {
     if (int rc = fmm_setup(ctx)) return rc;
   }
   Geom g{ctx->fmm_geom[0], ctx->fmm_geom[1], ctx->fmm_geom[2], ctx->fmm_geom[3], ctx->a_const, ctx->fmm_L_used};
+  if (fmm_use_svd(ctx)) {
+    int rc = 0;
+    switch (ctx->fmm_order) {
+      case 4: rc = fmm_svd_prepare<4>(ctx, g); break;
+      case 6: rc = fmm_svd_prepare<6>(ctx, g); break;
+      default: rc = fmm_svd_prepare<8>(ctx, g); break;
+    }
+    if (rc) return rc;
+  }
   if (ctx->fmm_poly) switch (ctx->fmm_order) {
       case 4: return fmm_launch<4, true>(ctx, g, f4, mu, u4, done);
       case 6: return fmm_launch<6, true>(ctx, g, f4, mu, u4, done);

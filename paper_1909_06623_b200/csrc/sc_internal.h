@@ -146,6 +146,18 @@ struct sc_ctx {
   sc::DBuf<double> fmm_M, fmm_L;
   std::vector<int64_t> fmm_lev_off;
   sc::DBuf<int64_t> fmm_lev_off_dev;
+  // compressed M2L (sc_set_fmm_compression): per level l the basis U_l (3n^3 x k_l) of the M2L
+  // operators and the 316 compressed operators C_o = U^T K_o U (k_l x k_l), cached for a geometry key
+  int fmm_compress = 2;           // 0 off, 1 on, 2 auto (orders 6 and 8)
+  double fmm_svd_key[5] = {};     // (root side, leaf level, order, a, valid)
+  std::vector<int> fmm_svd_k;     // k_l per level (index l)
+  std::vector<int64_t> fmm_svd_uoff, fmm_svd_coff;  // offsets of U_l, C_l in the buffers below
+  sc::DBuf<double> fmm_svd_U, fmm_svd_C, fmm_Mc, fmm_Lc, fmm_svd_work;
+  sc::DBuf<int32_t> fmm_svd_li;   // offset index (7^3 grid) -> operator index (-1: adjacent)
+  std::vector<int32_t> fmm_svd_lih;  // (host copy)
+  sc::DBuf<uint64_t> fmm_svd_ptrs;   // batched-GEMM pointer tables
+  void* cublas = nullptr;         // cublasHandle_t / cusolverDnHandle_t (fmm.cu)
+  void* cusolver = nullptr;
   sc::DBuf<double> rpy6_part;   // full RPY: nsplit * npad * 6 partials
   sc::DBuf<double> ft_tmp;      // n x 6 scratch (F_c for the full-RPY U_c)
   int nsplit = 1;
@@ -244,6 +256,8 @@ int choose_nsplit(int64_t npad, int world);
 int fmm_init_device(sc_ctx* ctx);  // interpolation tables into constant memory (sc_create)
 int fmm_setup(sc_ctx* ctx);
 int fmm_apply(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int32_t* done);
+void fmm_destroy_handles(sc_ctx* ctx);
+bool fmm_uses_library_calls(const sc_ctx* ctx);  // the compressed M2L (cuBLAS) is active
 // per-device kernel attributes (max dynamic shared memory); called by sc_create
 int rpy_init_device(sc_ctx* ctx);
 int persist_init_device(sc_ctx* ctx);
