@@ -188,9 +188,10 @@ int sc_set_fmm_params(sc_ctx* ctx, int order, int leaf_level);
  * fraction of the order's stated error; M2L becomes
  * L = U_l sum_o C_o (U_l^T M), C_o = U_l^T K_o U_l (k_l x k_l).  The bases are computed once per
  * tree geometry (root side, leaf level, order, radius) and cached; polydisperse radii keep the
- * direct M2L.  mode 0: direct M2L; mode 1: compressed at every order; mode 2 (default): compressed at
- * orders 6 and 8 (where it is faster; the root side is then rounded up to 8a 2^(i/8) so the cached
- * bases survive small changes of the bounding box).  Errors: SC_EINVAL (mode not 0/1/2). */
+ * direct M2L.  mode 0: direct M2L; mode 1: compressed at every order; mode 2 (default): compressed
+ * where it measured faster -- order 8 from N = 2^15, order 6 from N = 2^18 (the root side is then
+ * rounded up to 8a 2^(i/8) so the cached bases survive small changes of the bounding box).
+ * Errors: SC_EINVAL (mode not 0/1/2). */
 int sc_set_fmm_compression(sc_ctx* ctx, int mode);
 /* out3 = {order, leaf level of the current tree (0: not built yet), tree built (0/1)} */
 int sc_get_fmm_info(const sc_ctx* ctx, int32_t* out3);

@@ -55,10 +55,13 @@ struct Geom {
 
 __host__ __device__ inline int64_t nbox(int l) { return int64_t(1) << (3 * l); }
 
-// compressed M2L for this context: mode 1 (on), or mode 2 (auto, the default) at orders 6 and 8;
+// compressed M2L for this context: mode 1 (on), or mode 2 (auto, the default) where it measured
+// faster (profiles/r02/fmm_compressed_vs_direct.jsonl): order 8 from N = 2^15, order 6 from 2^18;
 // monodisperse only (the polydisperse far field keeps the direct M2L)
 inline bool fmm_use_svd(const sc_ctx* ctx) {
-  return !ctx->poly && (ctx->fmm_compress == 1 || (ctx->fmm_compress == 2 && ctx->fmm_order >= 6));
+  if (ctx->poly || ctx->fmm_compress == 0) return false;
+  if (ctx->fmm_compress == 1) return true;
+  return (ctx->fmm_order == 8 && ctx->n >= (int64_t(1) << 15)) || (ctx->fmm_order == 6 && ctx->n >= (int64_t(1) << 18));
 }
 
 // 1-D interpolation weights w[k] = S_n(xbar_k, u), u in [-1, 1]

@@ -253,3 +253,59 @@ def test_fmm_two_contexts_different_orders():
         assert torch.equal(ua, ref[4]) and torch.equal(ub, ref[8])
     a.close()
     b.close()
+
+
+# ------------------------------------------------ compressed M2L (sc_set_fmm_compression)
+@pytest.mark.parametrize("order", [4, 6, 8])
+@pytest.mark.parametrize("n,leaf_level", [(20000, 0), (40000, 3)])
+def test_fmm_compressed_m2l_vs_oracle(ctx, order, n, leaf_level):
+    """The compressed M2L (per-level orthonormal basis of the 316 M2L operators, rank kept at 3% of
+    the order's bar) meets the same stated bars against the oracle's direct sum, and repeated
+    applies are bitwise equal (fixed-order batched GEMMs)."""
+    p = make_problem("C5", n=n)
+    ctx.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+    ctx.set_mobility_model("rpy_fmm")
+    ctx.set_fmm_params(order, leaf_level)
+    ctx.set_fmm_compression(1)
+    try:
+        FT = np.random.default_rng(21).normal(size=(p.n, 6))
+        U = ctx.mobility_apply(_cuda(FT))
+        U2 = ctx.mobility_apply(_cuda(FT))
+    finally:
+        ctx.set_fmm_compression("auto")
+        ctx.set_mobility_model("rpy")
+    assert torch.equal(U, U2)
+    Uo = oracle.rpy_apply(p.pos, p.radius, p.mu, FT)
+    err = _relL2(U.cpu().numpy()[:, :3], Uo[:, :3])
+    assert err <= TOL[order], (order, n, err)
+
+
+def test_fmm_compressed_converged_solve_certified_by_oracle(ctx):
+    """BBPGD with the compressed order-8 operator (host-enqueued iterations: the compressed M2L calls
+    cuBLAS) converges, and the oracle's direct LCP certifies its gamma as for the direct M2L."""
+    p = make_problem("C5", n=20000, fixed_iters=0)
+    t = _cuda
+    ctx.set_mobility_model("rpy_fmm")
+    ctx.set_fmm_params(8, 0)
+    ctx.set_fmm_compression(1)
+    try:
+        ctx.build_contacts_spheres(t(p.pos), t(p.radius), p.gap_abs, p.gap_rel)
+        ctx.assemble_D()
+        ctx.lcp_q(p.dt, ctx.mobility_apply(t(p.force), mu=p.mu))
+        r = ctx.bbpgd_solve(mu=p.mu, tol=p.tol, max_iter=p.max_iter)
+    finally:
+        ctx.set_fmm_compression("auto")
+        ctx.set_mobility_model("rpy")
+    assert r["status"] == 0 and r["residual"] < p.tol
+    g = r["gamma"].cpu().numpy()
+    sysm = oracle.system_for(p)
+    F = oracle.apply_D(p.n, sysm.ct, g) + p.force
+    go = sysm.lcp_q(p.dt, sysm.mobility(F))
+    q = sysm.lcp_q(p.dt, sysm.mobility(p.force))
+    phi = float(np.linalg.norm(np.minimum(g, go)))
+    assert phi <= 1e-5 * float(np.linalg.norm(q)), phi
+
+
+def test_fmm_compression_mode_errors(ctx):
+    with pytest.raises(ScError):
+        ctx.set_fmm_compression(3)
