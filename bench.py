@@ -418,7 +418,8 @@ def other_configs():
     ms = e0.elapsed_time(e1)
     res["C5_fast_summation_order8"] = {"n": p.n, "n_c": r["nc"], "bbpgd_iters": r["iters"], "step_ms": ms,
                                        "bbpgd_iters_per_s": r["iters"] / (ms / 1e3), "fmm": ctx.fmm_info(),
-                                       "note": "approximate RPY operator (DESIGN.md section 11); not part of value"}
+                                       "note": "approximate RPY operator (DESIGN.md section 11; order 8 with the compressed M2L); "
+                                               "not part of value"}
     ctx.close()
     return res
 
