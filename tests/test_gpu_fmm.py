@@ -309,3 +309,22 @@ def test_fmm_compressed_converged_solve_certified_by_oracle(ctx):
 def test_fmm_compression_mode_errors(ctx):
     with pytest.raises(ScError):
         ctx.set_fmm_compression(3)
+
+
+@pytest.mark.parametrize("n", [5, 300])
+def test_fmm_compressed_tiny_problems(ctx, n):
+    """Compression forced on a two-level tree (leaf level 2: the smallest interaction grids)."""
+    rng = np.random.default_rng(n + 7)
+    pos = rng.uniform(0, 2.0 * max(1.0, n ** (1 / 3)), size=(n, 3))
+    FT = rng.normal(size=(n, 6))
+    ctx.build_contacts_spheres(_cuda(pos), None, 0.0, 0.1)
+    ctx.set_mobility_model("rpy_fmm")
+    ctx.set_fmm_params(6, 0)
+    ctx.set_fmm_compression(1)
+    try:
+        U = ctx.mobility_apply(_cuda(FT)).cpu().numpy()
+    finally:
+        ctx.set_fmm_compression("auto")
+        ctx.set_mobility_model("rpy")
+    Uo = oracle.rpy_apply(pos, np.ones(n), 1.0, FT)
+    assert _relL2(U, Uo) <= TOL[6]
