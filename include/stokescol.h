@@ -181,16 +181,18 @@ int sc_set_mobility_model(sc_ctx* ctx, int model);
  * order (leaf side >= 2 a_max).  Errors: SC_EINVAL (order not 4/6/8, leaf_level outside 0..8; model 2 on
  * a multi-GPU context, at the first apply). */
 int sc_set_fmm_params(sc_ctx* ctx, int order, int leaf_level);
-/* mode 1: compressed M2L for the monodisperse fast summation.  Per level l, the 316 M2L operators
+/* Compressed M2L of the fast summation.  Per level l, the 316 M2L operators
  * K_o (3n^3 x 3n^3: the RPY far branch between the Chebyshev nodes of a box and of the box at
  * offset o) share one orthonormal basis U_l, the dominant eigenvectors of sum_o K_o K_o^T (K_o^T =
  * K_-o, so one basis serves both sides), kept while lambda >= eps^2 lambda_max with eps a fixed
  * fraction of the order's stated error; M2L becomes
  * L = U_l sum_o C_o (U_l^T M), C_o = U_l^T K_o U_l (k_l x k_l).  The bases are computed once per
- * tree geometry (root side, leaf level, order, radius) and cached; polydisperse radii keep the
- * direct M2L.  mode 0: direct M2L; mode 1: compressed at every order; mode 2 (default): compressed
- * where it measured faster -- order 8 from N = 2^15, order 6 from N = 2^18 (the root side is then
- * rounded up to 8a 2^(i/8) so the cached bases survive small changes of the bounding box).
+ * tree geometry (root side, leaf level, order, radius) and cached.  Polydisperse: one basis for the
+ * two radius-free parts O and D of the split far branch, four compressed products per offset.
+ * mode 0: direct M2L; mode 1: compressed at every order; mode 2 (default): compressed where it
+ * measured faster -- monodisperse order 8 from N = 2^15, order 6 from 2^18; polydisperse order 8
+ * from 2^17, order 6 from 2^20 (the root side is then rounded up to 8 a_max 2^(i/8) so the cached
+ * bases survive small changes of the bounding box).
  * Errors: SC_EINVAL (mode not 0/1/2). */
 int sc_set_fmm_compression(sc_ctx* ctx, int mode);
 /* out3 = {order, leaf level of the current tree (0: not built yet), tree built (0/1)} */

@@ -56,11 +56,13 @@ struct Geom {
 __host__ __device__ inline int64_t nbox(int l) { return int64_t(1) << (3 * l); }
 
 // compressed M2L for this context: mode 1 (on), or mode 2 (auto, the default) where it measured
-// faster (profiles/r02/fmm_compressed_vs_direct.jsonl): order 8 from N = 2^15, order 6 from 2^18;
-// monodisperse only (the polydisperse far field keeps the direct M2L)
+// faster (profiles/r02/fmm_compressed_vs_direct*.jsonl): monodisperse order 8 from N = 2^15, order 6
+// from 2^18; polydisperse order 8 from 2^17, order 6 from 2^20
 inline bool fmm_use_svd(const sc_ctx* ctx) {
-  if (ctx->poly || ctx->fmm_compress == 0) return false;
+  if (ctx->fmm_compress == 0) return false;
   if (ctx->fmm_compress == 1) return true;
+  if (ctx->poly)  // (polydisperse: 4 compressed products per offset; measured faster from these N)
+    return (ctx->fmm_order == 8 && ctx->n >= (int64_t(1) << 17)) || (ctx->fmm_order == 6 && ctx->n >= (int64_t(1) << 20));
   return (ctx->fmm_order == 8 && ctx->n >= (int64_t(1) << 15)) || (ctx->fmm_order == 6 && ctx->n >= (int64_t(1) << 18));
 }
 
@@ -420,9 +422,11 @@ constexpr int kOffGrid = 343, kOffCount = 316;
 
 // K for q offsets (oi list), column-major with leading dimension R = 3 n^3:
 // K[(c R + col) R + row], c = 0..q-1.
+// kind 0: the monodisperse far branch T (radius^2 a2); 1: its Oseen part O = (1/r) I + (1/r^3) d d^T;
+// 2: its radius part D = (2/3)(1/r^3) I - 2 (1/r^5) d d^T (polydisperse: T = O + abar^2 D)
 template <int NN>
 __global__ void svd_build_k_kernel(double* __restrict__ K, const int32_t* __restrict__ ois, int q, double w,
-                                   double a2) {
+                                   double a2, int kind) {
   constexpr int NB = NN * NN * NN, R = 3 * NB;
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= static_cast<int64_t>(R) * R * q) return;
@@ -438,8 +442,17 @@ __global__ void svd_build_k_kernel(double* __restrict__ K, const int32_t* __rest
                        w * (2.0 * oz + c_xbar[nz] - c_xbar[mz])};
   const double r2 = fma(d[2], d[2], fma(d[1], d[1], d[0] * d[0]));
   const double y = 1.0 / sqrt(r2), h = y * y, e = y * h;
-  const double c1 = fma(2.0 / 3.0 * a2, e, y);
-  const double c2 = e * fma(-2.0 * a2, h, 1.0);
+  double c1, c2;
+  if (kind == 0) {
+    c1 = fma(2.0 / 3.0 * a2, e, y);
+    c2 = e * fma(-2.0 * a2, h, 1.0);
+  } else if (kind == 1) {
+    c1 = y;
+    c2 = e;
+  } else {
+    c1 = (2.0 / 3.0) * e;
+    c2 = -2.0 * e * h;
+  }
   K[t] = (al == be ? c1 : 0.0) + c2 * d[al] * d[be];
 }
 
@@ -532,6 +545,23 @@ __global__ void __launch_bounds__(256) m2l_svd_gemm_kernel(int Dp, int k, const 
       if (r < k) LcP[(static_cast<int64_t>(pc) * npad + gc) * k + r] = acc[u][v];
     }
   }
+}
+
+// polydisperse node strengths [box][node][9] = (s0, s1, s2) <-> three channels [c][box][node][3]
+__global__ void svd_poly_split_kernel(int64_t nvals /* nbox NB */, const double* __restrict__ M9,
+                                      double* __restrict__ S) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nvals * 9) return;
+  const int64_t node = t / 9;
+  const int c = static_cast<int>(t % 9) / 3, a = static_cast<int>(t % 3);
+  S[(c * nvals + node) * 3 + a] = M9[t];
+}
+__global__ void svd_poly_merge_kernel(int64_t nvals, const double* __restrict__ S, double* __restrict__ L9) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nvals * 9) return;
+  const int64_t node = t / 9;
+  const int c = static_cast<int>(t % 9) / 3, a = static_cast<int>(t % 3);
+  L9[t] = S[(c * nvals + node) * 3 + a];
 }
 
 // natural box order (k x nbox, box T = (z D + y) D + x) <-> class-padded order (McP layout)
@@ -711,11 +741,14 @@ int svd_handles(sc_ctx* ctx) {
 }
 
 // Bases and compressed operators of every level for the current tree (cached by geometry key).
-template <int NN>
+// Monodisperse: one basis for the operators K_o of the far branch.  Polydisperse: one basis for
+// both radius-free parts O_o and D_o (dominant eigenvectors of their trace-normalised Gram
+// matrices' sum) and two operator sets C^O_o, C^D_o.
+template <int NN, bool POLY>
 int fmm_svd_prepare(sc_ctx* ctx, const Geom& g) {
   double escale = 1.0;
   if (const char* v = std::getenv("SC_FMM_SVD_EPS_SCALE")) escale = std::atof(v);
-  const double key[5] = {g.H, static_cast<double>(g.L), static_cast<double>(NN), g.a, escale};
+  const double key[5] = {g.H, static_cast<double>(g.L), static_cast<double>(NN), POLY ? -1.0 : g.a, escale};
   bool same = true;
   for (int i = 0; i < 5; ++i) same = same && ctx->fmm_svd_key[i] == key[i];
   if (same) return 0;
@@ -723,9 +756,9 @@ int fmm_svd_prepare(sc_ctx* ctx, const Geom& g) {
   cublasHandle_t cb = static_cast<cublasHandle_t>(ctx->cublas);
   cusolverDnHandle_t cs = static_cast<cusolverDnHandle_t>(ctx->cusolver);
   constexpr int NB = NN * NN * NN, R = 3 * NB;
-  // kept singular directions: sigma >= eps sigma_max
-  double eps = NN == 4 ? 6e-5 : (NN == 6 ? 1.8e-6 : 9e-8);  // 3% of the order's stated error bar
-  if (const char* v = std::getenv("SC_FMM_SVD_EPS_SCALE")) eps *= std::atof(v);  // (tuning)
+  constexpr int NK = POLY ? 2 : 1;  // operator families
+  // kept singular directions: sigma >= eps sigma_max, eps = 3% of the order's stated error bar
+  const double eps = (NN == 4 ? 6e-5 : (NN == 6 ? 1.8e-6 : 9e-8)) * escale;
   const int L = g.L;
   std::vector<int32_t> tab(kOffGrid + kOffCount, -1);  // [li_of_oi (343) | oi of li (316)]
   int nl = 0;
@@ -747,30 +780,50 @@ int fmm_svd_prepare(sc_ctx* ctx, const Geom& g) {
   int lwork = 0;
   SC_CUSOLVER(cusolverDnDsyevd_bufferSize(cs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, R, nullptr, R,
                                           nullptr, &lwork));
-  // work: K chunk (Q R R) | G (R R) | eigenvalues (R) | syevd work (lwork) | info | eigvecs per level
+  // work: K chunk (Q R R) | G (R R) | G2 (R R) | eigenvalues (R) | syevd work | info | eigvecs per level
   const size_t nK = size_t(Q) * R * R, nG = size_t(R) * R;
-  const size_t nwork = nK + nG + R + size_t(lwork) + 2 + size_t(L + 1) * R * R;
+  const size_t nwork = nK + 2 * nG + R + size_t(lwork) + 2 + size_t(L + 1) * R * R;
   if (int rc = ensure(ctx, ctx->fmm_svd_work, nwork)) return rc;
   double* K = ctx->fmm_svd_work.p;
   double* G = K + nK;
-  double* W = G + nG;
+  double* G2 = G + nG;
+  double* W = G2 + nG;
   double* wk = W + R;
   int* info = reinterpret_cast<int*>(wk + lwork);
   double* Uall = wk + lwork + 2;  // level l: R x R eigenvectors at Uall + l R R
   const double one = 1.0, zero = 0.0;
   const unsigned kb = 256;
+  const double a2 = g.a * g.a;
+  auto build = [&](double w, int c0, int q, int kind) -> int {
+    const int64_t tot = int64_t(R) * R * q;
+    svd_build_k_kernel<NN><<<static_cast<unsigned>((tot + kb - 1) / kb), kb, 0, ctx->stream>>>(K, ois + c0, q, w, a2,
+                                                                                             kind);
+    return check_launch(ctx, "fmm_svd_build_k");
+  };
+  auto gram = [&](double w, int kind, double* Gx) -> int {  // Gx = sum_o K_o K_o^T (lower)
+    SC_CUDA(cudaMemsetAsync(Gx, 0, sizeof(double) * nG, ctx->stream));
+    for (int c0 = 0; c0 < kOffCount; c0 += Q) {
+      const int q = std::min(Q, kOffCount - c0);
+      if (int rc = build(w, c0, q, kind)) return rc;
+      SC_CUBLAS(cublasDsyrk(cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, R, R * q, &one, K, R, &one, Gx, R));
+    }
+    return 0;
+  };
   ctx->fmm_svd_k.assign(L + 1, 0);
   std::vector<double> hW(R);
   for (int l = 2; l <= L; ++l) {
     const double w = g.H / static_cast<double>(int64_t(1) << (l + 1));
-    SC_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * nG, ctx->stream));
-    for (int c0 = 0; c0 < kOffCount; c0 += Q) {
-      const int q = std::min(Q, kOffCount - c0);
-      const int64_t tot = int64_t(R) * R * q;
-      svd_build_k_kernel<NN><<<static_cast<unsigned>((tot + kb - 1) / kb), kb, 0, ctx->stream>>>(K, ois + c0, q, w,
-                                                                                               g.a * g.a);
-      if (int rc = check_launch(ctx, "fmm_svd_build_k")) return rc;
-      SC_CUBLAS(cublasDsyrk(cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, R, R * q, &one, K, R, &one, G, R));
+    if (!POLY) {
+      if (int rc = gram(w, 0, G)) return rc;
+    } else {  // G = G_O / tr(G_O) + G_D / tr(G_D): both families equally represented
+      if (int rc = gram(w, 1, G)) return rc;
+      if (int rc = gram(w, 2, G2)) return rc;
+      double trO = 0.0, trD = 0.0;
+      SC_CUBLAS(cublasDasum(cb, R, G, R + 1, &trO));  // (diagonal of a Gram matrix: >= 0)
+      SC_CUBLAS(cublasDasum(cb, R, G2, R + 1, &trD));
+      if (!(trO > 0.0) || !(trD > 0.0)) return fail(ctx, SC_ECUDA, "fmm compression: degenerate operators");
+      const double sO = 1.0 / trO, sD = 1.0 / trD;
+      SC_CUBLAS(cublasDgeam(cb, CUBLAS_OP_N, CUBLAS_OP_N, R, R, &sO, G, R, &sD, G2, R, G, R));
     }
     SC_CUSOLVER(cusolverDnDsyevd(cs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, R, G, R, W, wk, lwork, info));
     SC_CUDA(cudaMemcpyAsync(hW.data(), W, sizeof(double) * R, cudaMemcpyDeviceToHost, ctx->stream));
@@ -786,7 +839,7 @@ int fmm_svd_prepare(sc_ctx* ctx, const Geom& g) {
     SC_CUDA(cudaMemcpyAsync(Uall + size_t(l) * R * R, G + size_t(R - k) * R, sizeof(double) * R * k,
                             cudaMemcpyDeviceToDevice, ctx->stream));
   }
-  // U_l and C_l (316 k_l x k_l, column-major, operator index li) into their buffers
+  // U_l and C_l ([family][316] k_l x k_l, column-major, operator index li) into their buffers
   ctx->fmm_svd_uoff.assign(L + 2, 0);
   ctx->fmm_svd_coff.assign(L + 2, 0);
   int64_t nu = 0, ncop = 0, kmax = 1;
@@ -794,12 +847,12 @@ int fmm_svd_prepare(sc_ctx* ctx, const Geom& g) {
     ctx->fmm_svd_uoff[l] = nu;
     ctx->fmm_svd_coff[l] = ncop;
     nu += int64_t(R) * ctx->fmm_svd_k[l];
-    ncop += int64_t(kOffCount) * ctx->fmm_svd_k[l] * ctx->fmm_svd_k[l];
+    ncop += int64_t(NK) * kOffCount * ctx->fmm_svd_k[l] * ctx->fmm_svd_k[l];
     kmax = std::max<int64_t>(kmax, ctx->fmm_svd_k[l]);
   }
   if (int rc = ensure(ctx, ctx->fmm_svd_U, nu)) return rc;
   if (int rc = ensure(ctx, ctx->fmm_svd_C, ncop)) return rc;
-  // T1 = K_o U reuses G's and the K chunk's space when it fits, else a fresh chunk size
+  // T1 = K_o U in G's space
   const int Q2 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(Q, int64_t(nG) / (int64_t(R) * kmax))));
   for (int l = 2; l <= L; ++l) {
     const int k = ctx->fmm_svd_k[l];
@@ -807,65 +860,89 @@ int fmm_svd_prepare(sc_ctx* ctx, const Geom& g) {
     double* U = ctx->fmm_svd_U.p + ctx->fmm_svd_uoff[l];
     SC_CUDA(cudaMemcpyAsync(U, Uall + size_t(l) * R * R, sizeof(double) * R * k, cudaMemcpyDeviceToDevice,
                             ctx->stream));
-    double* Cl = ctx->fmm_svd_C.p + ctx->fmm_svd_coff[l];
-    for (int c0 = 0; c0 < kOffCount; c0 += Q2) {
-      const int q = std::min(Q2, kOffCount - c0);
-      const int64_t tot = int64_t(R) * R * q;
-      svd_build_k_kernel<NN><<<static_cast<unsigned>((tot + kb - 1) / kb), kb, 0, ctx->stream>>>(K, ois + c0, q, w,
-                                                                                               g.a * g.a);
-      if (int rc = check_launch(ctx, "fmm_svd_build_k")) return rc;
-      // T1_c = K_c U (R x k) into G's space; C_c = U^T T1_c (k x k)
-      SC_CUBLAS(cublasDgemmStridedBatched(cb, CUBLAS_OP_N, CUBLAS_OP_N, R, k, R, &one, K, R, int64_t(R) * R, U, R,
-                                          0, &zero, G, R, int64_t(R) * k, q));
-      SC_CUBLAS(cublasDgemmStridedBatched(cb, CUBLAS_OP_T, CUBLAS_OP_N, k, k, R, &one, U, R, 0, G, R,
-                                          int64_t(R) * k, &zero, Cl + int64_t(c0) * k * k, k, int64_t(k) * k, q));
+    for (int f = 0; f < NK; ++f) {
+      double* Cl = ctx->fmm_svd_C.p + ctx->fmm_svd_coff[l] + int64_t(f) * kOffCount * k * k;
+      for (int c0 = 0; c0 < kOffCount; c0 += Q2) {
+        const int q = std::min(Q2, kOffCount - c0);
+        if (int rc = build(w, c0, q, POLY ? 1 + f : 0)) return rc;
+        SC_CUBLAS(cublasDgemmStridedBatched(cb, CUBLAS_OP_N, CUBLAS_OP_N, R, k, R, &one, K, R, int64_t(R) * R, U, R,
+                                            0, &zero, G, R, int64_t(R) * k, q));
+        SC_CUBLAS(cublasDgemmStridedBatched(cb, CUBLAS_OP_T, CUBLAS_OP_N, k, k, R, &one, U, R, 0, G, R,
+                                            int64_t(R) * k, &zero, Cl + int64_t(c0) * k * k, k, int64_t(k) * k, q));
+      }
     }
   }
   SC_CUDA(cudaStreamSynchronize(ctx->stream));
   for (int i = 0; i < 5; ++i) ctx->fmm_svd_key[i] = key[i];
   if (std::getenv("SC_FMM_DEBUG"))
-    for (int l = 2; l <= L; ++l) std::fprintf(stderr, "fmm svd: order %d level %d rank %d of %d\n", NN, l, ctx->fmm_svd_k[l], R);
+    for (int l = 2; l <= L; ++l)
+      std::fprintf(stderr, "fmm svd: order %d %s level %d rank %d of %d\n", NN, POLY ? "poly" : "mono", l,
+                   ctx->fmm_svd_k[l], R);
   return 0;
 }
 
-// The compressed M2L of every level: M^c = U^T M, L^c = sum_o C_o M^c, L = U L^c (writes L).
-template <int NN>
+// The compressed M2L of every level (writes L):
+//   mono  M^c = U^T M,  L^c = sum_o C_o M^c,  L = U L^c
+//   poly  P_c = U^T s_c (c = 0, 1, 2);  A = sum_o C^O_o P_0 + C^D_o P_2,  B = sum_o C^D_o P_1,
+//         C = sum_o C^D_o P_0;  (L_A, L_B, L_C) = U (A, B, C)
+// Each level: 189 batched GEMM calls (one per offset of every parity class, distinct outputs per
+// call) plus, polydisperse, 189 more for the D s2 term of A; accumulated in call order.
+template <int NN, bool POLY>
 int fmm_m2l_compressed(sc_ctx* ctx, const Geom& g, const double* M, double* Lx, const int32_t* done) {
+  (void)done;
   constexpr int NB = NN * NN * NN, R = 3 * NB;
+  constexpr int NCH = POLY ? 3 : 1;  // channels in and out
   cublasHandle_t cb = static_cast<cublasHandle_t>(ctx->cublas);
   SC_CUBLAS(cublasSetStream(cb, ctx->stream));
   const std::vector<int64_t>& lo = ctx->fmm_lev_off;
   int64_t need = 1;
   for (int l = 2; l <= g.L; ++l) {
     const int64_t Dq = (int64_t(1) << (l - 1)) + 2;
-    need = std::max<int64_t>(need, 8 * Dq * Dq * Dq * ctx->fmm_svd_k[l]);
+    need = std::max<int64_t>(need, int64_t(NCH) * 8 * Dq * Dq * Dq * ctx->fmm_svd_k[l]);
   }
-  // Mc / Lc: [natural k x nbox | class-padded 8 (Dp+2)^3 k]
-  const int64_t nat = nbox(g.L) * *std::max_element(ctx->fmm_svd_k.begin(), ctx->fmm_svd_k.end());
-  if (int rc = ensure(ctx, ctx->fmm_Mc, nat + need)) return rc;
+  const int kmax = *std::max_element(ctx->fmm_svd_k.begin(), ctx->fmm_svd_k.end());
+  const int64_t nat = int64_t(NCH) * nbox(g.L) * kmax;    // natural order, NCH channels
+  const int64_t split = POLY ? int64_t(NCH) * nbox(g.L) * R : 0;  // poly: split / merged R-vectors
+  if (int rc = ensure(ctx, ctx->fmm_Mc, nat + need + split)) return rc;
   if (int rc = ensure(ctx, ctx->fmm_Lc, nat + need)) return rc;
+  constexpr int NE = POLY ? 32 : 8;  // batch entries per offset (poly: 24 + 8)
+  if (int rc = ensure(ctx, ctx->fmm_svd_ptrs, 3 * 189 * NE)) return rc;
   const double one = 1.0, zero = 0.0;
   for (int l = 2; l <= g.L; ++l) {
     const int k = ctx->fmm_svd_k[l];
-    const int nb = static_cast<int>(nbox(l));
+    const int64_t nb = nbox(l);
     const int D = 1 << l, Dp = D / 2, Dq = Dp + 2;
     const int64_t npad = int64_t(Dq) * Dq * Dq;
     const double* U = ctx->fmm_svd_U.p + ctx->fmm_svd_uoff[l];
-    double* mcn = ctx->fmm_Mc.p;
-    double* mcp = ctx->fmm_Mc.p + nat;
+    double* mcn = ctx->fmm_Mc.p;                 // [ch][box][k]
+    double* mcp = ctx->fmm_Mc.p + nat;           // [ch][class][padded][k]
+    double* sbuf = ctx->fmm_Mc.p + nat + need;   // poly: [ch][box][node][3]
     double* lcn = ctx->fmm_Lc.p;
     double* lcp = ctx->fmm_Lc.p + nat;
-    SC_CUBLAS(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, k, nb, R, &one, U, R, M + lo[l] * R, R, &zero, mcn, k));
-    SC_CUDA(cudaMemsetAsync(mcp, 0, sizeof(double) * 8 * npad * k, ctx->stream));  // zero halo
-    const int64_t tot = int64_t(nb) * k;
-    svd_to_classes_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(D, k, mcn, mcp);
+    const double* Ml = M + lo[l] * NB * (POLY ? 9 : 3);
+    double* Ll = Lx + lo[l] * NB * (POLY ? 9 : 3);
+    const int64_t nvals = nb * NB;
+    if (POLY) {
+      svd_poly_split_kernel<<<static_cast<unsigned>((nvals * 9 + 255) / 256), 256, 0, ctx->stream>>>(nvals, Ml, sbuf);
+      SC_CUBLAS(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, k, static_cast<int>(NCH * nb), R, &one, U, R, sbuf, R, &zero,
+                            mcn, k));
+    } else {
+      SC_CUBLAS(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, k, static_cast<int>(nb), R, &one, U, R, Ml, R, &zero, mcn,
+                            k));
+    }
+    SC_CUDA(cudaMemsetAsync(mcp, 0, sizeof(double) * NCH * 8 * npad * k, ctx->stream));  // zero halo
+    const int64_t tot = nb * k;
+    for (int ch = 0; ch < NCH; ++ch)
+      svd_to_classes_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(
+          D, k, mcn + ch * nb * k, mcp + ch * 8 * npad * k);
     const int64_t cbeg = (int64_t(1) * Dq + 1) * Dq + 1, cend = (int64_t(Dp) * Dq + Dp) * Dq + Dp + 1;
     const int ncol = static_cast<int>(cend - cbeg);
-    // 189 batched GEMMs: batch entry pc = the i-th offset of class pc (distinct outputs), the
-    // calls accumulate in offset order (beta 0, then 1) -> fixed order
-    const double* Cl = ctx->fmm_svd_C.p + ctx->fmm_svd_coff[l];
-    std::vector<const double*> hA(189 * 8), hB(189 * 8);
-    std::vector<double*> hC(189 * 8);
+    const double* C0 = ctx->fmm_svd_C.p + ctx->fmm_svd_coff[l];  // mono: C; poly: C^O
+    const double* C1 = C0 + int64_t(kOffCount) * k * k;           // poly: C^D
+    auto chan_in = [&](int ch, int spc, int64_t dl) { return mcp + ((int64_t(ch) * 8 + spc) * npad + cbeg + dl) * k; };
+    auto chan_out = [&](int ch, int pc) { return lcp + ((int64_t(ch) * 8 + pc) * npad + cbeg) * k; };
+    std::vector<const double*> hA(189 * NE), hB(189 * NE);
+    std::vector<double*> hC(189 * NE);
     for (int pc = 0; pc < 8; ++pc) {
       const int pxb = pc & 1, pyb = (pc >> 1) & 1, pzb = pc >> 2;
       int i = 0;
@@ -877,27 +954,61 @@ int fmm_m2l_compressed(sc_ctx* ctx, const Geom& g, const double* M, double* Lx, 
             const int qx = pxb + ox, qy = pyb + oy, qz = pzb + oz;
             const int spc = (qx & 1) | ((qy & 1) << 1) | ((qz & 1) << 2);
             const int64_t dl = ((int64_t((qz - (qz & 1)) / 2)) * Dq + (qy - (qy & 1)) / 2) * Dq + (qx - (qx & 1)) / 2;
-            hA[i * 8 + pc] = Cl + int64_t(ctx->fmm_svd_lih[oi]) * k * k;
-            hB[i * 8 + pc] = mcp + (int64_t(spc) * npad + cbeg + dl) * k;
-            hC[i * 8 + pc] = lcp + (int64_t(pc) * npad + cbeg) * k;
+            const int64_t li = ctx->fmm_svd_lih[oi];
+            const double* cO = C0 + li * k * k;
+            const double* cD = C1 + li * k * k;
+            double** Cp = hC.data() + i * NE;
+            const double** Ap = hA.data() + i * NE;
+            const double** Bp = hB.data() + i * NE;
+            if (!POLY) {
+              Ap[pc] = cO;
+              Bp[pc] = chan_in(0, spc, dl);
+              Cp[pc] = chan_out(0, pc);
+            } else {  // [A = C^O P0 | B = C^D P1 | C = C^D P0] (24), then [A += C^D P2] (8)
+              Ap[pc] = cO;
+              Bp[pc] = chan_in(0, spc, dl);
+              Cp[pc] = chan_out(0, pc);
+              Ap[8 + pc] = cD;
+              Bp[8 + pc] = chan_in(1, spc, dl);
+              Cp[8 + pc] = chan_out(1, pc);
+              Ap[16 + pc] = cD;
+              Bp[16 + pc] = chan_in(0, spc, dl);
+              Cp[16 + pc] = chan_out(2, pc);
+              Ap[24 + pc] = cD;
+              Bp[24 + pc] = chan_in(2, spc, dl);
+              Cp[24 + pc] = chan_out(0, pc);
+            }
             ++i;
           }
     }
-    if (int rc = ensure(ctx, ctx->fmm_svd_ptrs, 3 * 189 * 8)) return rc;
     const double** dA = reinterpret_cast<const double**>(ctx->fmm_svd_ptrs.p);
-    const double** dB = dA + 189 * 8;
-    double** dC = reinterpret_cast<double**>(ctx->fmm_svd_ptrs.p + 2 * 189 * 8);
-    SC_CUDA(cudaMemcpyAsync(dA, hA.data(), sizeof(void*) * 189 * 8, cudaMemcpyHostToDevice, ctx->stream));
-    SC_CUDA(cudaMemcpyAsync(dB, hB.data(), sizeof(void*) * 189 * 8, cudaMemcpyHostToDevice, ctx->stream));
-    SC_CUDA(cudaMemcpyAsync(dC, hC.data(), sizeof(void*) * 189 * 8, cudaMemcpyHostToDevice, ctx->stream));
-    for (int i = 0; i < 189; ++i)
-      SC_CUBLAS(cublasDgemmBatched(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, ncol, k, &one, dA + i * 8, k, dB + i * 8, k,
-                                   i == 0 ? &zero : &one, dC + i * 8, k, 8));
-    SC_CUDA(cudaStreamSynchronize(ctx->stream));  // (the host pointer tables are reused next level)
-    svd_from_classes_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(D, k, lcp, lcn);
-    SC_CUBLAS(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, R, nb, k, &one, U, R, lcn, k, &zero, Lx + lo[l] * R, R));
+    const double** dB = dA + 189 * NE;
+    double** dC = reinterpret_cast<double**>(ctx->fmm_svd_ptrs.p + 2 * 189 * NE);
+    // (pageable host -> device: the copies return once the tables are staged; stream-ordered after
+    // the previous level's GEMMs that read the same device tables)
+    SC_CUDA(cudaMemcpyAsync(dA, hA.data(), sizeof(void*) * 189 * NE, cudaMemcpyHostToDevice, ctx->stream));
+    SC_CUDA(cudaMemcpyAsync(dB, hB.data(), sizeof(void*) * 189 * NE, cudaMemcpyHostToDevice, ctx->stream));
+    SC_CUDA(cudaMemcpyAsync(dC, hC.data(), sizeof(void*) * 189 * NE, cudaMemcpyHostToDevice, ctx->stream));
+    const int first = POLY ? 24 : 8;
+    for (int i = 0; i < 189; ++i) {
+      SC_CUBLAS(cublasDgemmBatched(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, ncol, k, &one, dA + i * NE, k, dB + i * NE, k,
+                                   i == 0 ? &zero : &one, dC + i * NE, k, first));
+      if (POLY)
+        SC_CUBLAS(cublasDgemmBatched(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, ncol, k, &one, dA + i * NE + 24, k,
+                                     dB + i * NE + 24, k, &one, dC + i * NE + 24, k, 8));
+    }
+    for (int ch = 0; ch < NCH; ++ch)
+      svd_from_classes_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(
+          D, k, lcp + ch * 8 * npad * k, lcn + ch * nb * k);
+    if (POLY) {
+      SC_CUBLAS(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, R, static_cast<int>(NCH * nb), k, &one, U, R, lcn, k, &zero,
+                            sbuf, R));
+      svd_poly_merge_kernel<<<static_cast<unsigned>((nvals * 9 + 255) / 256), 256, 0, ctx->stream>>>(nvals, sbuf, Ll);
+    } else {
+      SC_CUBLAS(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, R, static_cast<int>(nb), k, &one, U, R, lcn, k, &zero, Ll, R));
+    }
   }
-  ctx->launch_count += 5 * (g.L - 1);
+  ctx->launch_count += (POLY ? 9 : 5) * (g.L - 1);
   return 0;
 }
 
@@ -920,11 +1031,11 @@ int fmm_launch(sc_ctx* ctx, const Geom& g, const double4* f4, double mu, double4
   for (int l = L - 1; l >= 2; --l)
     transfer_kernel<NN, true, C><<<static_cast<unsigned>(nbox(l)), nb, 0, ctx->stream>>>(
         l, M + lo[l] * NB * C, M + lo[l + 1] * NB * C, done);
-  if (POLY)
+  if (fmm_use_svd(ctx)) {
+    if (int rc = fmm_m2l_compressed<NN, POLY>(ctx, g, M, Lc, done)) return rc;
+  } else if (POLY)
     m2l_poly_kernel<NN><<<static_cast<unsigned>(lo[L + 1] - lo[2]), nb, 0, ctx->stream>>>(g, loff, M, Lc, done);
-  else if (fmm_use_svd(ctx)) {
-    if (int rc = fmm_m2l_compressed<NN>(ctx, g, M, Lc, done)) return rc;
-  } else
+  else
     m2l_kernel<NN><<<static_cast<unsigned>(lo[L + 1] - lo[2]), nb, 0, ctx->stream>>>(g, loff, M, Lc, done);
   for (int l = 2; l < L; ++l)
     transfer_kernel<NN, false, C><<<static_cast<unsigned>(nbox(l + 1)), nb, 0, ctx->stream>>>(
@@ -1055,7 +1166,7 @@ int fmm_setup(sc_ctx* ctx) {
       double m2l = (ctx->poly ? 1.8 : 1.0) * 0.8 * 1.15 * leaves * 150.0 * nb3 * nb3;  // (poly: 3 fields)
       if (fmm_use_svd(ctx)) {  // compressed: 189 k^2 FMA per box on the GEMM path, ~7.8 FMA per P2P pair
         const double kest = nn == 4 ? 132.0 : (nn == 6 ? 286.0 : 454.0);
-        m2l = leaves * 189.0 * kest * kest / 7.8;
+        m2l = (ctx->poly ? 4.4 : 1.0) * leaves * 189.0 * kest * kest / 7.8;  // (poly: 4 products, larger k)
       }
       const double fill = std::min(1.0, leaves * std::max(1.0, static_cast<double>(n) / leaves / 128.0) /
                                             (2.0 * std::max(ctx->num_sms, 1)));
@@ -1142,10 +1253,11 @@ int fmm_apply(sc_ctx* ctx, const double4* f4, double mu, double4* u4, const int3
   Geom g{ctx->fmm_geom[0], ctx->fmm_geom[1], ctx->fmm_geom[2], ctx->fmm_geom[3], ctx->a_const, ctx->fmm_L_used};
   if (fmm_use_svd(ctx)) {
     int rc = 0;
+    const bool pl = ctx->fmm_poly != 0;
     switch (ctx->fmm_order) {
-      case 4: rc = fmm_svd_prepare<4>(ctx, g); break;
-      case 6: rc = fmm_svd_prepare<6>(ctx, g); break;
-      default: rc = fmm_svd_prepare<8>(ctx, g); break;
+      case 4: rc = pl ? fmm_svd_prepare<4, true>(ctx, g) : fmm_svd_prepare<4, false>(ctx, g); break;
+      case 6: rc = pl ? fmm_svd_prepare<6, true>(ctx, g) : fmm_svd_prepare<6, false>(ctx, g); break;
+      default: rc = pl ? fmm_svd_prepare<8, true>(ctx, g) : fmm_svd_prepare<8, false>(ctx, g); break;
     }
     if (rc) return rc;
   }

@@ -328,3 +328,25 @@ def test_fmm_compressed_tiny_problems(ctx, n):
         ctx.set_mobility_model("rpy")
     Uo = oracle.rpy_apply(pos, np.ones(n), 1.0, FT)
     assert _relL2(U, Uo) <= TOL[6]
+
+
+@pytest.mark.parametrize("order", [6, 8])
+def test_fmm_compressed_polydisperse_vs_oracle(ctx, order):
+    """Polydisperse compressed M2L (one basis for the radius-free parts O and D, four products per
+    offset) on the C2 recipe: within the stated bars and bitwise-repeatable."""
+    p = make_problem("C2", n=8192)
+    ctx.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+    ctx.set_mobility_model("rpy_fmm")
+    ctx.set_fmm_params(order, 3)
+    ctx.set_fmm_compression(1)
+    try:
+        FT = np.random.default_rng(31).normal(size=(p.n, 6))
+        U = ctx.mobility_apply(_cuda(FT), mu=p.mu)
+        U2 = ctx.mobility_apply(_cuda(FT), mu=p.mu)
+    finally:
+        ctx.set_fmm_compression("auto")
+        ctx.set_mobility_model("rpy")
+    assert torch.equal(U, U2)
+    Uo = oracle.rpy_apply(p.pos, p.radius, p.mu, FT)
+    err = _relL2(U.cpu().numpy()[:, :3], Uo[:, :3])
+    assert err <= TOL[order], (order, err)

@@ -1,7 +1,7 @@
 """Compressed vs direct M2L of the fast summation (sc_set_fmm_compression), C5 recipe: time per apply
 (CUDA events, after a warm-up apply that also builds the bases), relative L2 error against the
 ORACLE's direct rows on 48 sampled bodies, and the two operators' relative difference.
-  python tools/fmm_compress_check.py [log2n ...]"""
+  python tools/fmm_compress_check.py [log2n ...]    (FMM_RECIPE=C2: polydisperse)"""
 import json
 import os
 import sys
@@ -34,7 +34,7 @@ def timed(ctx, F, mu, reps=3):
 
 for k in [int(x) for x in sys.argv[1:]] or [16, 18, 20]:
     n = 1 << k
-    p = make_problem("C5", n=n)
+    p = make_problem(os.environ.get("FMM_RECIPE", "C5"), n=n)
     t = lambda a: torch.as_tensor(a, device="cuda:0")
     ctx = Context(0)
     ctx.build_contacts_spheres(t(p.pos), t(p.radius), p.gap_abs, p.gap_rel)
@@ -42,7 +42,7 @@ for k in [int(x) for x in sys.argv[1:]] or [16, 18, 20]:
     rows = np.sort(np.random.default_rng(k).choice(n, 48, replace=False))
     Uo = np.stack([oracle.rpy_apply_rows(p.pos, p.radius, p.mu, p.force, int(r), int(r) + 1)[0] for r in rows])
     ctx.set_mobility_model("rpy_fmm")
-    row = {"n": n}
+    row = {"n": n, "recipe": os.environ.get("FMM_RECIPE", "C5")}
     for order in (4, 6, 8):
         ctx.set_fmm_params(order, 0)
         res = {}
