@@ -190,7 +190,8 @@ int sc_set_fmm_params(sc_ctx* ctx, int order, int leaf_level);
  * tree geometry (root side, leaf level, order, radius) and cached.  Polydisperse: one basis for the
  * two radius-free parts O and D of the split far branch, four compressed products per offset.
  * mode 0: direct M2L; mode 1: compressed at every order; mode 2 (default): compressed where it
- * measured faster -- monodisperse order 8 from N = 2^15, order 6 from 2^18; polydisperse order 8
+ * measured faster -- monodisperse order 8 from N = 2^15, order 6 from 2^18, order 4 from 2^21;
+ * polydisperse order 8
  * from 2^17, order 6 from 2^20 (the root side is then rounded up to 8 a_max 2^(i/8) so the cached
  * bases survive small changes of the bounding box).
  * Errors: SC_EINVAL (mode not 0/1/2). */

@@ -57,13 +57,14 @@ __host__ __device__ inline int64_t nbox(int l) { return int64_t(1) << (3 * l); }
 
 // compressed M2L for this context: mode 1 (on), or mode 2 (auto, the default) where it measured
 // faster (profiles/r02/fmm_compressed_vs_direct*.jsonl): monodisperse order 8 from N = 2^15, order 6
-// from 2^18; polydisperse order 8 from 2^17, order 6 from 2^20
+// from 2^18, order 4 from 2^21; polydisperse order 8 from 2^17, order 6 from 2^20
 inline bool fmm_use_svd(const sc_ctx* ctx) {
   if (ctx->fmm_compress == 0) return false;
   if (ctx->fmm_compress == 1) return true;
   if (ctx->poly)  // (polydisperse: 4 compressed products per offset; measured faster from these N)
     return (ctx->fmm_order == 8 && ctx->n >= (int64_t(1) << 17)) || (ctx->fmm_order == 6 && ctx->n >= (int64_t(1) << 20));
-  return (ctx->fmm_order == 8 && ctx->n >= (int64_t(1) << 15)) || (ctx->fmm_order == 6 && ctx->n >= (int64_t(1) << 18));
+  return (ctx->fmm_order == 8 && ctx->n >= (int64_t(1) << 15)) || (ctx->fmm_order == 6 && ctx->n >= (int64_t(1) << 18)) ||
+         (ctx->fmm_order == 4 && ctx->n >= (int64_t(1) << 21));
 }
 
 // 1-D interpolation weights w[k] = S_n(xbar_k, u), u in [-1, 1]
