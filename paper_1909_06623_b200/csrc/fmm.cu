@@ -19,6 +19,9 @@
 // xbar_k = cos((2k+1) pi / (2n)); IL(T) = the children of the parent's neighbours that are not
 // adjacent to T (at most 189).  Every sum is in a fixed order (deterministic).  Polydisperse radii:
 // the far branch is split into radius-free kernels (m2l_poly_kernel), 9 node components instead of 3.
+// Compressed M2L (default where faster, sc_set_fmm_compression): per level one orthonormal basis U
+// of the 316 offset operators K_o (eigenvectors of sum_o K_o K_o^T, cuSOLVER, once per geometry),
+// C_o = U^T K_o U, and M2L as class-batched GEMMs L = U sum_o C_o U^T M (cuBLAS: plain GEMMs).
 #include <cublas_v2.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cusolverDn.h>
