@@ -1075,6 +1075,9 @@ int sc_bbpgd_solve(sc_ctx* ctx, const sc_bbpgd_opts* opts, double* gamma, double
     // (multi-GPU: the done flag is identical on every rank -- K-FINALIZE runs on every rank on the
     // all-reduced partials -- so every rank enqueues the same batches and the collectives match)
     int batch = std::max(1, std::min(32, static_cast<int>(1e-3 / t_iter)));
+    // (the compressed fast summation's cuBLAS calls do not read the done flag: one iteration per
+    // host read, so nothing runs after convergence)
+    if (spheres && ctx->mobility_model == 2 && fmm_uses_library_calls(ctx)) batch = 1;
     if (ctx->batch_override > 0) batch = ctx->batch_override;  // tuning (env SC_BATCH)
     auto enqueue_iter = [&](int pp) -> int {
       if (dist) {  // Steps 8-9 on own constraints, then every rank needs the full gamma_j
