@@ -196,6 +196,9 @@ int sc_set_fmm_params(sc_ctx* ctx, int order, int leaf_level);
  * bases survive small changes of the bounding box).
  * Errors: SC_EINVAL (mode not 0/1/2). */
 int sc_set_fmm_compression(sc_ctx* ctx, int mode);
+/* out4 = {mode (0/1/2), compressed M2L active for the current bodies and order (0/1), rank of the
+ * cached bases at their leaf level (0: none built yet), that leaf level} */
+int sc_get_fmm_compression_info(const sc_ctx* ctx, int32_t* out4);
 /* out3 = {order, leaf level of the current tree (0: not built yet), tree built (0/1)} */
 int sc_get_fmm_info(const sc_ctx* ctx, int32_t* out3);
 

@@ -188,7 +188,11 @@ class Context:
     def fmm_info(self) -> dict:
         out = (C.c_int32 * 3)()
         self._rc(self.lib.sc_get_fmm_info(self._h, out))
-        return dict(zip(["order", "leaf_level", "ready"], list(out)))
+        info = dict(zip(["order", "leaf_level", "ready"], list(out)))
+        c4 = (C.c_int32 * 4)()
+        self._rc(self.lib.sc_get_fmm_compression_info(self._h, c4))
+        info.update(zip(["compression_mode", "compressed", "rank", "rank_level"], list(c4)))
+        return info
 
     # ------------------------------------------------------------- (a1)
     def build_contacts_spheres(self, pos, radius=None, gap_abs=0.0, gap_rel=0.1) -> int:

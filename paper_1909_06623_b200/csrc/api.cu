@@ -671,6 +671,16 @@ int sc_set_fmm_compression(sc_ctx* ctx, int mode) {
   return SC_OK;
 }
 
+int sc_get_fmm_compression_info(const sc_ctx* ctx, int32_t* out4) {
+  if (ctx == nullptr || out4 == nullptr) return SC_EINVAL;
+  out4[0] = ctx->fmm_compress;
+  out4[1] = fmm_uses_library_calls(ctx) ? 1 : 0;
+  const bool built = ctx->fmm_svd_key[4] != 0.0 && !ctx->fmm_svd_k.empty();
+  out4[2] = built ? ctx->fmm_svd_k.back() : 0;                     // rank at the leaf level
+  out4[3] = built ? static_cast<int32_t>(ctx->fmm_svd_k.size()) - 1 : 0;  // leaf level of the bases
+  return SC_OK;
+}
+
 int sc_get_fmm_info(const sc_ctx* ctx, int32_t* out3) {
   if (ctx == nullptr || out3 == nullptr) return SC_EINVAL;
   out3[0] = ctx->fmm_order;

@@ -49,6 +49,7 @@ def test_fmm_apply_vs_oracle(ctx, order, n, leaf_level):
     ctx.set_mobility_model("rpy")
     Uo = oracle.rpy_apply(p.pos, p.radius, p.mu, FT)
     assert info["ready"] == 1 and info["leaf_level"] >= 2 and (leaf_level == 0 or info["leaf_level"] == leaf_level)
+    assert info["compression_mode"] == 2 and info["compressed"] == 0  # (auto: direct M2L below 2^15)
     err = _relL2(U[:, :3], Uo[:, :3])
     assert err <= TOL[order], (order, n, info, err)
     np.testing.assert_allclose(U[:, 3:], Uo[:, 3:], rtol=1e-13, atol=0)  # self rotation (exact)
@@ -271,9 +272,12 @@ def test_fmm_compressed_m2l_vs_oracle(ctx, order, n, leaf_level):
         FT = np.random.default_rng(21).normal(size=(p.n, 6))
         U = ctx.mobility_apply(_cuda(FT))
         U2 = ctx.mobility_apply(_cuda(FT))
+        info = ctx.fmm_info()
     finally:
         ctx.set_fmm_compression("auto")
         ctx.set_mobility_model("rpy")
+    assert info["compression_mode"] == 1 and info["compressed"] == 1
+    assert 0 < info["rank"] < 3 * order ** 3 and info["rank_level"] == info["leaf_level"]
     assert torch.equal(U, U2)
     Uo = oracle.rpy_apply(p.pos, p.radius, p.mu, FT)
     err = _relL2(U.cpu().numpy()[:, :3], Uo[:, :3])
