@@ -584,7 +584,7 @@ void sc_destroy(sc_ctx* ctx) {
   release(ctx->w); release(ctx->gam_user); release(ctx->uc); release(ctx->prev_key); release(ctx->prev_gam); release(ctx->chunk_part); release(ctx->chunk_red);
   release(ctx->fmm_key); release(ctx->fmm_idx0); release(ctx->fmm_sidx); release(ctx->fmm_cnt); release(ctx->fmm_lstart); release(ctx->fmm_cubtmp); release(ctx->fmm_spos4); release(ctx->fmm_sf4); release(ctx->fmm_M); release(ctx->fmm_L); release(ctx->fmm_lev_off_dev);
   release(ctx->fmm_svd_U); release(ctx->fmm_svd_C); release(ctx->fmm_Mc); release(ctx->fmm_Lc); release(ctx->fmm_svd_work);
-  release(ctx->fmm_svd_li); release(ctx->fmm_svd_ptrs);
+  release(ctx->fmm_svd_li); release(ctx->fmm_svd_ptrs); release(ctx->fmm_acc); release(ctx->fmm_fx);
   fmm_destroy_handles(ctx);
   release(ctx->sym_pairs); release(ctx->sym_acc); release(ctx->fx_scale); release(ctx->trace); release(ctx->f4); release(ctx->t4); release(ctx->u4); release(ctx->rpy_part);
   release(ctx->bbox_part); release(ctx->cell_of); release(ctx->cell_cnt); release(ctx->cell_start);

@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "fixed_point.cuh"
 #include "rpy_common.cuh"
 #include "sc_internal.h"
 
@@ -48,6 +49,10 @@ __constant__ double c_tab[tab_size(4) + tab_size(6) + tab_size(8)];
 #define c_xbar (c_tab + tab_off(NN))
 #define c_T (c_tab + tab_off(NN) + NN)
 #define c_P (c_tab + tab_off(NN) + NN + NN * NN)
+
+#ifndef SC_FMM_P2P_SYM
+#define SC_FMM_P2P_SYM 1  // near field by p2p_sym_kernel (each unordered leaf pair once; 0: per target)
+#endif
 
 struct Geom {
   double ox, oy, oz;  // root cube corner
@@ -597,14 +602,192 @@ __global__ void svd_from_classes_kernel(int D, int k, const double* __restrict__
 // L2P + P2P: one CTA per leaf; thread = target body (chunks of blockDim); sources of the 27
 // neighbouring leaves through shared memory (exact RPY incl. the overlap branch and the self term).
 // POLY: the leaf's 9-component local expansion (m2l_poly_kernel) and the pair radius w_i + w_j.
-template <int NN, bool POLY>
+// ---- symmetric near field (default): each unordered leaf pair once --------------------------
+// The exact pair sum over the 27 leaves around a body is symmetric (T_ij = T_ji), so the pairs
+// between leaf b and the 13 neighbours q in the "forward" half-space (plus b itself) are
+// evaluated once and feed both bodies: U_i += T F_j (forward, in registers) and U_j += T F_i
+// (reverse, the warp-rotation of rpy.cu's symmetric kernel: lane l meets source (l + s) mod 32 at
+// step s and carries that source's accumulator, passed on by one shuffle per step).  Every
+// partial sum is added as 128-bit fixed point (fixed_point.cuh) -- exact, order-independent --
+// and the L2P kernel adds the limbs.  CTA: (leaf b, neighbour index f in 0..13, chunk of 128
+// targets of b); 4 warps x 32 targets; sources of q in chunks of 128 through shared memory.
+// f = 0 (b itself): every ordered pair, forward only.
+__global__ void fmm_fx_prep_kernel(const double4* __restrict__ spos, const double4* __restrict__ sf, int64_t n,
+                                   FxScale* __restrict__ fs, const int32_t* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  double mf = 0.0, mi = 0.0;
+  for (int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < n;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double4 f = sf[b];
+    mf = fmax(mf, fmax(fabs(f.x), fmax(fabs(f.y), fabs(f.z))));
+    mi = fmax(mi, 0.5 / spos[b].w);  // w = a/2 (abar >= a_min)
+  }
+  if (!(mf <= 1.7e308)) mf = 1.7e308;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    mf = fmax(mf, __shfl_xor_sync(0xffffffffu, mf, o));
+    mi = fmax(mi, __shfl_xor_sync(0xffffffffu, mi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&fs->maxf_bits, static_cast<unsigned long long>(__double_as_longlong(mf)));
+    atomicMax(&fs->maxinva_bits, static_cast<unsigned long long>(__double_as_longlong(mi)));
+  }
+}
+
+// the exact RPY pair block (far branch, or the overlap branch with abar) applied to f: c1 f + c2 (d.f) d
+template <bool POLY>
+__device__ __forceinline__ void near_pair_coefs(const double4& pi, const double4& pj, double a, double a2,
+                                                double ia, long long near_bits, double& dx, double& dy,
+                                                double& dz, double& c1, double& c2, bool& coincident) {
+  const double r2 = rpy_r2(pi, pj, dx, dy, dz);
+  const double ab = POLY ? pi.w + pj.w : a;
+  coincident = false;
+  if (!rpy_is_near(r2, ab, POLY, near_bits)) {
+    const double y = rsqrt_dp(r2);
+    const double h = y * y, e = y * h, ab2 = POLY ? ab * ab : a2;
+    c1 = fma(2.0 / 3.0 * ab2, e, y);
+    c2 = e * fma(-2.0 * ab2, h, 1.0);
+  } else {
+    double rs = 0.0, rr = 0.0;
+    if (r2 > 0.0) {
+      rs = rsqrt_dp(r2);
+      rr = r2 * rs;
+    } else {
+      coincident = true;
+    }
+    const double iab = POLY ? 1.0 / ab : ia;
+    c1 = (4.0 / 3.0) * iab * fma(-9.0 / 32.0 * iab, rr, 1.0);
+    c2 = 0.125 * iab * iab * rs;
+  }
+}
+
+template <bool POLY>
+__global__ void __launch_bounds__(128) p2p_sym_kernel(const double4* __restrict__ spos, const double4* __restrict__ sf,
+                                                      const int32_t* __restrict__ lstart, Geom g,
+                                                      long long* __restrict__ acc, FxScale* __restrict__ fs,
+                                                      int64_t fx_count, int32_t* __restrict__ err,
+                                                      const int32_t* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  constexpr int TS = 128;
+  __shared__ double4 sp[TS], sfs[TS];
+  __shared__ double rev[4][TS][3];
+  const int64_t b = blockIdx.x;
+  const int f = static_cast<int>(blockIdx.y);
+  const int D = 1 << g.L;
+  const int bx = static_cast<int>(b % D), by = static_cast<int>((b / D) % D), bz = static_cast<int>(b / D / D);
+  // forward neighbour f: 0 = b; 1..13 = the half-space (oz > 0) | (oz = 0, oy > 0) | (0, 0, ox > 0)
+  int ox = 0, oy = 0, oz = 0;
+  if (f > 0) {
+    int c = 0;
+    for (int z = 0; z <= 1 && c < f; ++z)
+      for (int y = -1; y <= 1 && c < f; ++y)
+        for (int x = -1; x <= 1 && c < f; ++x) {
+          const bool fwd = z > 0 || (y > 0) || (y == 0 && x > 0);
+          if (!fwd) continue;
+          if (++c == f) {
+            ox = x;
+            oy = y;
+            oz = z;
+          }
+        }
+  }
+  const int qx = bx + ox, qy = by + oy, qz = bz + oz;
+  if (qx < 0 || qy < 0 || qz < 0 || qx >= D || qy >= D || qz >= D) return;  // (uniform in the CTA)
+  const int64_t q = (static_cast<int64_t>(qz) * D + qy) * D + qx;
+  const int32_t i0 = lstart[b] + static_cast<int32_t>(blockIdx.z) * TS, i1 = min(lstart[b + 1], i0 + TS);
+  if (i0 >= i1) return;
+  const int32_t j0 = lstart[q], j1 = lstart[q + 1];
+  if (j0 >= j1) return;
+  const double a = g.a, a2 = a * a, ia = 1.0 / a;
+  const long long near_bits = __double_as_longlong(4.0 * a2);
+  const double scale = pow2(fx_shift(fs, fx_count));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t ti = i0 + threadIdx.x;  // this thread's target
+  const bool tval = ti < i1;
+  const double4 pi = tval ? spos[ti] : make_double4(1e300, 1e300, 1e300, 1.0);
+  const double4 fi = tval ? sf[ti] : make_double4(0, 0, 0, 0);
+  double ux = 0.0, uy = 0.0, uz = 0.0;
+  bool bad = false, coinc = false;
+  for (int32_t c0 = j0; c0 < j1; c0 += TS) {
+    const int cn = min(TS, j1 - c0);
+    __syncthreads();
+    if (threadIdx.x < cn) {
+      sp[threadIdx.x] = spos[c0 + threadIdx.x];
+      sfs[threadIdx.x] = sf[c0 + threadIdx.x];
+    }
+    __syncthreads();
+    if (f == 0) {  // b itself: every ordered pair (i, j != i), forward only
+      if (tval)
+        for (int jj = 0; jj < cn; ++jj) {
+          if (c0 + jj == ti) continue;
+          double dx, dy, dz, c1, c2;
+          bool co;
+          near_pair_coefs<POLY>(pi, sp[jj], a, a2, ia, near_bits, dx, dy, dz, c1, c2, co);
+          coinc |= co;
+          const double4 fj = sfs[jj];
+          const double t = c2 * fma(dz, fj.z, fma(dy, fj.y, dx * fj.x));
+          ux = fma(t, dx, fma(c1, fj.x, ux));
+          uy = fma(t, dy, fma(c1, fj.y, uy));
+          uz = fma(t, dz, fma(c1, fj.z, uz));
+        }
+      continue;
+    }
+    // q != b: 32 x 32 rotation blocks; each warp's 32 targets against the chunk's sources
+    for (int sb = 0; sb * 32 < cn; ++sb) {
+      double rx = 0.0, ry = 0.0, rz = 0.0;
+#pragma unroll 1
+      for (int st = 0; st < 32; ++st) {
+        const int jj = sb * 32 + ((lane + st) & 31);
+        if (tval && jj < cn) {
+          double dx, dy, dz, c1, c2;
+          bool co;
+          near_pair_coefs<POLY>(pi, sp[jj], a, a2, ia, near_bits, dx, dy, dz, c1, c2, co);
+          coinc |= co;
+          const double4 fj = sfs[jj];
+          const double t = c2 * fma(dz, fj.z, fma(dy, fj.y, dx * fj.x));
+          ux = fma(t, dx, fma(c1, fj.x, ux));
+          uy = fma(t, dy, fma(c1, fj.y, uy));
+          uz = fma(t, dz, fma(c1, fj.z, uz));
+          const double tr = c2 * fma(dz, fi.z, fma(dy, fi.y, dx * fi.x));  // T even in d
+          rx = fma(tr, dx, fma(c1, fi.x, rx));
+          ry = fma(tr, dy, fma(c1, fi.y, ry));
+          rz = fma(tr, dz, fma(c1, fi.z, rz));
+        }
+        const int src = (lane + 1) & 31;  // next step this lane meets the source lane+1 met now
+        rx = __shfl_sync(0xffffffffu, rx, src);
+        ry = __shfl_sync(0xffffffffu, ry, src);
+        rz = __shfl_sync(0xffffffffu, rz, src);
+      }
+      // lane l now holds source sb*32 + l's reverse sum over this warp's targets
+      rev[w][sb * 32 + lane][0] = rx;
+      rev[w][sb * 32 + lane][1] = ry;
+      rev[w][sb * 32 + lane][2] = rz;
+    }
+    __syncthreads();
+    if (threadIdx.x < cn) {  // the 4 warps' reverse sums in warp order -> one fixed-point add
+      double v[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[c] = ((rev[0][threadIdx.x][c] + rev[1][threadIdx.x][c]) + rev[2][threadIdx.x][c]) +
+                                         rev[3][threadIdx.x][c];
+      fx_red3(acc + static_cast<int64_t>(c0 + threadIdx.x) * 9, v[0], v[1], v[2], scale, bad);
+    }
+  }
+  if (tval) fx_red3(acc + static_cast<int64_t>(ti) * 9, ux, uy, uz, scale, bad);
+  if (coinc) atomicExch(err, 1);  // coincident centres (reading A12)
+  if (bad) fs->bad = 1;
+}
+
+// NEAR_FX: the near field was summed by p2p_sym_kernel into fixed-point limbs (acc, scale fs); this
+// kernel then adds them (and zeroes them for the next apply) instead of running the 27-leaf loop.
+template <int NN, bool POLY, bool NEAR_FX>
 __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict__ spos,
                                                       const double4* __restrict__ sf,
                                                       const int32_t* __restrict__ sidx,
                                                       const int32_t* __restrict__ lstart, Geom g,
                                                       const double* __restrict__ Lc, int64_t loff_L, double scale,
                                                       double4* __restrict__ u4, int32_t* __restrict__ err,
-                                                      const int32_t* __restrict__ done) {
+                                                      const int32_t* __restrict__ done, long long* __restrict__ acc,
+                                                      FxScale* __restrict__ fs, int64_t fx_count) {
   if (done != nullptr && *done) return;
   constexpr int NB = NN * NN * NN;
   constexpr int TS = 128;
@@ -662,6 +845,7 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
       }
     }
     // near field: the 27 leaves around b (incl. b), fixed order
+    if (!NEAR_FX)
     for (int oz = -1; oz <= 1; ++oz)
       for (int oy = -1; oy <= 1; ++oy)
         for (int ox = -1; ox <= 1; ++ox) {
@@ -711,6 +895,19 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
       ux = fma(cs, fi.x, ux);
       uy = fma(cs, fi.y, uy);
       uz = fma(cs, fi.z, uz);
+      if (NEAR_FX) {  // + the exact near-field sums (one rounding each), then reset the limbs
+        if (fs->bad) {
+          ux = uy = uz = __longlong_as_double(0x7ff8000000000000LL);  // -> SC_ENONFINITE
+        } else {
+          const double inv = pow2(-fx_shift(fs, fx_count));
+          long long* l = acc + static_cast<int64_t>(k) * 9;
+          ux += fx_value(l + 0, inv);
+          uy += fx_value(l + 3, inv);
+          uz += fx_value(l + 6, inv);
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) acc[static_cast<int64_t>(k) * 9 + q] = 0;
+      }
       SC_DCHECK(sidx[k] >= 0 && sidx[k] < lstart[int64_t(1) << (3 * g.L)]);
       u4[sidx[k]] = make_double4(scale * ux, scale * uy, scale * uz, 0.0);
     }
@@ -1045,10 +1242,25 @@ int fmm_launch(sc_ctx* ctx, const Geom& g, const double4* f4, double mu, double4
     transfer_kernel<NN, false, C><<<static_cast<unsigned>(nbox(l + 1)), nb, 0, ctx->stream>>>(
         l, Lc + lo[l] * NB * C, Lc + lo[l + 1] * NB * C, done);
   const double scale = 1.0 / (8.0 * 3.14159265358979323846 * mu);
-  const dim3 gp(static_cast<unsigned>(nbox(L)), static_cast<unsigned>(std::max<int64_t>(1, (ctx->fmm_maxleaf + 127) / 128)));
-  l2p_p2p_kernel<NN, POLY><<<gp, 128, 0, ctx->stream>>>(
-      ctx->fmm_spos4.p, ctx->fmm_sf4.p, ctx->fmm_sidx.p, ctx->fmm_lstart.p, g, Lc, lo[L], scale, u4, ctx->derr,
-      done);
+  const unsigned nchunk = static_cast<unsigned>(std::max<int64_t>(1, (ctx->fmm_maxleaf + 127) / 128));
+  const dim3 gp(static_cast<unsigned>(nbox(L)), nchunk);
+  if (SC_FMM_P2P_SYM) {
+    const int64_t fx_count = 27 * std::max<int64_t>(1, ctx->fmm_maxleaf);  // sources per row, at most
+    FxScale* fs = reinterpret_cast<FxScale*>(ctx->fmm_fx.p);
+    SC_CUDA(cudaMemsetAsync(fs, 0, sizeof(FxScale), ctx->stream));
+    fmm_fx_prep_kernel<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4 * 148)), 256, 0, ctx->stream>>>(
+        ctx->fmm_spos4.p, ctx->fmm_sf4.p, n, fs, done);
+    p2p_sym_kernel<POLY><<<dim3(static_cast<unsigned>(nbox(L)), 14, nchunk), 128, 0, ctx->stream>>>(
+        ctx->fmm_spos4.p, ctx->fmm_sf4.p, ctx->fmm_lstart.p, g, ctx->fmm_acc.p, fs, fx_count, ctx->derr, done);
+    l2p_p2p_kernel<NN, POLY, true><<<gp, 128, 0, ctx->stream>>>(
+        ctx->fmm_spos4.p, ctx->fmm_sf4.p, ctx->fmm_sidx.p, ctx->fmm_lstart.p, g, Lc, lo[L], scale, u4, ctx->derr,
+        done, ctx->fmm_acc.p, fs, fx_count);
+    ctx->launch_count += 2;
+  } else {
+    l2p_p2p_kernel<NN, POLY, false><<<gp, 128, 0, ctx->stream>>>(
+        ctx->fmm_spos4.p, ctx->fmm_sf4.p, ctx->fmm_sidx.p, ctx->fmm_lstart.p, g, Lc, lo[L], scale, u4, ctx->derr,
+        done, nullptr, nullptr, 0);
+  }
   timer_end(ctx, SC_K_RPY);
   ctx->launch_count += 4 + 2 * (L - 2);
   cudaError_t e = cudaGetLastError();
@@ -1217,6 +1429,11 @@ int fmm_setup(sc_ctx* ctx) {
   SC_CUDA(cub::DeviceRadixSort::SortPairs(ctx->fmm_cubtmp.p, tmp_bytes, key_in, key_out, ctx->fmm_idx0.p,
                                           ctx->fmm_sidx.p, static_cast<int>(n), 0, 3 * L, ctx->stream));
   if (int rc = ensure(ctx, ctx->fmm_spos4, std::max<int64_t>(n, 1))) return rc;
+  if (ctx->fmm_acc.n < static_cast<size_t>(9 * std::max<int64_t>(n, 1)) || ctx->fmm_acc.p == nullptr) {
+    if (int rc = ensure(ctx, ctx->fmm_acc, 9 * std::max<int64_t>(n, 1))) return rc;
+    SC_CUDA(cudaMemsetAsync(ctx->fmm_acc.p, 0, sizeof(long long) * 9 * std::max<int64_t>(n, 1), ctx->stream));
+  }
+  if (int rc = ensure(ctx, ctx->fmm_fx, 4)) return rc;
   if (int rc = ensure(ctx, ctx->fmm_sf4, std::max<int64_t>(n, 1))) return rc;
   gather_sorted_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->fmm_sidx.p, n,
                                                                                        ctx->pos4.p, ctx->fmm_spos4.p);

@@ -144,6 +144,8 @@ struct sc_ctx {
   sc::DBuf<char> fmm_cubtmp;
   sc::DBuf<double4> fmm_spos4, fmm_sf4;
   sc::DBuf<double> fmm_M, fmm_L;
+  sc::DBuf<long long> fmm_acc;              // symmetric near field: fixed-point limbs, 9 per (sorted) body
+  sc::DBuf<unsigned long long> fmm_fx;      // ... and its scale block (FxScale)
   std::vector<int64_t> fmm_lev_off;
   sc::DBuf<int64_t> fmm_lev_off_dev;
   // compressed M2L (sc_set_fmm_compression): per level l the basis U_l (3n^3 x k_l) of the M2L
