@@ -634,41 +634,45 @@ __global__ void fmm_fx_prep_kernel(const double4* __restrict__ spos, const doubl
   }
 }
 
-// the exact RPY pair block (far branch, or the overlap branch with abar) applied to f: c1 f + c2 (d.f) d
+// The far-branch coefficients at the high-word-clamped r^2 (rpy_common.cuh) -- branch-free: a pair
+// in the overlap branch (r < 2 abar) gets a bounded far value here, which the L2P kernel swaps for
+// the overlap branch from the contacts' near list (the same arithmetic as rpy_far_clamped_contrib).
 template <bool POLY>
-__device__ __forceinline__ void near_pair_coefs(const double4& pi, const double4& pj, double a, double a2,
-                                                double ia, long long near_bits, double& dx, double& dy,
-                                                double& dz, double& c1, double& c2, bool& coincident) {
+__device__ __forceinline__ void clamped_far_coefs(const double4& pi, const double4& pj, double a2, int tau_hi,
+                                                  double& dx, double& dy, double& dz, double& c1, double& c2) {
   const double r2 = rpy_r2(pi, pj, dx, dy, dz);
-  const double ab = POLY ? pi.w + pj.w : a;
-  coincident = false;
-  if (!rpy_is_near(r2, ab, POLY, near_bits)) {
-    const double y = rsqrt_dp(r2);
-    const double h = y * y, e = y * h, ab2 = POLY ? ab * ab : a2;
-    c1 = fma(2.0 / 3.0 * ab2, e, y);
-    c2 = e * fma(-2.0 * ab2, h, 1.0);
-  } else {
-    double rs = 0.0, rr = 0.0;
-    if (r2 > 0.0) {
-      rs = rsqrt_dp(r2);
-      rr = r2 * rs;
-    } else {
-      coincident = true;
-    }
-    const double iab = POLY ? 1.0 / ab : ia;
-    c1 = (4.0 / 3.0) * iab * fma(-9.0 / 32.0 * iab, rr, 1.0);
-    c2 = 0.125 * iab * iab * rs;
+  double ab2 = a2;
+  int th = tau_hi;
+  if (POLY) {
+    const double ab = pi.w + pj.w;
+    ab2 = ab * ab;
+    th = rpy_tau_hi(ab2);
   }
+  const double r2c = rpy_clamp_r2(r2, th);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2c));
+  double h = r2c * y;
+  double e = fma(-h, y, 1.0);
+  h = fma(0.375, e, 0.5);
+  e = y * e;
+  y = fma(e, h, y);
+  h = y * y;
+  e = y * h;
+  const double sc = ab2 * h;
+  c1 = y * fma(sc, 2.0 / 3.0, 1.0);
+  c2 = e * fma(sc, -2.0, 1.0);
 }
 
-template <bool POLY>
+// TPT targets per lane (each source load and shuffle serves TPT pairs): 2 for leaves of >= 192
+// bodies on average, 1 for smaller leaves (fewer idle lanes) -- fmm_launch picks it.
+template <bool POLY, int TPT>
 __global__ void __launch_bounds__(128) p2p_sym_kernel(const double4* __restrict__ spos, const double4* __restrict__ sf,
                                                       const int32_t* __restrict__ lstart, Geom g,
                                                       long long* __restrict__ acc, FxScale* __restrict__ fs,
                                                       int64_t fx_count, int32_t* __restrict__ err,
                                                       const int32_t* __restrict__ done) {
   if (done != nullptr && *done) return;
-  constexpr int TS = 128;
+  constexpr int TS = 128, TT = TS * TPT;  // sources per chunk, targets per CTA
   __shared__ double4 sp[TS], sfs[TS];
   __shared__ double rev[4][TS][3];
   const int64_t b = blockIdx.x;
@@ -694,20 +698,28 @@ __global__ void __launch_bounds__(128) p2p_sym_kernel(const double4* __restrict_
   const int qx = bx + ox, qy = by + oy, qz = bz + oz;
   if (qx < 0 || qy < 0 || qz < 0 || qx >= D || qy >= D || qz >= D) return;  // (uniform in the CTA)
   const int64_t q = (static_cast<int64_t>(qz) * D + qy) * D + qx;
-  const int32_t i0 = lstart[b] + static_cast<int32_t>(blockIdx.z) * TS, i1 = min(lstart[b + 1], i0 + TS);
+  const int32_t i0 = lstart[b] + static_cast<int32_t>(blockIdx.z) * TT, i1 = min(lstart[b + 1], i0 + TT);
   if (i0 >= i1) return;
   const int32_t j0 = lstart[q], j1 = lstart[q + 1];
   if (j0 >= j1) return;
-  const double a = g.a, a2 = a * a, ia = 1.0 / a;
-  const long long near_bits = __double_as_longlong(4.0 * a2);
+  const double a2 = g.a * g.a;
+  const int tau_hi = rpy_tau_hi(a2);  // (monodisperse)
   const double scale = pow2(fx_shift(fs, fx_count));
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int32_t ti = i0 + threadIdx.x;  // this thread's target
-  const bool tval = ti < i1;
-  const double4 pi = tval ? spos[ti] : make_double4(1e300, 1e300, 1e300, 1.0);
-  const double4 fi = tval ? sf[ti] : make_double4(0, 0, 0, 0);
-  double ux = 0.0, uy = 0.0, uz = 0.0;
-  bool bad = false, coinc = false;
+  // targets of this lane: i0 + w 32 TPT + m 32 + lane, m < TPT
+  int32_t ti[TPT];
+  bool tval[TPT];
+  double4 pi[TPT], fi[TPT];
+  double u[TPT][3];
+#pragma unroll
+  for (int m = 0; m < TPT; ++m) {
+    ti[m] = i0 + w * 32 * TPT + m * 32 + lane;
+    tval[m] = ti[m] < i1;
+    pi[m] = tval[m] ? spos[ti[m]] : make_double4(1e300, 1e300, 1e300, 1.0);
+    fi[m] = tval[m] ? sf[ti[m]] : make_double4(0, 0, 0, 0);
+    u[m][0] = u[m][1] = u[m][2] = 0.0;
+  }
+  bool bad = false;
   for (int32_t c0 = j0; c0 < j1; c0 += TS) {
     const int cn = min(TS, j1 - c0);
     __syncthreads();
@@ -717,41 +729,43 @@ __global__ void __launch_bounds__(128) p2p_sym_kernel(const double4* __restrict_
     }
     __syncthreads();
     if (f == 0) {  // b itself: every ordered pair (i, j != i), forward only
-      if (tval)
-        for (int jj = 0; jj < cn; ++jj) {
-          if (c0 + jj == ti) continue;
+      for (int jj = 0; jj < cn; ++jj) {
+        const double4 pj = sp[jj], fj = sfs[jj];
+#pragma unroll
+        for (int m = 0; m < TPT; ++m) {
+          if (!tval[m] || c0 + jj == ti[m]) continue;
           double dx, dy, dz, c1, c2;
-          bool co;
-          near_pair_coefs<POLY>(pi, sp[jj], a, a2, ia, near_bits, dx, dy, dz, c1, c2, co);
-          coinc |= co;
-          const double4 fj = sfs[jj];
+          clamped_far_coefs<POLY>(pi[m], pj, a2, tau_hi, dx, dy, dz, c1, c2);
           const double t = c2 * fma(dz, fj.z, fma(dy, fj.y, dx * fj.x));
-          ux = fma(t, dx, fma(c1, fj.x, ux));
-          uy = fma(t, dy, fma(c1, fj.y, uy));
-          uz = fma(t, dz, fma(c1, fj.z, uz));
+          u[m][0] = fma(t, dx, fma(c1, fj.x, u[m][0]));
+          u[m][1] = fma(t, dy, fma(c1, fj.y, u[m][1]));
+          u[m][2] = fma(t, dz, fma(c1, fj.z, u[m][2]));
         }
+      }
       continue;
     }
-    // q != b: 32 x 32 rotation blocks; each warp's 32 targets against the chunk's sources
+    // q != b: 32-source rotation blocks; each warp's 32 TPT targets against the chunk's sources
     for (int sb = 0; sb * 32 < cn; ++sb) {
       double rx = 0.0, ry = 0.0, rz = 0.0;
 #pragma unroll 1
       for (int st = 0; st < 32; ++st) {
         const int jj = sb * 32 + ((lane + st) & 31);
-        if (tval && jj < cn) {
-          double dx, dy, dz, c1, c2;
-          bool co;
-          near_pair_coefs<POLY>(pi, sp[jj], a, a2, ia, near_bits, dx, dy, dz, c1, c2, co);
-          coinc |= co;
-          const double4 fj = sfs[jj];
-          const double t = c2 * fma(dz, fj.z, fma(dy, fj.y, dx * fj.x));
-          ux = fma(t, dx, fma(c1, fj.x, ux));
-          uy = fma(t, dy, fma(c1, fj.y, uy));
-          uz = fma(t, dz, fma(c1, fj.z, uz));
-          const double tr = c2 * fma(dz, fi.z, fma(dy, fi.y, dx * fi.x));  // T even in d
-          rx = fma(tr, dx, fma(c1, fi.x, rx));
-          ry = fma(tr, dy, fma(c1, fi.y, ry));
-          rz = fma(tr, dz, fma(c1, fi.z, rz));
+        if (jj < cn) {
+          const double4 pj = sp[jj], fj = sfs[jj];
+#pragma unroll
+          for (int m = 0; m < TPT; ++m) {
+            if (!tval[m]) continue;
+            double dx, dy, dz, c1, c2;
+            clamped_far_coefs<POLY>(pi[m], pj, a2, tau_hi, dx, dy, dz, c1, c2);
+            const double t = c2 * fma(dz, fj.z, fma(dy, fj.y, dx * fj.x));
+            u[m][0] = fma(t, dx, fma(c1, fj.x, u[m][0]));
+            u[m][1] = fma(t, dy, fma(c1, fj.y, u[m][1]));
+            u[m][2] = fma(t, dz, fma(c1, fj.z, u[m][2]));
+            const double tr = c2 * fma(dz, fi[m].z, fma(dy, fi[m].y, dx * fi[m].x));  // T even in d
+            rx = fma(tr, dx, fma(c1, fi[m].x, rx));
+            ry = fma(tr, dy, fma(c1, fi[m].y, ry));
+            rz = fma(tr, dz, fma(c1, fi[m].z, rz));
+          }
         }
         const int src = (lane + 1) & 31;  // next step this lane meets the source lane+1 met now
         rx = __shfl_sync(0xffffffffu, rx, src);
@@ -772,8 +786,10 @@ __global__ void __launch_bounds__(128) p2p_sym_kernel(const double4* __restrict_
       fx_red3(acc + static_cast<int64_t>(c0 + threadIdx.x) * 9, v[0], v[1], v[2], scale, bad);
     }
   }
-  if (tval) fx_red3(acc + static_cast<int64_t>(ti) * 9, ux, uy, uz, scale, bad);
-  if (coinc) atomicExch(err, 1);  // coincident centres (reading A12)
+#pragma unroll
+  for (int m = 0; m < TPT; ++m)
+    if (tval[m]) fx_red3(acc + static_cast<int64_t>(ti[m]) * 9, u[m][0], u[m][1], u[m][2], scale, bad);
+  (void)err;  // (coincident centres: flagged by the L2P kernel's near-list pass)
   if (bad) fs->bad = 1;
 }
 
@@ -787,7 +803,11 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
                                                       const double* __restrict__ Lc, int64_t loff_L, double scale,
                                                       double4* __restrict__ u4, int32_t* __restrict__ err,
                                                       const int32_t* __restrict__ done, long long* __restrict__ acc,
-                                                      FxScale* __restrict__ fs, int64_t fx_count) {
+                                                      FxScale* __restrict__ fs, int64_t fx_count,
+                                                      const double4* __restrict__ pos4o,
+                                                      const double4* __restrict__ f4o,
+                                                      const int32_t* __restrict__ near_ptr,
+                                                      const int32_t* __restrict__ near_idx) {
   if (done != nullptr && *done) return;
   constexpr int NB = NN * NN * NN;
   constexpr int TS = 128;
@@ -907,6 +927,33 @@ __global__ void __launch_bounds__(128) l2p_p2p_kernel(const double4* __restrict_
         }
 #pragma unroll
         for (int q = 0; q < 9; ++q) acc[static_cast<int64_t>(k) * 9 + q] = 0;
+        // overlapping pairs (the contacts' near list, original order): the clamped far value the
+        // symmetric near field used -> the overlap branch (r < 2 abar)
+        const int32_t o = sidx[k];
+        const double4 po = pos4o[o];
+        for (int32_t e = near_ptr[o]; e < near_ptr[o + 1]; ++e) {
+          const int32_t j = near_idx[e];
+          const double4 pj = pos4o[j];
+          const double4 fj = f4o[j];
+          double dx, dy, dz;
+          const double r2 = rpy_r2(po, pj, dx, dy, dz);
+          const double ab = POLY ? po.w + pj.w : a;
+          double rs = 0.0, rr = 0.0;
+          if (r2 > 0.0) {
+            rs = rsqrt_dp(r2);
+            rr = r2 * rs;
+          } else {
+            atomicExch(err, 1);  // coincident centres (reading A12)
+          }
+          const double iab = 1.0 / ab;
+          const double c1 = (4.0 / 3.0) * iab * fma(-9.0 / 32.0 * iab, rr, 1.0);
+          const double c2 = 0.125 * iab * iab * rs * fma(dz, fj.z, fma(dy, fj.y, dx * fj.x));
+          double fx_, fy_, fz_;
+          rpy_far_clamped_contrib(dx, dy, dz, r2, ab, fj, fx_, fy_, fz_);
+          ux += fma(c2, dx, c1 * fj.x) - fx_;
+          uy += fma(c2, dy, c1 * fj.y) - fy_;
+          uz += fma(c2, dz, c1 * fj.z) - fz_;
+        }
       }
       SC_DCHECK(sidx[k] >= 0 && sidx[k] < lstart[int64_t(1) << (3 * g.L)]);
       u4[sidx[k]] = make_double4(scale * ux, scale * uy, scale * uz, 0.0);
@@ -1250,16 +1297,24 @@ int fmm_launch(sc_ctx* ctx, const Geom& g, const double4* f4, double mu, double4
     SC_CUDA(cudaMemsetAsync(fs, 0, sizeof(FxScale), ctx->stream));
     fmm_fx_prep_kernel<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4 * 148)), 256, 0, ctx->stream>>>(
         ctx->fmm_spos4.p, ctx->fmm_sf4.p, n, fs, done);
-    p2p_sym_kernel<POLY><<<dim3(static_cast<unsigned>(nbox(L)), 14, nchunk), 128, 0, ctx->stream>>>(
-        ctx->fmm_spos4.p, ctx->fmm_sf4.p, ctx->fmm_lstart.p, g, ctx->fmm_acc.p, fs, fx_count, ctx->derr, done);
+    const int tpt = n >= 192 * nbox(L) ? 2 : 1;  // (measured: profiles/r02/fmm_p2p_sym_ab.txt)
+    const unsigned nchunk_s =
+        static_cast<unsigned>(std::max<int64_t>(1, (ctx->fmm_maxleaf + 128 * tpt - 1) / (128 * tpt)));
+    const dim3 gs(static_cast<unsigned>(nbox(L)), 14, nchunk_s);
+    if (tpt == 2)
+      p2p_sym_kernel<POLY, 2><<<gs, 128, 0, ctx->stream>>>(ctx->fmm_spos4.p, ctx->fmm_sf4.p, ctx->fmm_lstart.p, g,
+                                                            ctx->fmm_acc.p, fs, fx_count, ctx->derr, done);
+    else
+      p2p_sym_kernel<POLY, 1><<<gs, 128, 0, ctx->stream>>>(ctx->fmm_spos4.p, ctx->fmm_sf4.p, ctx->fmm_lstart.p, g,
+                                                            ctx->fmm_acc.p, fs, fx_count, ctx->derr, done);
     l2p_p2p_kernel<NN, POLY, true><<<gp, 128, 0, ctx->stream>>>(
         ctx->fmm_spos4.p, ctx->fmm_sf4.p, ctx->fmm_sidx.p, ctx->fmm_lstart.p, g, Lc, lo[L], scale, u4, ctx->derr,
-        done, ctx->fmm_acc.p, fs, fx_count);
+        done, ctx->fmm_acc.p, fs, fx_count, ctx->pos4.p, f4, ctx->near_ptr.p, ctx->near_idx.p);
     ctx->launch_count += 2;
   } else {
     l2p_p2p_kernel<NN, POLY, false><<<gp, 128, 0, ctx->stream>>>(
         ctx->fmm_spos4.p, ctx->fmm_sf4.p, ctx->fmm_sidx.p, ctx->fmm_lstart.p, g, Lc, lo[L], scale, u4, ctx->derr,
-        done, nullptr, nullptr, 0);
+        done, nullptr, nullptr, 0, nullptr, nullptr, nullptr, nullptr);
   }
   timer_end(ctx, SC_K_RPY);
   ctx->launch_count += 4 + 2 * (L - 2);
