@@ -9,9 +9,9 @@
 
 namespace sc {
 
-// Exact, order-independent accumulation of the symmetric kernel's partial sums (DESIGN.md
-// "K-RPY"): every partial sum v (a CTA's forward sum for one of its target rows, or its reverse
-// sum for one of its source rows) is rounded ONCE to the fixed-point integer X = round(v 2^s)
+// Exact, order-independent accumulation of partial sums (the symmetric RPY
+// kernel and the fast summation's symmetric near field): every partial sum v (a CTA's forward sum
+// for one of its target rows, or its reverse sum for one of its source rows) is rounded ONCE to the fixed-point integer X = round(v 2^s)
 // (|X| < 2^100 by the choice of s, fx_shift) and added with integer atomics into three int64
 // limbs per (row, component): X = x2 2^86 + x1 2^43 + x0, 0 <= x0, x1 < 2^43.  Integer addition
 // is associative, so the sums -- hence U -- are bitwise independent of the CTA schedule and of
