@@ -181,6 +181,11 @@ int sc_set_mobility_model(sc_ctx* ctx, int model);
  * order (leaf side >= 2 a_max).  Errors: SC_EINVAL (order not 4/6/8, leaf_level outside 0..8; model 2 on
  * a multi-GPU context, at the first apply). */
 int sc_set_fmm_params(sc_ctx* ctx, int order, int leaf_level);
+/* The lowest order whose stated relative L2 bar of the apply (2e-3 / 6e-5 / 3e-6 for orders
+ * 4 / 6 / 8) meets rel_err, with the automatic leaf level; order_out
+ * (nullable) receives it.  Errors: SC_EINVAL (rel_err below 3e-6 or not finite: the direct kernel
+ * is the exact operator). */
+int sc_set_fmm_tolerance(sc_ctx* ctx, double rel_err, int* order_out);
 /* Compressed M2L of the fast summation.  Per level l, the 316 M2L operators
  * K_o (3n^3 x 3n^3: the RPY far branch between the Chebyshev nodes of a box and of the box at
  * offset o) share one orthonormal basis U_l, the dominant eigenvectors of sum_o K_o K_o^T (K_o^T =

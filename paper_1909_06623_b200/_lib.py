@@ -28,7 +28,7 @@ EXPORTS = [
     "sc_set_walls", "sc_set_mobility_model", "sc_minmap_residual", "sc_set_residual_trace",
     "sc_get_residual_trace", "sc_comm_info", "sc_sym_pair_table", "sc_set_wall_velocities", "sc_get_walls",
     "sc_set_fmm_params", "sc_get_fmm_info", "sc_build_flags", "sc_set_fmm_compression",
-    "sc_get_fmm_compression_info",
+    "sc_get_fmm_compression_info", "sc_set_fmm_tolerance",
 ]
 
 
@@ -110,6 +110,7 @@ def load(build_if_missing: bool = True):
         "sc_get_fmm_info": (ci, [vp, vp]),
         "sc_set_fmm_compression": (ci, [vp, ci]),
         "sc_get_fmm_compression_info": (ci, [vp, vp]),
+        "sc_set_fmm_tolerance": (ci, [vp, C.c_double, C.POINTER(ci)]),
         "sc_apgd_solve": (ci, [vp, C.POINTER(BbpgdOpts), vp, vp, C.POINTER(BbpgdStats)]),
         "sc_time_step": (ci, [vp, C.POINTER(Problem), C.POINTER(BbpgdOpts), vp, vp, vp, vp, C.POINTER(i64),
                               C.POINTER(BbpgdStats)]),

@@ -178,6 +178,12 @@ class Context:
         fast RPY summation used with set_mobility_model("rpy_fmm")."""
         self._rc(self.lib.sc_set_fmm_params(self._h, int(order), int(leaf_level)))
 
+    def set_fmm_tolerance(self, rel_err) -> int:
+        """Pick the lowest fast-summation order whose stated error bar meets rel_err; returns it."""
+        o = C.c_int32()
+        self._rc(self.lib.sc_set_fmm_tolerance(self._h, float(rel_err), C.byref(o)))
+        return int(o.value)
+
     def set_fmm_compression(self, mode=1):
         """Compressed M2L of the fast summation (one orthonormal basis per level for its M2L
         operators, include/stokescol.h sc_set_fmm_compression): 0 / False off, 1 / True on,

@@ -663,6 +663,20 @@ int sc_set_fmm_params(sc_ctx* ctx, int order, int leaf_level) {
   return SC_OK;
 }
 
+int sc_set_fmm_tolerance(sc_ctx* ctx, double rel_err, int* order_out) {
+  if (ctx == nullptr) return SC_EINVAL;
+  // the stated relative L2 bars of the apply per order (tests/test_gpu_fmm.py)
+  int order = 0;
+  if (rel_err >= 2e-3) order = 4;
+  else if (rel_err >= 6e-5) order = 6;
+  else if (rel_err >= 3e-6) order = 8;
+  if (order == 0 || !std::isfinite(rel_err))
+    return fail(ctx, SC_EINVAL, "set_fmm_tolerance: below the order-8 bar (3e-6): use the direct RPY kernel");
+  if (int rc = sc_set_fmm_params(ctx, order, 0)) return rc;
+  if (order_out) *order_out = order;
+  return SC_OK;
+}
+
 int sc_set_fmm_compression(sc_ctx* ctx, int mode) {
   if (ctx == nullptr) return SC_EINVAL;
   if (mode < 0 || mode > 2) return fail(ctx, SC_EINVAL, "set_fmm_compression: 0 (off), 1 (on) or 2 (auto)");

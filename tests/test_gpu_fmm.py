@@ -354,3 +354,20 @@ def test_fmm_compressed_polydisperse_vs_oracle(ctx, order):
     Uo = oracle.rpy_apply(p.pos, p.radius, p.mu, FT)
     err = _relL2(U.cpu().numpy()[:, :3], Uo[:, :3])
     assert err <= TOL[order], (order, err)
+
+
+def test_fmm_tolerance_picks_order_and_meets_it(ctx):
+    assert ctx.set_fmm_tolerance(1e-2) == 4
+    assert ctx.set_fmm_tolerance(1e-4) == 6
+    assert ctx.set_fmm_tolerance(5e-6) == 8
+    with pytest.raises(ScError):
+        ctx.set_fmm_tolerance(1e-7)
+    p = make_problem("C5", n=20000)
+    ctx.build_contacts_spheres(_cuda(p.pos), _cuda(p.radius), p.gap_abs, p.gap_rel)
+    ctx.set_mobility_model("rpy_fmm")
+    assert ctx.set_fmm_tolerance(1e-4) == 6 and ctx.fmm_info()["order"] == 6
+    FT = np.random.default_rng(41).normal(size=(p.n, 6))
+    U = ctx.mobility_apply(_cuda(FT)).cpu().numpy()
+    ctx.set_mobility_model("rpy")
+    Uo = oracle.rpy_apply(p.pos, p.radius, p.mu, FT)
+    assert _relL2(U[:, :3], Uo[:, :3]) <= 1e-4
